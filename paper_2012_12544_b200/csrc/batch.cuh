@@ -1,0 +1,100 @@
+// batch.cuh -- per-batch device state shared by the kernels.
+#pragma once
+#include <stdint.h>
+
+#include "../../include/bapipe_b200.h"
+#include "common.cuh"
+
+namespace bpk {
+
+// One explore() query as the kernels see it.
+struct QDesc {
+    int32_t net, cl, N, nbase;
+    int64_t mini;
+    int64_t m_off;        // into Mpool (base micro-batch list)
+    int64_t cand_off;     // first candidate (global index)
+    int64_t stage_off;    // first bp_stage / candidate plan slot of this query
+    int64_t qstage_off;   // per-query stage arrays (DP / refined plan, F/B/W)
+    int64_t mslot_off;    // per-(query, M slot) arrays
+    int32_t schema_ok;    // host-side validation (explorer.hpp:82-83, candidate_Ms)
+    int32_t pad;
+};
+
+// Per-query device state.
+struct QState {
+    int32_t need_refine;
+    int32_t dp_shape;      // 1 = InfeasibleShape (U < N) for the whole-layer DP
+    int32_t refine_err;    // Err code of refine + refined-plan stage sums
+    int32_t refined;       // refine ran
+    int64_t target;        // max stage compute time of the DP plan (integer)
+    int64_t refine_iters;
+    // validate_plan (plan.hpp:41-85) of the refined plan, raised at simulate()
+    int32_t vcode;         // BP_IP_* or 0
+    int32_t verr;          // Err code of the coverage Rat sums
+    int64_t vwhere;
+    Rat vaux;
+    // exact simulator scaling for the refined plan
+    int64_t D;             // lcm of F/B denominators, 0 if >= 2^62
+    int64_t sumFB_D;       // sum over stages of (F+B)*D, saturated at 2^62
+};
+
+// Per (query, M slot) bottleneck analysis (partition.hpp:454-466).
+struct MState {
+    int32_t bott;          // detect_comm_bottleneck().bottleneck
+    int32_t err;           // overflow in Rat(min_bw) * target
+    int64_t a_th;
+    int64_t K;             // coarse block count
+    int32_t coarse_ok;     // coarse DP done
+    int32_t pad;
+};
+
+// Per-candidate plan kinds.
+enum { PLAN_NONE = 0, PLAN_REFINED = 1, PLAN_WHOLE = 2 };
+
+// Per-candidate device state (beyond the bp_candidate output record).
+struct CState {
+    int32_t plan_kind;
+    int32_t sim_ready;     // 1: passed estimate + memory check, needs simulate
+    int64_t D;             // simulator scale for this candidate's plan
+};
+
+// DP work item: a (query, a_th) pair; a_th < 0 = whole-layer partition.
+struct DPItem {
+    int32_t q;
+    int32_t mslot;         // -1 for the whole-layer DP
+    int64_t a_th;
+};
+
+struct BatchDev {
+    Pools P;
+    int nq;
+    int64_t ncand;
+    const QDesc* q;
+    const int64_t* Mpool;
+    QState* qs;
+    MState* ms;
+    CState* cs;
+    bp_candidate* cand;       // output records (device)
+    bp_stage* stages;         // output stages (device), null in best-only mode
+    bp_query_result* res;     // output per query (device)
+    // per-query stage arrays (qstage_off)
+    int32_t *qlo, *qhi;       // DP plan, then refined plan
+    Rat *qlead, *qtrail;
+    Rat *qF, *qB, *qW, *qT;
+    uint8_t* qdirty;
+    // per-candidate plan slots (stage_off + local*N)
+    int32_t *clo, *chi;
+    // per-candidate estimate scratch (stage_off + local*N), 6 arrays
+    Rat *sF, *sB, *sW, *sMem;
+    int64_t *sA, *sSR;
+    Rat* simbuf;              // exact simulator state, 9 Rats per stage slot
+    int32_t* cq;              // candidate -> query
+    int32_t* corder;          // ranking scratch, one slot per candidate
+    int details;              // write bp_stage records
+    // DP work lists
+    DPItem* dp_items;
+    int32_t* dp_count;        // [0] whole-layer items, [1] coarse items
+    unsigned long long* work; // instrumentation counters
+};
+
+}  // namespace bpk

@@ -1,0 +1,241 @@
+// host_prep.hpp -- host-side preparation of networks, clusters and query
+// batches (plain C++; shared by api.cu and the tests/emu harness).
+//
+//   * validation mirrors validate_network / validate_cluster / validate_pair
+//     (profiles.hpp:83-132) plus explore()'s mini-batch and candidate_Ms
+//     checks (explorer.hpp:82-83, 26-49) and resolves to a per-query flag;
+//   * K1 cost_prefix tables (prefix sums per accelerator type) are built on
+//     the host at upload time for the CPU harness and on the device
+//     (cost_prefix kernel) for the product;
+//   * the batch layout assigns each query its candidate / stage / M-slot
+//     ranges (dense, in query order, the same rule as bp_layout()).
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "batch.cuh"
+
+namespace bpk {
+
+struct HostNets {
+    std::vector<NetDesc> desc;
+    std::vector<int64_t> fp, bp, w, a, asort, Pfp, Pbp, Pc, Pw;
+    std::vector<uint8_t> type_ok;
+    int max_L = 0, max_T = 0;
+};
+
+struct HostCls {
+    std::vector<ClDesc> desc;
+    std::vector<int32_t> ctype;
+    std::vector<int64_t> cap, minm, bw;
+    int max_N = 0;
+};
+
+inline bool build_nets(const bp_network* nets, int n, HostNets& H, std::string& err, bool prefix) {
+    H = HostNets();
+    const int64_t LIM = (int64_t)1 << 62;
+    for (int i = 0; i < n; ++i) {
+        const bp_network& b = nets[i];
+        if (b.n_layers < 0 || b.n_types < 1 || (b.n_layers > 0 && (!b.fp_us || !b.bp_us || !b.weight_bytes || !b.out_act_bytes))) {
+            err = "network " + std::to_string(i) + ": bad array arguments";
+            return false;
+        }
+        NetDesc d{};
+        d.L = b.n_layers;
+        d.T = b.n_types;
+        d.off_layer = (int64_t)H.w.size();
+        d.off_typed = (int64_t)H.fp.size();
+        d.off_pref = (int64_t)H.Pw.size();
+        d.off_tpref = (int64_t)H.Pfp.size();
+        d.off_tflag = (int64_t)H.type_ok.size();
+        const int64_t L = b.n_layers;
+        bool valid = L >= 1;
+        std::vector<uint8_t> tok(b.n_types, 1);
+        for (int64_t j = 0; j < L; ++j) {
+            bool anyf = false, anyb = false;
+            for (int t = 0; t < b.n_types; ++t) {
+                int64_t f = b.fp_us[(size_t)t * L + j], bb = b.bp_us[(size_t)t * L + j];
+                if (f < 0 || bb < 0) valid = false;          // present but < 1
+                anyf |= f != 0;
+                anyb |= bb != 0;
+                if (f == 0 || bb == 0) tok[t] = 0;
+            }
+            if (!anyf || !anyb) valid = false;                // maps must be non-empty
+            if (b.weight_bytes[j] < 0 || b.out_act_bytes[j] < 0) valid = false;
+        }
+        d.valid = valid ? 1 : 0;
+        H.desc.push_back(d);
+        for (int t = 0; t < b.n_types; ++t) {
+            H.type_ok.push_back(valid ? tok[t] : 0);
+            for (int64_t j = 0; j < L; ++j) {
+                H.fp.push_back(b.fp_us[(size_t)t * L + j]);
+                H.bp.push_back(b.bp_us[(size_t)t * L + j]);
+            }
+        }
+        std::vector<int64_t> as;
+        for (int64_t j = 0; j < L; ++j) {
+            H.w.push_back(b.weight_bytes[j]);
+            H.a.push_back(b.out_act_bytes[j]);
+            if (j + 1 < L) as.push_back(b.out_act_bytes[j]);
+        }
+        std::sort(as.begin(), as.end());
+        as.resize((size_t)L, 0);
+        H.asort.insert(H.asort.end(), as.begin(), as.end());
+        // prefix sums (always on the host for the magnitude check; the
+        // device tables are rebuilt by the cost_prefix kernel)
+        int64_t sw = 0;
+        H.Pw.push_back(0);
+        for (int64_t j = 0; j < L; ++j) {
+            sw += std::max<int64_t>(b.weight_bytes[j], 0);
+            if (sw >= LIM) { err = "network " + std::to_string(i) + ": weight sum beyond 2^62"; return false; }
+            H.Pw.push_back(sw);
+        }
+        for (int t = 0; t < b.n_types; ++t) {
+            int64_t sf = 0, sb = 0;
+            H.Pfp.push_back(0);
+            H.Pbp.push_back(0);
+            H.Pc.push_back(0);
+            for (int64_t j = 0; j < L; ++j) {
+                sf += std::max<int64_t>(b.fp_us[(size_t)t * L + j], 0);
+                sb += std::max<int64_t>(b.bp_us[(size_t)t * L + j], 0);
+                if (sf + sb >= LIM) { err = "network " + std::to_string(i) + ": time sum beyond 2^62"; return false; }
+                H.Pfp.push_back(sf);
+                H.Pbp.push_back(sb);
+                H.Pc.push_back(sf + sb);
+            }
+        }
+        (void)prefix;
+        H.max_L = std::max<int>(H.max_L, (int)L);
+        H.max_T = std::max<int>(H.max_T, b.n_types);
+    }
+    return true;
+}
+
+inline bool build_clusters(const bp_cluster* cls, int n, HostCls& H, std::string& err) {
+    H = HostCls();
+    for (int i = 0; i < n; ++i) {
+        const bp_cluster& c = cls[i];
+        if (c.n_accels < 1 || !c.type_id || !c.mem_capacity || !c.min_micro || (c.n_accels > 1 && !c.link_bw) ||
+            (c.exec_mode != 0 && c.exec_mode != 1)) {
+            err = "cluster " + std::to_string(i) + ": bad arguments";
+            return false;
+        }
+        ClDesc d{};
+        d.N = c.n_accels;
+        d.mode = c.exec_mode;
+        d.off_acc = (int64_t)H.ctype.size();
+        d.off_link = (int64_t)H.bw.size();
+        d.first_bad_acc = c.n_accels;
+        d.first_bad_link = c.n_accels - 1;
+        for (int k = 0; k < c.n_accels; ++k) {
+            H.ctype.push_back(c.type_id[k]);
+            H.cap.push_back(c.mem_capacity[k]);
+            bool bad = c.mem_capacity[k] <= 0 || c.type_id[k] < 0;
+            for (int q = 0; q < 4; ++q) {
+                H.minm.push_back(c.min_micro[(size_t)k * 4 + q]);
+                if (c.min_micro[(size_t)k * 4 + q] < 1) bad = true;
+            }
+            if (bad && d.first_bad_acc == c.n_accels) d.first_bad_acc = k;
+        }
+        for (int k = 0; k + 1 < c.n_accels; ++k) {
+            H.bw.push_back(c.link_bw[k]);
+            if (c.link_bw[k] <= 0 && d.first_bad_link == c.n_accels - 1) d.first_bad_link = k;
+        }
+        H.bw.push_back(1);   // keep every cluster's link slice non-empty
+        H.desc.push_back(d);
+        H.max_N = std::max(H.max_N, c.n_accels);
+    }
+    return true;
+}
+
+struct HostBatch {
+    std::vector<QDesc> q;
+    std::vector<int64_t> Mpool;
+    std::vector<DPItem> whole_items;
+    int64_t ncand = 0, nstage = 0, nqstage = 0, nmslot = 0;
+    int max_units = 0, max_N = 0, max_nbase = 0;
+};
+
+inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const HostCls& HC, HostBatch& HB,
+                        std::string& err) {
+    HB = HostBatch();
+    HB.q.resize(nq);
+    std::unordered_map<int64_t, std::pair<int64_t, int>> divisors;   // mini -> (offset, count)
+    for (int i = 0; i < nq; ++i) {
+        const bp_query& b = qs[i];
+        if (b.network < 0 || b.network >= (int)HN.desc.size() || b.cluster < 0 || b.cluster >= (int)HC.desc.size()) {
+            err = "query " + std::to_string(i) + ": network/cluster index out of range";
+            return false;
+        }
+        const NetDesc& nd = HN.desc[b.network];
+        const ClDesc& cd = HC.desc[b.cluster];
+        int N = b.n_stages > 0 ? b.n_stages : cd.N;
+        if (N > cd.N || b.n_stages < 0) {
+            err = "query " + std::to_string(i) + ": n_stages exceeds the cluster";
+            return false;
+        }
+        QDesc& Q = HB.q[i];
+        Q = QDesc{};
+        Q.net = b.network;
+        Q.cl = b.cluster;
+        Q.N = N;
+        Q.mini = b.mini_batch;
+        bool ok = nd.valid && N <= cd.first_bad_acc && N - 1 <= cd.first_bad_link && b.mini_batch >= 1;
+        for (int k = 0; k < N && ok; ++k) {
+            int32_t t = HC.ctype[cd.off_acc + k];
+            if (t >= nd.T || !HN.type_ok[nd.off_tflag + t]) ok = false;
+        }
+        if (b.n_m > 0) {
+            if (!b.m_list) { err = "query " + std::to_string(i) + ": m_list is NULL"; return false; }
+            Q.m_off = (int64_t)HB.Mpool.size();
+            Q.nbase = b.n_m;
+            for (int k = 0; k < b.n_m; ++k) {
+                int64_t m = b.m_list[k];
+                if (m < 1 || (b.mini_batch >= 1 && b.mini_batch % m != 0)) ok = false;
+                HB.Mpool.push_back(m < 1 ? 1 : m);
+            }
+        } else if (b.mini_batch >= 1) {
+            auto it = divisors.find(b.mini_batch);
+            if (it == divisors.end()) {
+                int64_t off = (int64_t)HB.Mpool.size();
+                std::vector<int64_t> small, large;
+                for (int64_t d = 1; d * d <= b.mini_batch; ++d)
+                    if (b.mini_batch % d == 0) {
+                        small.push_back(d);
+                        if (d != b.mini_batch / d) large.push_back(b.mini_batch / d);
+                    }
+                for (auto x : small) HB.Mpool.push_back(x);
+                for (auto r = large.rbegin(); r != large.rend(); ++r) HB.Mpool.push_back(*r);
+                it = divisors.emplace(b.mini_batch, std::make_pair(off, (int)(small.size() + large.size()))).first;
+            }
+            Q.m_off = it->second.first;
+            Q.nbase = it->second.second;
+        }
+        Q.schema_ok = ok ? 1 : 0;   // nbase kept: the output layout counts the slots
+        Q.cand_off = HB.ncand;
+        Q.stage_off = HB.nstage;
+        Q.qstage_off = HB.nqstage;
+        Q.mslot_off = HB.nmslot;
+        HB.ncand += 2 * (int64_t)Q.nbase;
+        HB.nstage += 2 * (int64_t)Q.nbase * N;
+        HB.nqstage += N;
+        HB.nmslot += Q.nbase;
+        HB.max_N = std::max(HB.max_N, N);
+        HB.max_nbase = std::max(HB.max_nbase, Q.nbase);
+        if (ok && N >= 2) {
+            HB.whole_items.push_back(DPItem{i, -1, -1});
+            HB.max_units = std::max(HB.max_units, nd.L);
+        }
+    }
+    // heaviest DP instances first (load balance across thread blocks)
+    std::stable_sort(HB.whole_items.begin(), HB.whole_items.end(), [&](const DPItem& x, const DPItem& y) {
+        int64_t lx = HN.desc[HB.q[x.q].net].L, ly = HN.desc[HB.q[y.q].net].L;
+        return lx * lx > ly * ly;
+    });
+    return true;
+}
+
+}  // namespace bpk

@@ -1,0 +1,464 @@
+// model.cuh -- exact device emulation of the reference's per-candidate logic:
+//   estimate           cost_models.hpp:124-166 (+ stage_costs 103-119)
+//   validate_plan      plan.hpp:41-85
+//   memory_fine_tune   partition.hpp:339-435
+//   intra_layer_refine partition.hpp:248-333
+// Every Rat operation the reference performs on a path is performed here on
+// the same values (so overflow/domain errors match), and every layer read
+// the reference performs is bounds-checked (so its undefined behaviour is
+// reported, not silently different).  The first error wins.
+#pragma once
+#include "common.cuh"
+
+namespace bpk {
+
+// ---------------------------------------------------------------------------
+// Plan sources for estimate(): per-stage F, B, W and the stage's hi.
+struct WholePlan {          // fractions all 1 (DP / coarse / fine-tuned plans)
+    const NetView* v;
+    const ChainView* c;
+    const int32_t* lo;
+    const int32_t* hi;
+    BPK_HD int64_t H(int s) const { return hi[s]; }
+    // stage_fp_time etc. for a whole-layer stage; a non-empty stage outside
+    // [1, L] would read past net.layers (UB in the reference).
+    BPK_HD void FBW(int s, Rat& F, Rat& B, Rat& W, Err& e) const {
+        int64_t l = lo[s], h = hi[s];
+        if (l <= h && (l < 1 || h > v->L)) { e.set(ERR_UB); F = B = W = Rat{0, 1}; return; }
+        int32_t t = c->type[s];
+        F = R(stage_sum_whole(l, h, v->Pfp + (int64_t)t * (v->L + 1)));
+        B = R(stage_sum_whole(l, h, v->Pbp + (int64_t)t * (v->L + 1)));
+        W = R(stage_sum_whole(l, h, v->Pw));
+    }
+};
+
+struct CachedPlan {         // refined plan: F/B/W computed once per query
+    const int32_t* hi;
+    const Rat *F, *B, *W;
+    BPK_HD int64_t H(int s) const { return hi[s]; }
+    BPK_HD void FBW(int s, Rat& f, Rat& b, Rat& w, Err&) const {
+        f = F[s];
+        b = B[s];
+        w = W[s];
+    }
+};
+
+struct EstOut {
+    Rat minibatch, bubble, Fm, Bm;
+    int heuristic;
+    int feasible;
+    // overloads() (partition.hpp:344-356), computed after the estimate
+    Rat total_over;     // sum of max(mem - cap, 0)
+    int worst;          // first index of the maximal overload
+    Rat peak_mem;       // max_i(features_i + weights_i) (explorer.hpp:405-408)
+    Rat max_bw;         // max bandwidth demand (explorer.hpp:409-410)
+};
+
+// Optional per-stage outputs (features, weights, bw demand), may be null.
+struct EstStageOut {
+    Rat *features, *weights, *bw;
+};
+
+// Per-stage scratch of length N (caller-provided; local or global memory).
+struct EstScratch {
+    Rat *F, *B, *W, *Mem;
+    int64_t *A, *SR;
+};
+
+// minibatch_time, cost_models.hpp:50-63
+BPK_HD Rat minibatch_time(int kind, int64_t M, int64_t N, Rat F, Rat B, Rat SR, Err& e) {
+    Rat base = rat_mul(R(M + N - 1), rat_add(F, B, e), e);
+    if (kind == KIND_SNO)
+        return rat_add(base, rat_mul(rat_mul(R(N + M - 2 - ceil_div64(M - 1, N)), R(2), e), SR, e), e);
+    if (kind == KIND_SO) return rat_add(base, rat_mul(rat_mul(R(N - 1), R(2), e), SR, e), e);
+    return base;
+}
+
+// bubble_fraction, cost_models.hpp:65-82
+BPK_HD Rat bubble_fraction(int kind, int64_t M, int64_t N, Rat F, Rat B, Rat SR, Err& e) {
+    if (N == 1) return Rat{0, 1};
+    Rat total = minibatch_time(kind, M, N, F, B, SR, e);
+    if (kind == KIND_SNO) {
+        Rat inner = rat_add(rat_add(F, B, e), rat_mul(R(2), SR, e), e);
+        Rat num = rat_add(rat_mul(R(N - 1), inner, e),
+                          rat_mul(rat_mul(R(M - 1 - ceil_div64(M - 1, N)), R(2), e), SR, e), e);
+        return rat_div(num, total, e);
+    }
+    if (kind == KIND_SO) {
+        Rat inner = rat_add(rat_add(F, B, e), rat_mul(R(2), SR, e), e);
+        return rat_div(rat_mul(R(N - 1), inner, e), total, e);
+    }
+    return rat_nd(N - 1, M + N - 1, e);
+}
+
+// link_sr_time (plan.hpp:152-158) for the link after stage index k0 (0-based).
+template <class PS>
+BPK_HD int64_t link_sr(const PS& p, const NetView& v, const ChainView& c, int k0,
+                                           int64_t micro, Err& e) {
+    int64_t a = act_at(v, p.H(k0), e) * micro;
+    if (a == 0) return 0;
+    return ceil_div64(a, c.bw[k0]);
+}
+
+// estimate(kind, plan, net, cluster, M, micro), cost_models.hpp:124-166.
+template <class PS>
+BPK_HDNI void estimate(const PS& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
+                         const EstScratch& s, EstOut& o, const EstStageOut* so, Err& e) {
+    const int N = c.N;
+    // stage_costs (103-119), stage order F, B, w, a, SR
+    for (int i = 0; i < N; ++i) {
+        p.FBW(i, s.F[i], s.B[i], s.W[i], e);
+        if (e.bad()) return;
+        int64_t act = (i >= 1) ? act_at(v, p.H(i - 1), e) : act_at(v, p.H(0), e);
+        if (e.bad()) return;
+        s.A[i] = act * micro;
+        s.SR[i] = (i >= 1) ? link_sr(p, v, c, i - 1, micro, e) : 0;
+        if (e.bad()) return;
+    }
+    Rat Fm{0, 1}, Bm{0, 1};
+    int64_t SRm = 0;
+    bool balanced = true;
+    for (int i = 0; i < N; ++i) {
+        if (!rat_eq(s.F[i], s.F[0]) || !rat_eq(s.B[i], s.B[0])) balanced = false;
+        if (rat_gt(s.F[i], Fm)) Fm = s.F[i];
+        if (rat_gt(s.B[i], Bm)) Bm = s.B[i];
+        if (s.SR[i] > SRm) SRm = s.SR[i];
+    }
+    for (int i = 1; i < N; ++i)
+        if (s.SR[i] != s.SR[N > 1 ? 1 : 0]) balanced = false;
+    o.Fm = Fm;
+    o.Bm = Bm;
+    o.minibatch = minibatch_time(kind, M, N, Fm, Bm, R(SRm), e);
+    o.bubble = bubble_fraction(kind, M, N, Fm, Bm, R(SRm), e);
+    o.heuristic = (!balanced || M < N) ? 1 : 0;
+    if (e.bad()) return;
+    o.feasible = 1;
+    o.peak_mem = Rat{0, 1};
+    const bool dbl = (kind == KIND_FBP || kind == KIND_SO);
+    for (int i = 0; i < N; ++i) {
+        // features_memory (86-91), weights_memory (94), mem check (152-160)
+        Rat fm = rat_mul(R(N - i), R(s.A[i]), e);
+        if (dbl) fm = rat_mul(R(2), fm, e);
+        Rat wm = rat_mul(R(2), s.W[i], e);
+        Rat mem = rat_add(fm, wm, e);
+        if (e.bad()) return;
+        s.Mem[i] = mem;
+        if (rat_gt(mem, R(c.cap[i]))) o.feasible = 0;
+        if (so) { so->features[i] = fm; so->weights[i] = wm; }
+        if (rat_gt(mem, o.peak_mem)) o.peak_mem = mem;
+    }
+    // bandwidth_demand (97-100) per link (161-164)
+    o.max_bw = Rat{0, 1};
+    for (int k = 0; k + 1 < N; ++k) {
+        Rat a = R(act_at(v, p.H(k), e) * micro);
+        Rat d;
+        if (kind == KIND_FBP) d = rat_div(rat_mul(R(2), a, e), rat_add(Fm, Bm, e), e);
+        else d = rat_div(a, Fm, e);
+        if (e.bad()) return;
+        if (so) so->bw[k] = d;
+        if (rat_gt(d, o.max_bw)) o.max_bw = d;
+    }
+}
+
+// overloads() bookkeeping (partition.hpp:344-356) on the estimate in s.Mem:
+// ov = mem > cap ? mem - cap : 0; total += ov; worst = first max (381-383).
+// Only memory_fine_tune performs these Rat operations in the reference, so
+// only its call sites run this.
+BPK_HD void overloads_from_mem(const ChainView& c, const EstScratch& s, EstOut& o, Err& e) {
+    o.total_over = Rat{0, 1};
+    o.worst = 0;
+    Rat worst_over{0, 1};
+    for (int i = 0; i < c.N; ++i) {
+        Rat cap = R(c.cap[i]);
+        Rat ov = rat_gt(s.Mem[i], cap) ? rat_sub(s.Mem[i], cap, e) : Rat{0, 1};
+        o.total_over = rat_add(o.total_over, ov, e);
+        if (i > 0 && rat_gt(ov, worst_over)) o.worst = i;
+        if (i == 0 || rat_gt(ov, worst_over)) worst_over = ov;
+    }
+}
+
+// Note on the mem values: overloads() (partition.hpp:349) and explore()
+// (explorer.hpp:406) recompute features + weights -- identical values to the
+// estimate's own sum, hence identical overflow behaviour; computed once here.
+
+// ---------------------------------------------------------------------------
+// validate_plan (plan.hpp:41-85) for a whole-layer plan (all fractions 1).
+// Returns 0 or BP_IP_* with *where = stage (1-based) / layer.
+BPK_HD int validate_whole(const int32_t* lo, const int32_t* hi, int N, int64_t L,
+                                              int64_t* where) {
+    int64_t prev_hi = 0;
+    for (int n = 0; n < N; ++n) {
+        if (lo[n] < 1 || hi[n] > L || lo[n] > hi[n]) { *where = n + 1; return 1; }   // RANGE
+        if (n == 0) {
+            if (lo[n] != 1) { *where = 1; return 3; }                                // FIRST
+        } else {
+            bool shared = (lo[n] == prev_hi);
+            if (!shared && lo[n] != prev_hi + 1) { *where = n + 1; return 4; }      // CONTIG
+            if (shared) { *where = n + 1; return 5; }                                // SHARED_FULL (lead == 1)
+        }
+        prev_hi = hi[n];
+    }
+    if (hi[N - 1] != L) { *where = 0; return 7; }                                    // LAST
+    return 0;   // coverage of a contiguous whole plan sums to exactly 1
+}
+
+// validate_plan for a fractional (refined) plan, including the exact Rat
+// coverage sums of the reference's O(L*N) loop (78-84): only layers on a
+// stage boundary can have more than one owner; their sums are formed in
+// stage order exactly as `sum += owned_fraction(s, j)` does.
+BPK_HDNI int validate_frac(const int32_t* lo, const int32_t* hi, const Rat* lead, const Rat* trail, int N,
+                             int64_t L, int64_t* where, Rat* aux, Err& e) {
+    int64_t prev_hi = 0;
+    const Rat one{1, 1}, zero{0, 1};
+    for (int n = 0; n < N; ++n) {
+        if (lo[n] < 1 || hi[n] > L || lo[n] > hi[n]) { *where = n + 1; return 1; }
+        if (!rat_gt(lead[n], zero) || rat_gt(lead[n], one) || !rat_gt(trail[n], zero) || rat_gt(trail[n], one)) {
+            *where = n + 1;
+            return 2;
+        }
+        if (n == 0) {
+            if (lo[n] != 1 || !rat_eq(lead[n], one)) { *where = 1; return 3; }
+        } else {
+            bool shared = (lo[n] == prev_hi);
+            if (!shared && lo[n] != prev_hi + 1) { *where = n + 1; return 4; }
+            if (shared && rat_eq(lead[n], one)) { *where = n + 1; return 5; }
+            if (!shared && !rat_eq(lead[n], one)) { *where = n + 1; return 6; }
+        }
+        prev_hi = hi[n];
+    }
+    if (hi[N - 1] != L || !rat_eq(trail[N - 1], one)) { *where = 0; return 7; }
+    // coverage: walk layers in order; a layer j is owned by the run of
+    // consecutive stages whose range contains it.
+    int n = 0;
+    for (int64_t j = 1; j <= L;) {
+        while (n < N && hi[n] < j) ++n;           // first stage containing j
+        // interior layer of a single stage: owned fraction 1, sum = 1
+        if (lo[n] < j && j < hi[n]) { j = hi[n]; continue; }
+        Rat sum{0, 1};
+        for (int m = n; m < N && lo[m] <= j; ++m) {
+            if (hi[m] < j) continue;
+            Rat own;
+            if (lo[m] == hi[m]) own = rat_sub(rat_add(lead[m], trail[m], e), R(1), e);
+            else if (j == lo[m]) own = lead[m];
+            else if (j == hi[m]) own = trail[m];
+            else own = R(1);
+            sum = rat_add(sum, own, e);
+            if (e.bad()) return 0;
+        }
+        if (!rat_eq(sum, one)) { *where = j; *aux = sum; return 8; }
+        ++j;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// memory_fine_tune (partition.hpp:339-435) on a plan held in lo/hi.
+// o / s must hold the estimate of the input plan (the caller computed it with
+// the same scratch); overloads() bookkeeping is added here.  frac_lead / frac_trail (nullable) are the input plan's
+// fractions, used by the collapse step (359-373); at boundary n the loop
+// only ever compares the ORIGINAL trail[n] and lead[n+1] (each is mutated
+// only by its own boundary), so the originals suffice.
+// Returns FT_OK (plan in lo/hi, estimate of it in o/scratch) or FT_REJ /
+// FT_NOCONV; errors go to e.
+enum { FT_OK = 0, FT_REJ = 3, FT_NOCONV = 4 };
+
+BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
+                                int32_t* lo, int32_t* hi, const Rat* frac_lead, const Rat* frac_trail,
+                                const EstScratch& s, EstOut& o, Err& e) {
+    const int N = c.N;
+    overloads_from_mem(c, s, o, e);                        // first overloads() (357)
+    if (e.bad()) return FT_OK;
+    if (rat_eq(o.total_over, Rat{0, 1})) return FT_OK;   // identity
+    if (frac_lead) {
+        for (int n = 0; n < N - 1; ++n) {
+            if (hi[n] != lo[n + 1]) continue;
+            if (rat_ge(frac_trail[n], frac_lead[n + 1])) lo[n + 1] = hi[n] + 1;
+            else hi[n] = hi[n] - 1;
+        }
+    }
+    WholePlan wp{&v, &c, lo, hi};
+    estimate(wp, v, c, kind, M, micro, s, o, nullptr, e);
+    if (!e.bad()) overloads_from_mem(c, s, o, e);
+    if (e.bad()) return FT_OK;
+    Rat total = o.total_over;
+    int worst = o.worst;
+    int guard = 0;
+    const int limit = 8 * (int)((int64_t)N * v.L + 4);
+    const Rat zero{0, 1};
+    while (rat_gt(total, zero)) {
+        if (++guard > limit) return FT_NOCONV;
+        int cn[2], cd[2], nc = 0;
+        if (worst > 0) { cn[nc] = worst - 1; cd[nc] = -1; ++nc; }
+        if (worst < N - 1) { cn[nc] = worst + 1; cd[nc] = +1; ++nc; }
+        if (nc == 2) {
+            // headroom(i) = cap_i - (features_i + weights_i) on the current
+            // plan, whose estimate is the one in the scratch right now.
+            Rat hr = rat_sub(R(c.cap[worst + 1]), s.Mem[worst + 1], e);
+            Rat hl = rat_sub(R(c.cap[worst - 1]), s.Mem[worst - 1], e);
+            if (e.bad()) return FT_OK;
+            if (rat_gt(hr, hl)) {
+                int t = cn[0]; cn[0] = cn[1]; cn[1] = t;
+                t = cd[0]; cd[0] = cd[1]; cd[1] = t;
+            }
+        }
+        bool moved = false;
+        for (int relax = 0; relax < 2 && !moved; ++relax) {
+            for (int ci = 0; ci < nc; ++ci) {
+                if (lo[worst] == hi[worst]) continue;
+                int nb = cn[ci];
+                int32_t sw_lo = lo[worst], sw_hi = hi[worst], sn_lo = lo[nb], sn_hi = hi[nb];
+                if (cd[ci] < 0) { lo[worst] += 1; hi[nb] += 1; }
+                else { hi[worst] -= 1; lo[nb] -= 1; }
+                estimate(wp, v, c, kind, M, micro, s, o, nullptr, e);
+                if (!e.bad()) overloads_from_mem(c, s, o, e);
+                if (e.bad()) return FT_OK;
+                bool ok = rat_lt(o.total_over, total);
+                if (ok && !relax) {
+                    // max_stage_compute_time (plan.hpp:115-123), then
+                    // detect_comm_bottleneck (partition.hpp:228-241)
+                    Rat target{0, 1};
+                    for (int n = 0; n < N; ++n) {
+                        Rat t = rat_add(s.F[n], s.B[n], e);
+                        if (rat_gt(t, target)) target = t;
+                    }
+                    bool bott = false;
+                    for (int k = 0; k + 1 < N; ++k) {
+                        int64_t ct = link_sr(wp, v, c, k, micro, e);
+                        if (e.bad()) return FT_OK;
+                        if (rat_gt(R(ct), target)) bott = true;
+                    }
+                    ok = !bott;
+                }
+                if (ok) {
+                    total = o.total_over;
+                    worst = o.worst;
+                    moved = true;
+                    break;
+                }
+                lo[worst] = sw_lo; hi[worst] = sw_hi; lo[nb] = sn_lo; hi[nb] = sn_hi;
+            }
+        }
+        if (!moved) return FT_REJ;
+    }
+    return FT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// intra_layer_refine (partition.hpp:248-333) on one query's plan.
+// lo/hi/lead/trail: the plan (in/out).  tF/tB/tT: per-stage fp, bp and
+// compute time caches, recomputed lazily when a stage is marked dirty (the
+// reference recomputes them at every use; the values, hence the overflow
+// outcome, are the same).
+BPK_HD void stage_times(const NetView& v, const ChainView& c, int s, const int32_t* lo,
+                                            const int32_t* hi, const Rat* lead, const Rat* trail, Rat& F, Rat& B,
+                                            Err& e) {
+    int32_t t = c.type[s];
+    F = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pfp + (int64_t)t * (v.L + 1), e);
+    B = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pbp + (int64_t)t * (v.L + 1), e);
+}
+
+BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail,
+                       Rat* tF, Rat* tB, Rat* tT, uint8_t* dirty, int* iters, Err& e) {
+    const int N = c.N;
+    *iters = 0;
+    if (N <= 1) return;
+    for (int s = 0; s < N; ++s) dirty[s] = 1;
+    const Rat zero{0, 1};
+    const Rat step{1, 1024};
+    auto T = [&](int s) -> Rat {
+        if (dirty[s]) {
+            stage_times(v, c, s, lo, hi, lead, trail, tF[s], tB[s], e);
+            tT[s] = rat_add(tF[s], tB[s], e);
+            dirty[s] = 0;
+        }
+        return tT[s];
+    };
+    bool changed = true;
+    int guard = 0;
+    while (changed && ++guard < 1000) {
+        changed = false;
+        ++*iters;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int i = 0; i < N - 1; ++i) {
+                int n0 = (pass == 0) ? i : (N - 2 - i);
+                Rat t_a = T(n0);
+                if (e.bad()) return;
+                Rat t_b = T(n0 + 1);
+                if (e.bad()) return;
+                if (rat_eq(t_a, t_b)) continue;
+                int dir = rat_gt(t_a, t_b) ? +1 : -1;
+                int from = dir > 0 ? n0 : n0 + 1;
+                int to = dir > 0 ? n0 + 1 : n0;
+                int64_t j = dir > 0 ? hi[from] : lo[from];
+                bool shared = (hi[n0] == lo[n0 + 1]);
+                if (dir < 0 && !shared) {
+                    int64_t cur_cut = act_at(v, hi[n0], e);
+                    int64_t aj = act_at(v, j, e);
+                    if (e.bad()) return;
+                    if (aj > cur_cut) continue;
+                }
+                if (j < 1 || j > v.L) { e.set(ERR_UB); return; }
+                int64_t c_from = fpbp_at(v, j, c.type[from]);
+                int64_t c_to = fpbp_at(v, j, c.type[to]);
+                Rat t_hi = rat_max(t_a, t_b), t_lo = rat_min(t_a, t_b);
+                Rat x = rat_div(rat_sub(t_hi, t_lo, e), rat_add(R(c_from), R(c_to), e), e);
+                // avail = owned_fraction(from, j) (plan.hpp:33-39)
+                Rat avail;
+                if (lo[from] == hi[from]) avail = rat_sub(rat_add(lead[from], trail[from], e), R(1), e);
+                else if (j == lo[from]) avail = lead[from];
+                else avail = trail[from];
+                if (rat_ge(x, avail)) x = rat_sub(avail, step, e);
+                if (e.bad()) return;
+                if (!rat_gt(x, zero)) continue;
+                // quantize (257-265)
+                if (x.d > 1024) {
+                    Rat y = rat_mul(x, R(1024), e);
+                    if (e.bad()) return;
+                    Rat qlo = rat_nd(rat_floor(y), 1024, e);
+                    Rat qhi = rat_nd(rat_ceil(y), 1024, e);
+                    if (rat_ge(qhi, avail)) {
+                        x = qlo;
+                    } else {
+                        Rat s_lo = rat_max(rat_sub(t_hi, rat_mul(qlo, R(c_from), e), e),
+                                           rat_add(t_lo, rat_mul(qlo, R(c_to), e), e));
+                        Rat s_hi = rat_max(rat_sub(t_hi, rat_mul(qhi, R(c_from), e), e),
+                                           rat_add(t_lo, rat_mul(qhi, R(c_to), e), e));
+                        if (e.bad()) return;
+                        x = rat_le(s_lo, s_hi) ? qlo : qhi;
+                    }
+                }
+                if (!rat_gt(x, zero) || rat_ge(x, avail)) continue;
+                Rat nh = rat_sub(t_hi, rat_mul(x, R(c_from), e), e);
+                Rat nl = rat_add(t_lo, rat_mul(x, R(c_to), e), e);
+                if (e.bad()) return;
+                if (rat_ge(rat_max(nh, nl), t_hi)) continue;
+                // apply_move (269-292)
+                int a = n0, b = n0 + 1;
+                if (dir > 0) {
+                    if (shared) {
+                        trail[a] = rat_sub(trail[a], x, e);
+                        lead[b] = rat_add(lead[b], x, e);
+                    } else {
+                        trail[a] = rat_sub(R(1), x, e);
+                        lo[b] = hi[a];
+                        lead[b] = x;
+                    }
+                } else {
+                    if (shared) {
+                        lead[b] = rat_sub(lead[b], x, e);
+                        trail[a] = rat_add(trail[a], x, e);
+                    } else {
+                        lead[b] = rat_sub(R(1), x, e);
+                        hi[a] = lo[b];
+                        trail[a] = x;
+                    }
+                }
+                if (e.bad()) return;
+                dirty[a] = dirty[b] = 1;
+                changed = true;
+            }
+        }
+    }
+}
+
+}  // namespace bpk

@@ -1,0 +1,498 @@
+// phases.cuh -- per-thread bodies of the explore() pipeline kernels.
+//
+//   setup_query       K0  candidate records (explorer.hpp:87-108)
+//   bottleneck_slot   K1b detect_comm_bottleneck + a_th + coarse block count
+//                         per (query, micro-batch) (partition.hpp:454-465)
+//   refine_query      K3a intra_layer_refine once per query (partition.hpp:469)
+//                         + the refined plan's stage sums and validation
+//   prune_candidate   K3b balance_partition's branch logic, estimate, memory
+//                         fine-tune, explore's estimate (explorer.hpp:389-402)
+//   sim_exact         K4  simulate() with exact Rat events (simulator.hpp:81-246)
+//   rank_query        K5  ranking + query outcome (explorer.hpp:133-155)
+// All are __host__ __device__ so tests/emu can replay them on the CPU.
+#pragma once
+#include "batch.cuh"
+#include "model.cuh"
+
+namespace bpk {
+
+enum { C_PENDING = -1 };
+
+BPK_HD int kind_of_slot(int mode, int k) {   // feasible_kinds, explorer.hpp:17-21
+    return mode == MODE_ASYNC ? (k == 0 ? KIND_AS : KIND_FBP) : (k == 0 ? KIND_SNO : KIND_SO);
+}
+
+BPK_HD int status_of_err(uint32_t code) { return (int)code; }   // ERR_* == BP_C_*
+
+// ---------------------------------------------------------------- K0
+BPK_HDNI void setup_query(const BatchDev& B, int qi) {
+    const QDesc Q = B.q[qi];
+    QState& qs = B.qs[qi];
+    qs = QState{};
+    bp_query_result& r = B.res[qi];
+    r = bp_query_result{};
+    r.best = -1;
+    r.first_error = -1;
+    if (!Q.schema_ok) {
+        r.status = BP_Q_SCHEMA;
+        return;
+    }
+    ChainView c = chain_view(B.P, Q.cl, Q.N);
+    r.n_candidates = 2 * Q.nbase;
+    for (int k = 0; k < 2; ++k) {
+        int kind = kind_of_slot(c.mode, k);
+        int64_t min_micro = 1;   // candidate_Ms, explorer.hpp:42-47
+        for (int a = 0; a < Q.N; ++a) {
+            int64_t mm = c.minm[4 * a + kind];
+            if (mm > min_micro) min_micro = mm;
+        }
+        for (int m = 0; m < Q.nbase; ++m) {
+            int64_t local = (int64_t)k * Q.nbase + m;
+            int64_t ci = Q.cand_off + local;
+            bp_candidate cd = bp_candidate{};
+            cd.kind = kind;
+            cd.M = B.Mpool[Q.m_off + m];
+            cd.micro = Q.mini / cd.M;
+            cd.rank = -1;
+            cd.n_stages = Q.N;
+            cd.status = (Q.mini / cd.M >= min_micro) ? C_PENDING : BP_C_REJ_MIN_MICRO;
+            B.cand[ci] = cd;
+            B.cs[ci] = CState{};
+            B.cq[ci] = qi;
+        }
+    }
+    for (int m = 0; m < Q.nbase; ++m) B.ms[Q.mslot_off + m] = MState{};
+}
+
+// ---------------------------------------------------------------- K1b
+// Returns 1 when a coarse DP item must be queued for (qi, m).
+BPK_HDNI int bottleneck_slot(const BatchDev& B, int qi, int m) {
+    const QDesc Q = B.q[qi];
+    if (!Q.schema_ok || Q.N == 1 || m >= Q.nbase) return 0;
+    QState& qs = B.qs[qi];
+    if (qs.dp_shape) return 0;
+    bool alive = B.cand[Q.cand_off + m].status == C_PENDING ||
+                 B.cand[Q.cand_off + Q.nbase + m].status == C_PENDING;
+    if (!alive) return 0;
+    NetView v = net_view(B.P, Q.net);
+    ChainView c = chain_view(B.P, Q.cl, Q.N);
+    const int64_t micro = Q.mini / B.Mpool[Q.m_off + m];
+    const int64_t target = qs.target;
+    const int32_t* hi = B.qhi + Q.qstage_off;
+    MState& ms = B.ms[Q.mslot_off + m];
+    bool bott = false;
+    for (int k = 0; k + 1 < Q.N; ++k) {           // detect_comm_bottleneck (228-241)
+        int64_t a = v.a[hi[k] - 1] * micro;
+        int64_t sr = a == 0 ? 0 : ceil_div64(a, c.bw[k]);
+        if (sr > target) bott = true;
+    }
+    ms.bott = bott ? 1 : 0;
+    if (!bott) {
+        qs.need_refine = 1;
+        return 0;
+    }
+    int64_t min_bw = c.bw[0];
+    for (int k = 1; k + 1 < Q.N; ++k)
+        if (c.bw[k] < min_bw) min_bw = c.bw[k];
+    // a_th = (Rat(min_bw) * target / Rat(micro)).floor()  (460)
+    i128 prod = (i128)min_bw * target;
+    if (prod > (i128)INT64_MAX) { ms.err = ERR_OVERFLOW; return 0; }
+    int64_t a_th = (int64_t)prod / micro;
+    ms.a_th = a_th;
+    // coarsen_by_comm block count: layers j < L with a_j <= a_th, plus L
+    const int64_t n_sorted = v.L - 1;
+    int64_t lo = 0, hi2 = n_sorted;                 // upper_bound in asort
+    while (lo < hi2) {
+        int64_t mid = (lo + hi2) >> 1;
+        if (v.asort[mid] <= a_th) lo = mid + 1;
+        else hi2 = mid;
+    }
+    ms.K = lo + 1;
+    return ms.K >= Q.N ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- K3a
+// lcm accumulation for the simulator scale; returns 0 once above 2^62.
+BPK_HD int64_t lcm_sat(int64_t D, int64_t d) {
+    if (D == 0) return 0;
+    uint64_t g = gcd_u64((uint64_t)D, (uint64_t)d);
+    u128 l = (u128)(D / (int64_t)g) * (u128)d;
+    if (l >= ((u128)1 << 62)) return 0;
+    return (int64_t)l;
+}
+
+BPK_HDNI void refine_query(const BatchDev& B, int qi) {
+    const QDesc Q = B.q[qi];
+    QState& qs = B.qs[qi];
+    if (!Q.schema_ok || !qs.need_refine || qs.dp_shape || Q.N < 2) return;
+    NetView v = net_view(B.P, Q.net);
+    ChainView c = chain_view(B.P, Q.cl, Q.N);
+    const int64_t o = Q.qstage_off;
+    int32_t* lo = B.qlo + o;
+    int32_t* hi = B.qhi + o;
+    Rat* lead = B.qlead + o;
+    Rat* trail = B.qtrail + o;
+    for (int s = 0; s < Q.N; ++s) { lead[s] = R(1); trail[s] = R(1); }
+    Err e{ERR_NONE};
+    int iters = 0;
+    refine(v, c, lo, hi, lead, trail, B.qF + o, B.qB + o, B.qT + o, B.qdirty + o, &iters, e);
+    qs.refined = 1;
+    qs.refine_iters = iters;
+    // The refined plan's stage sums in estimate's order (stage_costs 103-119).
+    int64_t D = 1;
+    u128 sumFB = 0;
+    for (int s = 0; s < Q.N && !e.bad(); ++s) {
+        int32_t t = c.type[s];
+        Rat F = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pfp + (int64_t)t * (v.L + 1), e);
+        Rat Bt = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pbp + (int64_t)t * (v.L + 1), e);
+        Rat W = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pw, e);
+        B.qF[o + s] = F;
+        B.qB[o + s] = Bt;
+        B.qW[o + s] = W;
+        D = lcm_sat(lcm_sat(D, F.d), Bt.d);
+    }
+    qs.refine_err = e.code;
+    if (e.bad()) return;
+    qs.D = D;
+    if (D) {
+        for (int s = 0; s < Q.N; ++s) {
+            sumFB += (u128)((i128)B.qF[o + s].n * (D / B.qF[o + s].d));
+            sumFB += (u128)((i128)B.qB[o + s].n * (D / B.qB[o + s].d));
+        }
+        qs.sumFB_D = sumFB >= ((u128)1 << 62) ? -1 : (int64_t)sumFB;
+    }
+    // validate_plan of the refined plan (raised only when simulate() runs)
+    Err ve{ERR_NONE};
+    int64_t where = 0;
+    Rat aux{0, 1};
+    qs.vcode = validate_frac(lo, hi, lead, trail, Q.N, v.L, &where, &aux, ve);
+    qs.verr = ve.code;
+    qs.vwhere = where;
+    qs.vaux = aux;
+}
+
+// ---------------------------------------------------------------- K3b
+BPK_HD EstScratch cand_scratch(const BatchDev& B, int64_t slot) {
+    EstScratch s;
+    s.F = B.sF + slot;
+    s.B = B.sB + slot;
+    s.W = B.sW + slot;
+    s.Mem = B.sMem + slot;
+    s.A = B.sA + slot;
+    s.SR = B.sSR + slot;
+    return s;
+}
+
+BPK_HD void fail(bp_candidate& cd, const Err& e) { cd.status = status_of_err(e.code); }
+
+BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci) {
+    bp_candidate& cd = B.cand[ci];
+    if (cd.status != C_PENDING) return;
+    const int qi = B.cq[ci];
+    const QDesc Q = B.q[qi];
+    const QState& qs = B.qs[qi];
+    const int64_t local = ci - Q.cand_off;
+    const int m = (int)(local % Q.nbase);
+    const int N = Q.N;
+    const int kind = cd.kind;
+    const int64_t M = cd.M, micro = cd.micro;
+    NetView v = net_view(B.P, Q.net);
+    ChainView c = chain_view(B.P, Q.cl, N);
+    const int64_t slot = Q.stage_off + local * N;
+    int32_t* lo = B.clo + slot;
+    int32_t* hi = B.chi + slot;
+    EstScratch S = cand_scratch(B, slot);
+    CState& cs = B.cs[ci];
+    Err e{ERR_NONE};
+    EstOut o;
+    int plan_kind = PLAN_WHOLE;
+    int ft = FT_OK;
+    if (N == 1) {                                                  // 447-451
+        lo[0] = 1;
+        hi[0] = (int32_t)v.L;
+        WholePlan wp{&v, &c, lo, hi};
+        estimate(wp, v, c, kind, M, micro, S, o, nullptr, e);
+        if (!e.bad()) ft = memory_fine_tune(v, c, kind, M, micro, lo, hi, nullptr, nullptr, S, o, e);
+    } else if (qs.dp_shape) {                                      // 115-117
+        cd.status = BP_C_REJ_SHAPE;
+        cd.detail = v.L;
+        return;
+    } else {
+        const MState ms = B.ms[Q.mslot_off + m];
+        if (ms.bott) {                                             // 456-467
+            if (ms.err) { cd.status = status_of_err(ms.err); return; }
+            if (ms.K < N) { cd.status = BP_C_REJ_COARSEN; cd.detail = ms.K; return; }
+            WholePlan wp{&v, &c, lo, hi};
+            estimate(wp, v, c, kind, M, micro, S, o, nullptr, e);
+            if (!e.bad()) ft = memory_fine_tune(v, c, kind, M, micro, lo, hi, nullptr, nullptr, S, o, e);
+        } else {                                                   // 469-473
+            if (qs.refine_err) { cd.status = status_of_err(qs.refine_err); return; }
+            const int64_t qo = Q.qstage_off;
+            CachedPlan cp{B.qhi + qo, B.qF + qo, B.qB + qo, B.qW + qo};
+            estimate(cp, v, c, kind, M, micro, S, o, nullptr, e);
+            if (!e.bad() && !o.feasible) {
+                for (int s = 0; s < N; ++s) { lo[s] = B.qlo[qo + s]; hi[s] = B.qhi[qo + s]; }
+                ft = memory_fine_tune(v, c, kind, M, micro, lo, hi, B.qlead + qo, B.qtrail + qo, S, o, e);
+            } else {
+                plan_kind = PLAN_REFINED;
+            }
+        }
+    }
+    if (e.bad()) { fail(cd, e); return; }
+    if (ft == FT_REJ) { cd.status = BP_C_REJ_FINETUNE; return; }
+    if (ft == FT_NOCONV) { cd.status = BP_C_REJ_FINETUNE_NOCONV; return; }
+    // explore's estimate on the final plan (explorer.hpp:398-402)
+    bp_stage* st = B.details ? B.stages + slot : nullptr;
+    if (plan_kind == PLAN_REFINED) {
+        const int64_t qo = Q.qstage_off;
+        CachedPlan cp{B.qhi + qo, B.qF + qo, B.qB + qo, B.qW + qo};
+        estimate(cp, v, c, kind, M, micro, S, o, nullptr, e);
+    } else {
+        WholePlan wp{&v, &c, lo, hi};
+        estimate(wp, v, c, kind, M, micro, S, o, nullptr, e);
+    }
+    if (e.bad()) { fail(cd, e); return; }
+    if (!o.feasible) { cd.status = BP_C_REJ_MEM_POST; return; }
+    cd.est_minibatch = bp_rat{o.minibatch.n, o.minibatch.d};
+    cd.bubble = bp_rat{o.bubble.n, o.bubble.d};
+    cd.heuristic = o.heuristic;
+    cd.peak_memory = bp_rat{o.peak_mem.n, o.peak_mem.d};
+    cd.max_bw_demand = bp_rat{o.max_bw.n, o.max_bw.d};
+    cd.plan_fractional = 0;
+    cs.plan_kind = plan_kind;
+    cs.sim_ready = 1;
+    if (st || plan_kind == PLAN_REFINED) {
+        const int64_t qo = Q.qstage_off;
+        const bool dbl = (kind == KIND_FBP || kind == KIND_SO);
+        for (int s = 0; s < N; ++s) {
+            Rat ld = plan_kind == PLAN_REFINED ? B.qlead[qo + s] : R(1);
+            Rat tr = plan_kind == PLAN_REFINED ? B.qtrail[qo + s] : R(1);
+            if (ld.n != ld.d || tr.n != tr.d) cd.plan_fractional = 1;
+            if (!st) continue;
+            st[s].lo = plan_kind == PLAN_REFINED ? B.qlo[qo + s] : lo[s];
+            st[s].hi = plan_kind == PLAN_REFINED ? B.qhi[qo + s] : hi[s];
+            st[s].lead = bp_rat{ld.n, ld.d};
+            st[s].trail = bp_rat{tr.n, tr.d};
+            // features / weights exactly as estimate formed them (no new ops)
+            Err dummy{ERR_NONE};
+            Rat fm = rat_mul(R(N - s), R(S.A[s]), dummy);
+            if (dbl) fm = rat_mul(R(2), fm, dummy);
+            Rat wm = rat_mul(R(2), S.W[s], dummy);
+            st[s].features = bp_rat{fm.n, fm.d};
+            st[s].weights = bp_rat{wm.n, wm.d};
+            if (s + 1 < N) {
+                // bandwidth_demand of link s: the cut activation = A[s+1]
+                Rat d = (kind == KIND_FBP) ? rat_div(rat_mul(R(2), R(S.A[s + 1]), dummy), rat_add(o.Fm, o.Bm, dummy), dummy)
+                                           : rat_div(R(S.A[s + 1]), o.Fm, dummy);
+                st[s].bw_demand = bp_rat{d.n, d.d};
+            } else {
+                st[s].bw_demand = bp_rat{0, 1};
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- K4 (exact)
+// simulate(): validate_plan, chain_instance, simulate_chain with exact Rat
+// values for every event.  Ops are visited position by position: all F ops
+// at a position in ascending stage order, then all B ops in descending stage
+// order -- a topological order of the reference's sorted op list
+// (simulator.hpp:107-125), so every value equals the reference's.
+// Per link a 4-slot ring keyed by micro-batch carries arrivals.
+struct StageOp {
+    int is_f;
+    int64_t m;
+};
+
+BPK_HD StageOp op_at(int64_t p, int64_t w, int64_t M) {
+    if (p < w) return StageOp{1, p + 1};
+    int64_t r = p - w;
+    if (r < 2 * (M - w)) {
+        if ((r & 1) == 0) return StageOp{0, r / 2 + 1};
+        return StageOp{1, w + (r + 1) / 2};
+    }
+    return StageOp{0, (M - w) + (r - 2 * (M - w)) + 1};
+}
+
+BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci) {
+    const CState& cs = B.cs[ci];
+    if (!cs.sim_ready) return;
+    bp_candidate& cd = B.cand[ci];
+    const int qi = B.cq[ci];
+    const QDesc Q = B.q[qi];
+    const QState& qs = B.qs[qi];
+    const int64_t local = ci - Q.cand_off;
+    const int N = Q.N;
+    const int kind = cd.kind;
+    const int64_t M = cd.M, micro = cd.micro;
+    NetView v = net_view(B.P, Q.net);
+    ChainView c = chain_view(B.P, Q.cl, N);
+    const int64_t slot = Q.stage_off + local * N;
+    const int64_t qo = Q.qstage_off;
+    const int32_t* hi = cs.plan_kind == PLAN_REFINED ? B.qhi + qo : B.chi + slot;
+    // validate_plan (plan.hpp:41-85)
+    if (cs.plan_kind == PLAN_REFINED) {
+        if (qs.vcode) {
+            cd.status = BP_C_ERR_INVALID_PLAN;
+            cd.detail = qs.vcode;
+            cd.detail2 = qs.vwhere;
+            cd.aux = bp_rat{qs.vaux.n, qs.vaux.d};
+            return;
+        }
+        if (qs.verr) { cd.status = status_of_err(qs.verr); return; }
+    } else {
+        int64_t where = 0;
+        int vc = validate_whole(B.clo + slot, B.chi + slot, N, v.L, &where);
+        if (vc) {
+            cd.status = BP_C_ERR_INVALID_PLAN;
+            cd.detail = vc;
+            cd.detail2 = where;
+            return;
+        }
+    }
+    Err e{ERR_NONE};
+    // chain_instance (simulator.hpp:248-262): F, B per stage; SR per link.
+    Rat* F = B.sF + slot;
+    Rat* Bd = B.sB + slot;
+    int64_t* SR = B.sSR + slot;
+    int64_t* A = B.sA + slot;
+    for (int s = 0; s < N; ++s) {
+        if (cs.plan_kind == PLAN_REFINED) { F[s] = B.qF[qo + s]; Bd[s] = B.qB[qo + s]; }
+        else {
+            int32_t t = c.type[s];
+            F[s] = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pfp + (int64_t)t * (v.L + 1)));
+            Bd[s] = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pbp + (int64_t)t * (v.L + 1)));
+        }
+        A[s] = (s >= 1 ? v.a[hi[s - 1] - 1] : v.a[hi[0] - 1]) * micro;
+        if (s + 1 < N) {
+            int64_t a = v.a[hi[s] - 1] * micro;
+            SR[s] = a == 0 ? 0 : ceil_div64(a, c.bw[s]);
+        }
+    }
+    const bool async = kind_async(kind);
+    Rat* fr = B.simbuf + 9 * slot;     // free[N]
+    Rat* rf = fr + N;                  // ringF[N][4]: arrivals on link s -> s+1
+    Rat* rb = rf + 4 * N;              // ringB[N][4]: arrivals on link s+1 -> s
+    for (int s = 0; s < N; ++s) fr[s] = Rat{0, 1};
+    for (int64_t p = 0; p < 2 * M && !e.bad(); ++p) {
+        for (int s = 0; s < N; ++s) {
+            int64_t w = warmup_depth(kind, N, s + 1);
+            if (w > M) w = M;
+            StageOp op = op_at(p, w, M);
+            if (!op.is_f) continue;
+            Rat ready = fr[s];
+            if (s > 0) {
+                Rat arr = rf[4 * (s - 1) + (op.m & 3)];
+                if (rat_gt(arr, ready)) ready = arr;
+            }
+            Rat end = rat_add(ready, F[s], e);
+            fr[s] = end;
+            if (s + 1 < N) rf[4 * s + (op.m & 3)] = async ? end : rat_add(end, R(SR[s]), e);
+        }
+        for (int s = N - 1; s >= 0; --s) {
+            int64_t w = warmup_depth(kind, N, s + 1);
+            if (w > M) w = M;
+            StageOp op = op_at(p, w, M);
+            if (op.is_f) continue;
+            Rat ready = fr[s];   // >= endF(m, s): F(m, s) ran earlier on this stage
+            if (s + 1 < N) {
+                Rat arr = rb[4 * s + (op.m & 3)];
+                if (rat_gt(arr, ready)) ready = arr;
+            }
+            Rat end = rat_add(ready, Bd[s], e);
+            fr[s] = end;
+            if (s > 0) rb[4 * (s - 1) + (op.m & 3)] = async ? end : rat_add(end, R(SR[s - 1]), e);
+        }
+    }
+    if (e.bad()) { fail(cd, e); return; }
+    Rat mk{0, 1};
+    for (int s = 0; s < N; ++s)
+        if (rat_gt(fr[s], mk)) mk = fr[s];
+    // feature high-water = min(M, depth) * a (simulator.hpp:219-238): the
+    // in-flight count on a 1F1B stage peaks right after its warm-up.
+    for (int s = 0; s < N; ++s) {
+        int64_t w = warmup_depth(kind, N, s + 1);
+        if (w > M) w = M;
+        if ((i128)w * A[s] > (i128)INT64_MAX) { e.set(ERR_OVERFLOW); break; }
+    }
+    // link busy fraction Rat(M * SR) / makespan (239-244)
+    for (int k = 0; k + 1 < N && !e.bad(); ++k)
+        if (!rat_eq(mk, Rat{0, 1})) (void)rat_div(R(M * SR[k]), mk, e);
+    if (e.bad()) { fail(cd, e); return; }
+    cd.makespan = bp_rat{mk.n, mk.d};
+    cd.status = BP_C_OK;
+}
+
+// ---------------------------------------------------------------- K5
+BPK_HD bool cand_less(const bp_candidate& a, const bp_candidate& b) {   // explorer.hpp:142-152
+    Rat am{a.makespan.num, a.makespan.den}, bm{b.makespan.num, b.makespan.den};
+    if (!rat_eq(am, bm)) return rat_lt(am, bm);
+    Rat ap{a.peak_memory.num, a.peak_memory.den}, bpm{b.peak_memory.num, b.peak_memory.den};
+    if (!rat_eq(ap, bpm)) return rat_lt(ap, bpm);
+    Rat aw{a.max_bw_demand.num, a.max_bw_demand.den}, bw{b.max_bw_demand.num, b.max_bw_demand.den};
+    if (!rat_eq(aw, bw)) return rat_lt(aw, bw);
+    if (a.M != b.M) return a.M < b.M;
+    return a.kind < b.kind;
+}
+
+BPK_HD bool escaping(int st) {
+    return st == BP_C_ERR_OVERFLOW || st == BP_C_ERR_INVALID_PLAN || st == BP_C_ERR_DOMAIN || st == BP_C_REF_UB;
+}
+
+BPK_HD int q_status_of(int st) {
+    return st == BP_C_ERR_OVERFLOW ? BP_Q_OVERFLOW
+           : st == BP_C_ERR_INVALID_PLAN ? BP_Q_INVALID_PLAN
+           : st == BP_C_ERR_DOMAIN ? BP_Q_DOMAIN
+                                    : BP_Q_REF_UB;
+}
+
+BPK_HDNI void rank_query(const BatchDev& B, int qi) {
+    const QDesc Q = B.q[qi];
+    bp_query_result& r = B.res[qi];
+    if (!Q.schema_ok) return;
+    int32_t* order = B.corder + Q.cand_off;
+    const int nc = 2 * Q.nbase;
+    bp_candidate* cand = B.cand + Q.cand_off;
+    int nr = 0;
+    for (int i = 0; i < nc; ++i) {
+        int st = cand[i].status;
+        if (st != BP_C_OK) {
+            // a candidate that failed after its estimate (simulate) carries
+            // no values, like the reference's rejected/aborted candidates
+            bp_candidate& cd = cand[i];
+            cd.heuristic = 0;
+            cd.plan_fractional = 0;
+            cd.makespan = cd.est_minibatch = cd.bubble = cd.peak_memory = cd.max_bw_demand = bp_rat{0, 0};
+            if (B.details && B.cs[Q.cand_off + i].sim_ready) {
+                bp_stage* stg = B.stages + Q.stage_off + (int64_t)i * Q.N;
+                for (int s = 0; s < Q.N; ++s) stg[s] = bp_stage{};
+            }
+        }
+        if (escaping(st) && r.first_error < 0) {
+            r.first_error = i;
+            r.status = q_status_of(st);
+        }
+        if (st == BP_C_OK) {
+            // stable insertion by the 5 keys
+            int k = nr - 1;
+            while (k >= 0 && cand_less(cand[i], cand[order[k]])) { order[k + 1] = order[k]; --k; }
+            order[k + 1] = i;
+            ++nr;
+        }
+    }
+    if (r.first_error >= 0) return;
+    if (nr == 0) { r.status = BP_Q_NO_FEASIBLE; return; }
+    for (int i = 0; i < nr; ++i) cand[order[i]].rank = i;
+    const bp_candidate& b = cand[order[0]];
+    r.status = BP_Q_OK;
+    r.n_ranked = nr;
+    r.best = order[0];
+    r.best_kind = b.kind;
+    r.best_M = b.M;
+    r.best_micro = b.micro;
+    r.best_makespan = b.makespan;
+    r.best_peak_memory = b.peak_memory;
+    r.best_max_bw = b.max_bw_demand;
+}
+
+}  // namespace bpk

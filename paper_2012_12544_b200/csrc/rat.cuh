@@ -1,0 +1,203 @@
+// rat.cuh -- exact rationals on the device with bapipe::Rat semantics.
+//
+// bapipe::Rat (rational.hpp:14-110) stores a reduced int64 num/den (den > 0);
+// every + - * / computes the exact 128-bit result, reduces it by the gcd, and
+// throws std::overflow_error when the REDUCED value does not fit int64
+// (from128, lines 83-95).  Only values matter for results, and the overflow
+// predicate depends only on the reduced value, so any exact algorithm that
+// produces the same reduced value reproduces the reference bit for bit.  We
+// use the classic gcd-splitting forms (Knuth 4.5.1) so the common cases need
+// one 64-bit binary gcd and no 128-bit division.
+//
+// Errors do not throw: the first error is latched into an Err word and the
+// caller stops at its next check (exception emulation, first-error-wins).
+#pragma once
+#include <stdint.h>
+
+// The emulation code is __host__ __device__ so tests/emu can run it on the
+// CPU against the oracle; the product runs it only inside the kernels.
+#ifdef __CUDACC__
+#define BPK_HD __host__ __device__ __forceinline__
+#define BPK_HDNI __host__ __device__ __noinline__
+#else
+#define BPK_HD inline
+#define BPK_HDNI inline
+static inline int __ffsll(long long x) { return __builtin_ffsll(x); }
+#endif
+
+namespace bpk {
+
+typedef __int128 i128;
+typedef unsigned __int128 u128;
+
+// Candidate-level error codes (map 1:1 onto BP_C_* in bapipe_b200.h).
+enum : uint32_t {
+    ERR_NONE = 0,
+    ERR_OVERFLOW = 7,      // BP_C_ERR_OVERFLOW
+    ERR_INVALID_PLAN = 8,  // BP_C_ERR_INVALID_PLAN
+    ERR_DOMAIN = 9,        // BP_C_ERR_DOMAIN
+    ERR_UB = 10            // BP_C_REF_UB
+};
+
+struct Err {
+    uint32_t code;
+    BPK_HD void set(uint32_t c) {
+        if (code == ERR_NONE) code = c;
+    }
+    BPK_HD bool bad() const { return code != ERR_NONE; }
+};
+
+struct Rat {
+    int64_t n, d;
+};
+
+BPK_HD Rat R(int64_t v) { return Rat{v, 1}; }
+
+// ---- gcd ---------------------------------------------------------------
+BPK_HD uint64_t gcd_u64(uint64_t u, uint64_t v) {
+    if (u == 0) return v;
+    if (v == 0) return u;
+    int shift = __ffsll((long long)(u | v)) - 1;
+    u >>= (__ffsll((long long)u) - 1);
+    do {
+        v >>= (__ffsll((long long)v) - 1);
+        if (u > v) { uint64_t t = u; u = v; v = t; }
+        v -= u;
+    } while (v != 0);
+    return u << shift;
+}
+
+BPK_HD int ctz128(u128 x) {
+    uint64_t lo = (uint64_t)x;
+    if (lo) return __ffsll((long long)lo) - 1;
+    return 64 + __ffsll((long long)(uint64_t)(x >> 64)) - 1;
+}
+
+BPK_HDNI u128 gcd_u128(u128 u, u128 v) {
+    if (u == 0) return v;
+    if (v == 0) return u;
+    if ((u >> 64) == 0 && (v >> 64) == 0) return gcd_u64((uint64_t)u, (uint64_t)v);
+    int shift = ctz128(u | v);
+    u >>= ctz128(u);
+    do {
+        v >>= ctz128(v);
+        if (u > v) { u128 t = u; u = v; v = t; }
+        v -= u;
+        if ((u >> 64) == 0 && (v >> 64) == 0) {
+            u = gcd_u64((uint64_t)u, (uint64_t)v);
+            v = 0;
+        }
+    } while (v != 0);
+    return u << shift;
+}
+
+BPK_HD u128 uabs128(i128 x) { return x < 0 ? (u128)(-x) : (u128)x; }
+
+// from128 (rational.hpp:83-95): reduce an exact 128-bit fraction, check fit.
+BPK_HDNI Rat from128(i128 n, i128 d, Err& e) {
+    if (d == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
+    if (d < 0) { n = -n; d = -d; }
+    u128 g = gcd_u128(uabs128(n), (u128)d);
+    if (g > 1) { n /= (i128)g; d /= (i128)g; }
+    if (n > (i128)INT64_MAX || n < (i128)INT64_MIN || d > (i128)INT64_MAX) {
+        e.set(ERR_OVERFLOW);
+        return Rat{0, 1};
+    }
+    return Rat{(int64_t)n, (int64_t)d};
+}
+
+// A 128-bit value already known to be reduced: only the range check.
+BPK_HD Rat fit128(i128 n, i128 d, Err& e) {
+    if (n > (i128)INT64_MAX || n < (i128)INT64_MIN || d > (i128)INT64_MAX) {
+        e.set(ERR_OVERFLOW);
+        return Rat{0, 1};
+    }
+    return Rat{(int64_t)n, (int64_t)d};
+}
+
+BPK_HD uint64_t uabs64(int64_t x) {
+    return x < 0 ? (uint64_t)0 - (uint64_t)x : (uint64_t)x;
+}
+
+// Rat(n, d) constructor -> normalize() (rational.hpp:18, 100-106).
+BPK_HD Rat rat_nd(int64_t n, int64_t d, Err& e) {
+    if (d == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
+    if (d < 0) { n = -n; d = -d; }
+    uint64_t g = gcd_u64(uabs64(n), (uint64_t)d);
+    if (g > 1) { n /= (int64_t)g; d /= (int64_t)g; }
+    return Rat{n, d};
+}
+
+// a + s*b with s = +1 / -1 (operator+ / operator-).
+BPK_HD Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
+    i128 bn = s > 0 ? (i128)b.n : -(i128)b.n;
+    if (a.d == 1 && b.d == 1) return fit128((i128)a.n + bn, 1, e);
+    if (a.d == 1) return fit128((i128)a.n * b.d + bn, b.d, e);        // gcd(num, b.d) = 1
+    if (b.d == 1) return fit128((i128)bn * a.d + a.n, a.d, e);
+    uint64_t g = gcd_u64((uint64_t)a.d, (uint64_t)b.d);
+    if (g == 1) return fit128((i128)a.n * b.d + bn * a.d, (i128)a.d * b.d, e);
+    int64_t ad = a.d / (int64_t)g, bd = b.d / (int64_t)g;
+    i128 t = (i128)a.n * bd + bn * ad;
+    if (t == 0) return Rat{0, 1};
+    // g2 = gcd(t, g): reduce t mod g first (g < 2^63)
+    i128 tm = t % (i128)g;
+    uint64_t g2 = gcd_u64(uabs128(tm) > 0 ? (uint64_t)uabs128(tm) : 0, g);
+    if (g2 == 0) g2 = g;  // t divisible by g
+    i128 num = t / (i128)g2;
+    i128 den = (i128)ad * (i128)(b.d / (int64_t)g2);
+    return fit128(num, den, e);
+}
+
+BPK_HD Rat operator_add(Rat a, Rat b, Err& e) { return rat_addsub(a, b, +1, e); }
+
+BPK_HD Rat rat_add(Rat a, Rat b, Err& e) { return rat_addsub(a, b, +1, e); }
+BPK_HD Rat rat_sub(Rat a, Rat b, Err& e) { return rat_addsub(a, b, -1, e); }
+
+// operator* (rational.hpp:33-35).
+BPK_HD Rat rat_mul(Rat a, Rat b, Err& e) {
+    if (a.n == 0 || b.n == 0) return Rat{0, 1};
+    if (a.d == 1 && b.d == 1) return fit128((i128)a.n * b.n, 1, e);
+    uint64_t g1 = (b.d == 1) ? 1 : gcd_u64(uabs64(a.n), (uint64_t)b.d);
+    uint64_t g2 = (a.d == 1) ? 1 : gcd_u64(uabs64(b.n), (uint64_t)a.d);
+    int64_t an = g1 > 1 ? a.n / (int64_t)g1 : a.n;
+    int64_t bd = g1 > 1 ? b.d / (int64_t)g1 : b.d;
+    int64_t bn = g2 > 1 ? b.n / (int64_t)g2 : b.n;
+    int64_t ad = g2 > 1 ? a.d / (int64_t)g2 : a.d;
+    return fit128((i128)an * bn, (i128)ad * bd, e);
+}
+
+// operator/ (rational.hpp:36-39): b == 0 -> domain_error.
+BPK_HD Rat rat_div(Rat a, Rat b, Err& e) {
+    if (b.n == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
+    // a / b = a * (b.d / b.n); keep the sign on the numerator.
+    if (b.n == INT64_MIN) return from128((i128)a.n * b.d, (i128)a.d * b.n, e);
+    Rat inv = b.n < 0 ? Rat{-b.d, -b.n} : Rat{b.d, b.n};
+    return rat_mul(a, inv, e);
+}
+
+// Comparisons cross-multiply in 128 bits and never throw (lines 47-56).
+BPK_HD bool rat_eq(Rat a, Rat b) { return a.n == b.n && a.d == b.d; }
+BPK_HD bool rat_lt(Rat a, Rat b) {
+    if (a.d == b.d) return a.n < b.n;
+    return (i128)a.n * b.d < (i128)b.n * a.d;
+}
+BPK_HD bool rat_gt(Rat a, Rat b) { return rat_lt(b, a); }
+BPK_HD bool rat_le(Rat a, Rat b) { return !rat_lt(b, a); }
+BPK_HD bool rat_ge(Rat a, Rat b) { return !rat_lt(a, b); }
+BPK_HD Rat rat_max(Rat a, Rat b) { return rat_lt(a, b) ? b : a; }   // std::max
+BPK_HD Rat rat_min(Rat a, Rat b) { return rat_lt(b, a) ? b : a; }   // std::min
+
+BPK_HD int64_t rat_floor(Rat a) {   // 59-63
+    int64_t q = a.n / a.d;
+    if (a.n % a.d != 0 && a.n < 0) --q;
+    return q;
+}
+BPK_HD int64_t rat_ceil(Rat a) {    // 64-68
+    int64_t q = a.n / a.d;
+    if (a.n % a.d != 0 && a.n > 0) ++q;
+    return q;
+}
+
+BPK_HD int64_t ceil_div64(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace bpk

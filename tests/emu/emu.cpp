@@ -1,0 +1,235 @@
+// tests/emu/emu.cpp -- TEST HARNESS (never the product): runs the product's
+// per-thread phase code (csrc/phases.cuh, compiled for the host) on the CPU,
+// with a sequential mirror of the k_partition DP, behind the oracle-style
+// batch entry point.  It lets tests/test_emu.py check the exact-emulation
+// logic against the reference without a GPU; the product itself only ever
+// runs these phases inside CUDA kernels (libbapipe_b200.so).
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../paper_2012_12544_b200/csrc/host_prep.hpp"
+#include "../../paper_2012_12544_b200/csrc/phases.cuh"
+
+using namespace bpk;
+
+namespace {
+
+const int64_t INF = INT64_MAX / 4;
+
+// Sequential mirror of k_partition (csrc/dp.cu): same windows, same order.
+void host_partition(const BatchDev& B, const DPItem& item, uint64_t& work) {
+    const QDesc Q = B.q[item.q];
+    NetView v = net_view(B.P, Q.net);
+    ChainView c = chain_view(B.P, Q.cl, Q.N);
+    const int N = Q.N;
+    const int64_t L = v.L;
+    std::vector<int32_t> pos;
+    pos.push_back(0);
+    for (int64_t j = 1; j <= L; ++j)
+        if (item.a_th < 0 || j == L || v.a[j - 1] <= item.a_th) pos.push_back((int32_t)j);
+    const int U = (int)pos.size() - 1;
+    if (U < N) {
+        if (item.a_th < 0) B.qs[item.q].dp_shape = 1;
+        return;
+    }
+    std::vector<int64_t> C((size_t)v.T * (U + 1)), W(U + 1), A(U + 1);
+    for (int t = 0; t < v.T; ++t)
+        for (int j = 0; j <= U; ++j) C[(size_t)t * (U + 1) + j] = v.Pc[(int64_t)t * (L + 1) + pos[j]];
+    for (int j = 0; j <= U; ++j) {
+        W[j] = v.Pw[pos[j]];
+        A[j] = j >= 1 ? v.a[pos[j] - 1] : 0;
+    }
+    auto Cn = [&](int n) { return &C[(size_t)c.type[n - 1] * (U + 1)]; };
+    int64_t T_ub = 0;
+    for (int n = 1; n <= N; ++n) {
+        int64_t k = ((int64_t)(n - 1) * U) / N, j = ((int64_t)n * U) / N;
+        T_ub = std::max(T_ub, Cn(n)[j] - Cn(n)[k]);
+    }
+    std::vector<int64_t> prev(U + 1), cur(U + 1);
+    for (int j = 0; j <= U; ++j) prev[j] = j == 0 ? 0 : INF;
+    for (int n = 1; n <= N; ++n) {
+        const int64_t* Cc = Cn(n);
+        for (int j = 0; j <= U; ++j) {
+            int64_t best = INF;
+            if (j >= n && j <= U - (N - n)) {
+                for (int k = j - 1; k >= n - 1; --k) {
+                    int64_t s = Cc[j] - Cc[k];
+                    if (s > T_ub || s >= best) break;
+                    best = std::min(best, std::max(prev[k], s));
+                    ++work;
+                }
+                if (best > T_ub) best = INF;
+            }
+            cur[j] = best;
+        }
+        std::swap(prev, cur);
+    }
+    const int64_t T_opt = prev[U];
+    for (int j = 0; j <= U; ++j) prev[j] = j == 0 ? 0 : INF;
+    for (int n = 1; n <= N; ++n) {
+        const int64_t* Cc = Cn(n);
+        const int64_t cN = N - n + 1;
+        for (int j = 0; j <= U; ++j) {
+            int64_t best = INF;
+            if (j >= n && j <= U - (N - n)) {
+                for (int k = j - 1; k >= n - 1; --k) {
+                    if (Cc[j] - Cc[k] > T_opt) break;
+                    int64_t w2 = 2 * (W[j] - W[k]);
+                    if (w2 >= best) break;
+                    ++work;
+                    if (prev[k] == INF) continue;
+                    int64_t foot = w2 + cN * (k >= 1 ? A[k] : A[j]);
+                    best = std::min(best, std::max(prev[k], foot));
+                }
+            }
+            cur[j] = best;
+        }
+        std::swap(prev, cur);
+    }
+    const int64_t F_opt = prev[U];
+    std::vector<std::vector<char>> feas(N + 1, std::vector<char>(U + 1, 0));
+    feas[N][U] = 1;
+    for (int n = N - 1; n >= 0; --n) {
+        const int64_t* Cc = Cn(n + 1);
+        const int64_t cN = N - n;
+        for (int j = n; j <= U; ++j) {
+            for (int j2 = j + 1; j2 <= U; ++j2) {
+                if (Cc[j2] - Cc[j] > T_opt) break;
+                ++work;
+                int64_t foot = 2 * (W[j2] - W[j]) + cN * (j >= 1 ? A[j] : A[j2]);
+                if (foot > F_opt) {
+                    if (j >= 1) break;
+                    continue;
+                }
+                if (feas[n + 1][j2]) { feas[n][j] = 1; break; }
+            }
+        }
+    }
+    int curj = 0;
+    int64_t target = 0;
+    for (int n = 1; n <= N; ++n) {
+        const int64_t* Cc = Cn(n);
+        const int64_t cN = N - n + 1;
+        int chosen = -1;
+        for (int j = curj + 1; j <= U; ++j) {
+            if (Cc[j] - Cc[curj] > T_opt) break;
+            int64_t foot = 2 * (W[j] - W[curj]) + cN * (curj >= 1 ? A[curj] : A[j]);
+            if (foot > F_opt) continue;
+            if (feas[n][j]) { chosen = j; break; }
+        }
+        if (chosen < 0) {
+            if (item.a_th < 0) B.qs[item.q].target = -1;
+            return;
+        }
+        target = std::max(target, Cc[chosen] - Cc[curj]);
+        if (item.a_th < 0) {
+            B.qlo[Q.qstage_off + n - 1] = pos[curj] + 1;
+            B.qhi[Q.qstage_off + n - 1] = pos[chosen];
+        } else {
+            for (int k = 0; k < 2; ++k) {
+                int64_t o = Q.stage_off + ((int64_t)k * Q.nbase + item.mslot) * N + (n - 1);
+                B.clo[o] = pos[curj] + 1;
+                B.chi[o] = pos[chosen];
+            }
+        }
+        curj = chosen;
+    }
+    if (item.a_th < 0) B.qs[item.q].target = target;
+    else B.ms[Q.mslot_off + item.mslot].coarse_ok = 1;
+}
+
+template <class T>
+T* vec(std::vector<T>& v, size_t n) {
+    v.assign(n ? n : 1, T{});
+    return v.data();
+}
+
+}  // namespace
+
+extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_cluster* cls, int n_cls,
+                                   const bp_query* qs, int nq, bp_query_result* res, bp_candidate* cand,
+                                   bp_stage* stages, uint64_t* dp_work) {
+    std::string err;
+    HostNets HN;
+    HostCls HC;
+    HostBatch HB;
+    if (!build_nets(nets, n_nets, HN, err, true) || !build_clusters(cls, n_cls, HC, err) ||
+        !build_batch(qs, nq, HN, HC, HB, err))
+        return BP_BAD_INPUT;
+    for (int i = 0; i < nq; ++i)
+        if (qs[i].cand_offset != HB.q[i].cand_off || qs[i].stage_offset != HB.q[i].stage_off) return BP_BAD_INPUT;
+    BatchDev B{};
+    B.P.nets = HN.desc.data();
+    B.P.cls = HC.desc.data();
+    B.P.fp = HN.fp.data();
+    B.P.bp = HN.bp.data();
+    B.P.w = HN.w.data();
+    B.P.a = HN.a.data();
+    B.P.asort = HN.asort.data();
+    B.P.Pfp = HN.Pfp.data();
+    B.P.Pbp = HN.Pbp.data();
+    B.P.Pc = HN.Pc.data();
+    B.P.Pw = HN.Pw.data();
+    B.P.type_ok = HN.type_ok.data();
+    B.P.ctype = HC.ctype.data();
+    B.P.cap = HC.cap.data();
+    B.P.minm = HC.minm.data();
+    B.P.bw = HC.bw.data();
+    B.nq = nq;
+    B.ncand = HB.ncand;
+    B.q = HB.q.data();
+    B.Mpool = HB.Mpool.data();
+    std::vector<QState> vqs;
+    std::vector<MState> vms;
+    std::vector<CState> vcs;
+    std::vector<bp_candidate> vcand;
+    std::vector<bp_stage> vst;
+    std::vector<bp_query_result> vres;
+    std::vector<int32_t> vqlo, vqhi, vclo, vchi, vcq, vco;
+    std::vector<Rat> vql, vqt, vqF, vqB, vqW, vqT, vsF, vsB, vsW, vsM, vsim;
+    std::vector<uint8_t> vqd;
+    std::vector<int64_t> vsA, vsSR;
+    B.qs = vec(vqs, nq);
+    B.ms = vec(vms, HB.nmslot);
+    B.cs = vec(vcs, HB.ncand);
+    B.cand = vec(vcand, HB.ncand);
+    B.details = stages != nullptr;
+    B.stages = stages ? vec(vst, HB.nstage) : nullptr;
+    B.res = vec(vres, nq);
+    B.qlo = vec(vqlo, HB.nqstage);
+    B.qhi = vec(vqhi, HB.nqstage);
+    B.qlead = vec(vql, HB.nqstage);
+    B.qtrail = vec(vqt, HB.nqstage);
+    B.qF = vec(vqF, HB.nqstage);
+    B.qB = vec(vqB, HB.nqstage);
+    B.qW = vec(vqW, HB.nqstage);
+    B.qT = vec(vqT, HB.nqstage);
+    B.qdirty = vec(vqd, HB.nqstage);
+    B.clo = vec(vclo, HB.nstage);
+    B.chi = vec(vchi, HB.nstage);
+    B.sF = vec(vsF, HB.nstage);
+    B.sB = vec(vsB, HB.nstage);
+    B.sW = vec(vsW, HB.nstage);
+    B.sMem = vec(vsM, HB.nstage);
+    B.sA = vec(vsA, HB.nstage);
+    B.sSR = vec(vsSR, HB.nstage);
+    B.simbuf = vec(vsim, 9 * HB.nstage);
+    B.cq = vec(vcq, HB.ncand);
+    B.corder = vec(vco, HB.ncand);
+    uint64_t work = 0;
+    for (int i = 0; i < nq; ++i) setup_query(B, i);
+    for (const DPItem& it : HB.whole_items) host_partition(B, it, work);
+    for (int i = 0; i < nq; ++i)
+        for (int m = 0; m < HB.q[i].nbase; ++m)
+            if (bottleneck_slot(B, i, m)) host_partition(B, DPItem{i, m, B.ms[HB.q[i].mslot_off + m].a_th}, work);
+    for (int i = 0; i < nq; ++i) refine_query(B, i);
+    for (int64_t c = 0; c < HB.ncand; ++c) prune_candidate(B, c);
+    for (int64_t c = 0; c < HB.ncand; ++c) sim_exact(B, c);
+    for (int i = 0; i < nq; ++i) rank_query(B, i);
+    std::memcpy(res, B.res, sizeof(bp_query_result) * (size_t)nq);
+    if (cand) std::memcpy(cand, B.cand, sizeof(bp_candidate) * (size_t)HB.ncand);
+    if (stages) std::memcpy(stages, B.stages, sizeof(bp_stage) * (size_t)HB.nstage);
+    if (dp_work) *dp_work = work;
+    return BP_OK;
+}
