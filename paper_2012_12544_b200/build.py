@@ -1,0 +1,89 @@
+"""Build the product library (sm_100a) and the test-only checkers.
+
+    python -m paper_2012_12544_b200.build          # product + oracles
+
+The product is one shared library, paper_2012_12544_b200/libbapipe_b200.so,
+compiled with nvcc for `-gencode arch=compute_100a,code=sm_100a` (B200 only)
+with the system g++ as host compiler (dynamic libstdc++; see oracle/Makefile
+for why the /opt/gcc wrapper is avoided).
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+CSRC = os.path.join(HERE, "csrc")
+SO = os.path.join(HERE, "libbapipe_b200.so")
+SOURCES = ["api.cu", "kernels.cu", "dp.cu"]
+HEADERS = ["rat.cuh", "common.cuh", "model.cuh", "batch.cuh", "phases.cuh", "kernels.h", "host_prep.hpp"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nvcc():
+    for c in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if c and os.path.exists(c):
+            return c
+    raise RuntimeError("nvcc not found")
+
+
+def _host_cxx():
+    return "/usr/bin/g++" if os.path.exists("/usr/bin/g++") else (shutil.which("g++") or "g++")
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+
+
+def build_product(force=False, verbose=False):
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "bapipe_b200.h")]
+    if not force and not _stale(SO, deps):
+        return SO
+    objs = []
+    jobs = []
+    os.makedirs(os.path.join(CSRC, "_obj"), exist_ok=True)
+    for src in SOURCES:
+        obj = os.path.join(CSRC, "_obj", src.replace(".cu", ".o"))
+        objs.append(obj)
+        cmd = [_nvcc(), *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-ccbin", _host_cxx(),
+               "-I" + os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        jobs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True))
+    for j in jobs:
+        out, _ = j.communicate()
+        if verbose or j.returncode:
+            sys.stdout.write(out)
+        if j.returncode:
+            raise RuntimeError("nvcc failed")
+    tmp = SO + ".tmp"
+    subprocess.run([_nvcc(), *ARCH, "-shared", "-ccbin", _host_cxx(), "-o", tmp, *objs], check=True)
+    os.replace(tmp, SO)
+    return SO
+
+
+def build_oracles():
+    """Test-only checkers: the C restatement always, oracle/_ref when the
+    reference sources are present (dev container only)."""
+    targets = ["oracle"]
+    if os.path.isdir("/root/reference/proj/include"):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")] + targets, check=True)
+    emu = os.path.join(ROOT, "tests", "emu")
+    if os.path.isdir(emu):
+        sys.path.insert(0, emu)
+        import pyemu  # noqa: E402
+        if _stale(pyemu.SO, [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(emu, "emu.cpp")]):
+            pyemu.build()
+
+
+if __name__ == "__main__":
+    build_product(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build_oracles()
+    print(SO)

@@ -1,0 +1,607 @@
+// api.cu -- host implementation of the C ABI in include/bapipe_b200.h.
+//
+// The boundary replaces bapipe::explore (explorer.hpp:80-155) for batches of
+// queries.  Host work is limited to validation and layout (host_prep.hpp);
+// every candidate evaluation runs in the sm_100a kernels (kernels.cu, dp.cu).
+// There is no CPU fallback: without a usable device, bp_create returns NULL.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "host_prep.hpp"
+#include "kernels.h"
+
+using namespace bpk;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    bool ensure(size_t bytes) {
+        if (bytes <= cap) return true;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) return false;
+        cap = bytes;
+        return true;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct HostPinned {
+    void* p = nullptr;
+    size_t cap = 0;
+    bool ensure(size_t bytes) {
+        if (bytes <= cap) return true;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) return false;
+        cap = bytes;
+        return true;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+struct KStat {
+    double ms = 0;
+    int64_t launches = 0;
+    double work = 0;
+};
+
+// Bump layout of one contiguous allocation.
+struct Layout {
+    size_t off = 0;
+    template <class T>
+    size_t take(size_t n) {
+        size_t o = off;
+        off += ((n * sizeof(T)) + 255) & ~(size_t)255;
+        return o;
+    }
+};
+
+}  // namespace
+
+struct bp_batch {
+    HostBatch hb;
+    BatchDev dev{};
+    DevBuf mem;
+    HostPinned stage_in;
+    size_t in_off = 0, in_bytes = 0;
+    size_t cand_off = 0, stage_off = 0, res_off = 0;
+    bool details = false;
+    int nq = 0;
+    int dp_grid = 0, dp_max_units = 0;
+};
+
+struct bp_ctx {
+    int device = 0;
+    int sm_count = 148;
+    std::string err;
+    int64_t launches = 0;
+    HostNets hn;
+    HostCls hc;
+    bool have_nets = false, have_cls = false;
+    DevBuf nets_mem, cls_mem;
+    Pools P{};
+    int max_T = 1;
+    bool prof = false;
+    std::map<std::string, KStat> stats;
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> event_pool;
+    bp_batch* cached = nullptr;
+};
+
+namespace {
+
+int fail(bp_ctx* c, int code, const std::string& msg) {
+    if (c) c->err = msg;
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(bp_ctx* c, cudaError_t e, const char* where) {
+    return fail(c, BP_CUDA_ERROR, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+cudaEvent_t get_event(bp_ctx* c) {
+    if (!c->event_pool.empty()) {
+        cudaEvent_t e = c->event_pool.back();
+        c->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launch wrapper: counts launches, brackets them with events when profiling.
+template <class F>
+void timed(bp_ctx* c, const char* name, cudaStream_t st, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (c->prof) {
+        a = get_event(c);
+        b = get_event(c);
+        cudaEventRecord(a, st);
+    }
+    f();
+    ++c->launches;
+    if (c->prof) {
+        cudaEventRecord(b, st);
+        c->pending.push_back({name, {a, b}});
+    }
+}
+
+void collect(bp_ctx* c) {
+    for (auto& p : c->pending) {
+        float ms = 0;
+        cudaEventSynchronize(p.second.second);
+        cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+        KStat& k = c->stats[p.first];
+        k.ms += ms;
+        k.launches += 1;
+        c->event_pool.push_back(p.second.first);
+        c->event_pool.push_back(p.second.second);
+    }
+    c->pending.clear();
+}
+
+template <class T>
+T* dptr(void* base, size_t off) {
+    return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + off);
+}
+
+int upload_networks(bp_ctx* c) {
+    HostNets& H = c->hn;
+    Layout L;
+    size_t o_desc = L.take<NetDesc>(H.desc.size());
+    size_t o_fp = L.take<int64_t>(H.fp.size());
+    size_t o_bp = L.take<int64_t>(H.bp.size());
+    size_t o_w = L.take<int64_t>(H.w.size());
+    size_t o_a = L.take<int64_t>(H.a.size());
+    size_t o_as = L.take<int64_t>(H.asort.size());
+    size_t o_Pfp = L.take<int64_t>(H.Pfp.size());
+    size_t o_Pbp = L.take<int64_t>(H.Pbp.size());
+    size_t o_Pc = L.take<int64_t>(H.Pc.size());
+    size_t o_Pw = L.take<int64_t>(H.Pw.size());
+    size_t o_tok = L.take<uint8_t>(H.type_ok.size());
+    if (!c->nets_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(networks)");
+    void* b = c->nets_mem.p;
+    auto up = [&](size_t off, const void* src, size_t bytes) {
+        return bytes ? cudaMemcpy(dptr<char>(b, off), src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(NetDesc));
+    if (e == cudaSuccess) e = up(o_fp, H.fp.data(), H.fp.size() * 8);
+    if (e == cudaSuccess) e = up(o_bp, H.bp.data(), H.bp.size() * 8);
+    if (e == cudaSuccess) e = up(o_w, H.w.data(), H.w.size() * 8);
+    if (e == cudaSuccess) e = up(o_a, H.a.data(), H.a.size() * 8);
+    if (e == cudaSuccess) e = up(o_as, H.asort.data(), H.asort.size() * 8);
+    if (e == cudaSuccess) e = up(o_tok, H.type_ok.data(), H.type_ok.size());
+    if (e != cudaSuccess) return cuda_fail(c, e, "upload networks");
+    Pools& P = c->P;
+    P.nets = dptr<NetDesc>(b, o_desc);
+    P.fp = dptr<int64_t>(b, o_fp);
+    P.bp = dptr<int64_t>(b, o_bp);
+    P.w = dptr<int64_t>(b, o_w);
+    P.a = dptr<int64_t>(b, o_a);
+    P.asort = dptr<int64_t>(b, o_as);
+    P.Pfp = dptr<int64_t>(b, o_Pfp);
+    P.Pbp = dptr<int64_t>(b, o_Pbp);
+    P.Pc = dptr<int64_t>(b, o_Pc);
+    P.Pw = dptr<int64_t>(b, o_Pw);
+    P.type_ok = dptr<uint8_t>(b, o_tok);
+    c->max_T = std::max(1, H.max_T);
+    // K1 cost_prefix on the device
+    if (!H.desc.empty()) {
+        timed(c, "cost_prefix", 0, [&] {
+            launch_cost_prefix(P.nets, (int)H.desc.size(), P.fp, P.bp, P.w, const_cast<int64_t*>(P.Pfp),
+                               const_cast<int64_t*>(P.Pbp), const_cast<int64_t*>(P.Pc), const_cast<int64_t*>(P.Pw),
+                               0, c->max_T);
+        });
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) return cuda_fail(c, e, "cost_prefix");
+        collect(c);
+    }
+    return BP_OK;
+}
+
+int upload_clusters(bp_ctx* c) {
+    HostCls& H = c->hc;
+    Layout L;
+    size_t o_desc = L.take<ClDesc>(H.desc.size());
+    size_t o_t = L.take<int32_t>(H.ctype.size());
+    size_t o_cap = L.take<int64_t>(H.cap.size());
+    size_t o_mm = L.take<int64_t>(H.minm.size());
+    size_t o_bw = L.take<int64_t>(H.bw.size());
+    if (!c->cls_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(clusters)");
+    void* b = c->cls_mem.p;
+    auto up = [&](size_t off, const void* src, size_t bytes) {
+        return bytes ? cudaMemcpy(dptr<char>(b, off), src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    cudaError_t e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(ClDesc));
+    if (e == cudaSuccess) e = up(o_t, H.ctype.data(), H.ctype.size() * 4);
+    if (e == cudaSuccess) e = up(o_cap, H.cap.data(), H.cap.size() * 8);
+    if (e == cudaSuccess) e = up(o_mm, H.minm.data(), H.minm.size() * 8);
+    if (e == cudaSuccess) e = up(o_bw, H.bw.data(), H.bw.size() * 8);
+    if (e != cudaSuccess) return cuda_fail(c, e, "upload clusters");
+    c->P.cls = dptr<ClDesc>(b, o_desc);
+    c->P.ctype = dptr<int32_t>(b, o_t);
+    c->P.cap = dptr<int64_t>(b, o_cap);
+    c->P.minm = dptr<int64_t>(b, o_mm);
+    c->P.bw = dptr<int64_t>(b, o_bw);
+    return BP_OK;
+}
+
+// Host prep + device layout + H2D of the batch's inputs (on stream st).
+int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cudaStream_t st) {
+    if (!c->have_nets || !c->have_cls) return fail(c, BP_BAD_INPUT, "networks/clusters not set");
+    std::string err;
+    if (!build_batch(q, nq, c->hn, c->hc, B->hb, err)) return fail(c, BP_BAD_INPUT, err);
+    const HostBatch& hb = B->hb;
+    for (int i = 0; i < nq; ++i)
+        if (q[i].cand_offset != hb.q[i].cand_off || q[i].stage_offset != hb.q[i].stage_off)
+            return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
+    B->nq = nq;
+    B->details = details != 0;
+    const size_t nqs = (size_t)nq, nc = (size_t)hb.ncand, ns = (size_t)hb.nstage, nqst = (size_t)hb.nqstage,
+                 nms = (size_t)hb.nmslot;
+    Layout L;
+    // inputs (one H2D copy): QDesc, Mpool, DP items, dp_count
+    size_t o_q = L.take<QDesc>(nqs);
+    size_t o_M = L.take<int64_t>(hb.Mpool.size());
+    size_t o_items = L.take<DPItem>(nqs + nms);
+    size_t o_cnt = L.take<int32_t>(4);
+    size_t in_end = L.off;
+    // outputs
+    size_t o_res = L.take<bp_query_result>(nqs);
+    size_t o_cand = L.take<bp_candidate>(nc);
+    size_t o_st = L.take<bp_stage>(details ? ns : 0);
+    // state
+    size_t o_qs = L.take<QState>(nqs), o_ms = L.take<MState>(nms), o_cs = L.take<CState>(nc);
+    size_t o_qlo = L.take<int32_t>(nqst), o_qhi = L.take<int32_t>(nqst);
+    size_t o_ql = L.take<Rat>(nqst), o_qt = L.take<Rat>(nqst), o_qF = L.take<Rat>(nqst), o_qB = L.take<Rat>(nqst),
+           o_qW = L.take<Rat>(nqst), o_qT = L.take<Rat>(nqst);
+    size_t o_qd = L.take<uint8_t>(nqst);
+    size_t o_clo = L.take<int32_t>(ns), o_chi = L.take<int32_t>(ns);
+    size_t o_sF = L.take<Rat>(ns), o_sB = L.take<Rat>(ns), o_sW = L.take<Rat>(ns), o_sM = L.take<Rat>(ns);
+    size_t o_sA = L.take<int64_t>(ns), o_sSR = L.take<int64_t>(ns);
+    size_t o_sim = L.take<Rat>(9 * ns);
+    size_t o_cq = L.take<int32_t>(nc), o_co = L.take<int32_t>(nc);
+    size_t o_work = L.take<unsigned long long>(8);
+    if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
+    void* b = B->mem.p;
+    // stage the inputs in pinned memory and copy once
+    if (!B->stage_in.ensure(in_end)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc");
+    char* h = (char*)B->stage_in.p;
+    std::memcpy(h + o_q, hb.q.data(), nqs * sizeof(QDesc));
+    if (!hb.Mpool.empty()) std::memcpy(h + o_M, hb.Mpool.data(), hb.Mpool.size() * 8);
+    if (!hb.whole_items.empty()) std::memcpy(h + o_items, hb.whole_items.data(), hb.whole_items.size() * sizeof(DPItem));
+    int32_t cnt[4] = {(int32_t)hb.whole_items.size(), 0, 0, 0};
+    std::memcpy(h + o_cnt, cnt, sizeof(cnt));
+    B->in_off = 0;
+    B->in_bytes = in_end;
+    B->res_off = o_res;
+    B->cand_off = o_cand;
+    B->stage_off = o_st;
+    BatchDev& D = B->dev;
+    D = BatchDev{};
+    D.P = c->P;
+    D.nq = nq;
+    D.ncand = hb.ncand;
+    D.q = dptr<QDesc>(b, o_q);
+    D.Mpool = dptr<int64_t>(b, o_M);
+    D.qs = dptr<QState>(b, o_qs);
+    D.ms = dptr<MState>(b, o_ms);
+    D.cs = dptr<CState>(b, o_cs);
+    D.cand = dptr<bp_candidate>(b, o_cand);
+    D.stages = details ? dptr<bp_stage>(b, o_st) : nullptr;
+    D.res = dptr<bp_query_result>(b, o_res);
+    D.qlo = dptr<int32_t>(b, o_qlo);
+    D.qhi = dptr<int32_t>(b, o_qhi);
+    D.qlead = dptr<Rat>(b, o_ql);
+    D.qtrail = dptr<Rat>(b, o_qt);
+    D.qF = dptr<Rat>(b, o_qF);
+    D.qB = dptr<Rat>(b, o_qB);
+    D.qW = dptr<Rat>(b, o_qW);
+    D.qT = dptr<Rat>(b, o_qT);
+    D.qdirty = dptr<uint8_t>(b, o_qd);
+    D.clo = dptr<int32_t>(b, o_clo);
+    D.chi = dptr<int32_t>(b, o_chi);
+    D.sF = dptr<Rat>(b, o_sF);
+    D.sB = dptr<Rat>(b, o_sB);
+    D.sW = dptr<Rat>(b, o_sW);
+    D.sMem = dptr<Rat>(b, o_sM);
+    D.sA = dptr<int64_t>(b, o_sA);
+    D.sSR = dptr<int64_t>(b, o_sSR);
+    D.simbuf = dptr<Rat>(b, o_sim);
+    D.cq = dptr<int32_t>(b, o_cq);
+    D.corder = dptr<int32_t>(b, o_co);
+    D.dp_items = dptr<DPItem>(b, o_items);
+    D.dp_count = dptr<int32_t>(b, o_cnt);
+    D.work = dptr<unsigned long long>(b, o_work);
+    D.details = details ? 1 : 0;
+    // DP launch geometry: blocks resident per SM bounded by shared memory
+    int max_units = std::max(1, c->hn.max_L);
+    size_t smem = partition_smem_bytes(max_units, std::max(1, hb.max_N), c->max_T);
+    if (smem > 227 * 1024)
+        return fail(c, BP_BAD_INPUT, "network too large for the shared-memory DP (L=" + std::to_string(max_units) + ")");
+    int per_sm = (int)std::max<size_t>(1, (size_t)(200 * 1024) / (smem + 1024));
+    if (per_sm > 8) per_sm = 8;
+    B->dp_grid = c->sm_count * per_sm;
+    B->dp_max_units = max_units;
+    return BP_OK;
+}
+
+int upload_inputs(bp_ctx* c, bp_batch* B, cudaStream_t st) {
+    cudaError_t e = cudaMemcpyAsync(B->mem.p, B->stage_in.p, B->in_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D batch inputs");
+    return BP_OK;
+}
+
+int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
+    BatchDev& D = B->dev;
+    const HostBatch& hb = B->hb;
+    cudaError_t e;
+    e = cudaMemsetAsync(D.cand, 0, (size_t)hb.ncand * sizeof(bp_candidate), st);
+    if (e == cudaSuccess && D.stages) e = cudaMemsetAsync(D.stages, 0, (size_t)hb.nstage * sizeof(bp_stage), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(D.dp_count + 1, 0, sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(D.work, 0, 8 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "memset");
+    const int T = c->max_T, maxN = std::max(1, hb.max_N);
+    timed(c, "setup", st, [&] { launch_setup(D, st); });
+    if (!hb.whole_items.empty())
+        timed(c, "minmax_dp", st, [&] {
+            launch_partition(D, 0, std::min<int>(B->dp_grid, (int)hb.whole_items.size()), B->dp_max_units, maxN, T,
+                             st);
+        });
+    timed(c, "bottleneck", st, [&] { launch_bottleneck(D, st); });
+    if (hb.nmslot > 0)
+        timed(c, "minmax_dp_coarse", st, [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, st); });
+    timed(c, "refine", st, [&] { launch_refine(D, st); });
+    timed(c, "prune", st, [&] { launch_prune(D, st); });
+    timed(c, "simulate", st, [&] { launch_sim(D, st); });
+    timed(c, "rank", st, [&] { launch_rank(D, st); });
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "kernel launch");
+    return BP_OK;
+}
+
+int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_stage* stages, cudaStream_t st) {
+    const HostBatch& hb = B->hb;
+    cudaError_t e = cudaSuccess;
+    if (res) e = cudaMemcpyAsync(res, B->dev.res, (size_t)B->nq * sizeof(bp_query_result), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && cand && hb.ncand)
+        e = cudaMemcpyAsync(cand, B->dev.cand, (size_t)hb.ncand * sizeof(bp_candidate), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && stages && B->dev.stages && hb.nstage)
+        e = cudaMemcpyAsync(stages, B->dev.stages, (size_t)hb.nstage * sizeof(bp_stage), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cuda_fail(c, e, "fetch");
+    if (c->prof) {
+        unsigned long long work[8];
+        if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess)
+            c->stats["minmax_dp"].work += (double)work[0];
+        collect(c);
+    }
+    return BP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bp_abi_version(void) { return BP_ABI_VERSION; }
+
+const char* bp_last_error(const bp_ctx* c) { return c ? c->err.c_str() : g_err.c_str(); }
+
+bp_ctx* bp_create(int device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        g_err = std::string("no CUDA device: ") + (e != cudaSuccess ? cudaGetErrorString(e) : "count = 0");
+        return nullptr;
+    }
+    if (device < 0 || device >= n) {
+        g_err = "device index out of range";
+        return nullptr;
+    }
+    cudaDeviceProp prop;
+    if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+        g_err = "cannot use device";
+        return nullptr;
+    }
+    if (prop.major < 10) {
+        g_err = "libbapipe_b200 is built for sm_100a (B200); device is sm_" + std::to_string(prop.major) +
+                std::to_string(prop.minor);
+        return nullptr;
+    }
+    bp_ctx* c = new (std::nothrow) bp_ctx();
+    if (!c) return nullptr;
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    return c;
+}
+
+void bp_destroy(bp_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    if (c->cached) bp_batch_free(c, c->cached);
+    c->nets_mem.release();
+    c->cls_mem.release();
+    for (auto e : c->event_pool) cudaEventDestroy(e);
+    delete c;
+}
+
+int bp_set_networks(bp_ctx* c, const bp_network* nets, int n) {
+    if (!c || (!nets && n > 0) || n < 0) return fail(c, BP_BAD_INPUT, "bad arguments");
+    try {
+        cudaSetDevice(c->device);
+        std::string err;
+        if (!build_nets(nets, n, c->hn, err, true)) return fail(c, BP_BAD_INPUT, err);
+        int rc = upload_networks(c);
+        c->have_nets = rc == BP_OK;
+        return rc;
+    } catch (const std::bad_alloc&) {
+        return fail(c, BP_OUT_OF_MEMORY, "host allocation failed");
+    }
+}
+
+int bp_set_clusters(bp_ctx* c, const bp_cluster* cls, int n) {
+    if (!c || (!cls && n > 0) || n < 0) return fail(c, BP_BAD_INPUT, "bad arguments");
+    try {
+        cudaSetDevice(c->device);
+        std::string err;
+        if (!build_clusters(cls, n, c->hc, err)) return fail(c, BP_BAD_INPUT, err);
+        int rc = upload_clusters(c);
+        c->have_cls = rc == BP_OK;
+        return rc;
+    } catch (const std::bad_alloc&) {
+        return fail(c, BP_OUT_OF_MEMORY, "host allocation failed");
+    }
+}
+
+int bp_layout(bp_ctx* c, bp_query* q, int nq, int64_t* total_candidates, int64_t* total_stages) {
+    if (!c || (!q && nq > 0) || nq < 0) return fail(c, BP_BAD_INPUT, "bad arguments");
+    try {
+        HostBatch hb;
+        std::string err;
+        if (!build_batch(q, nq, c->hn, c->hc, hb, err)) return fail(c, BP_BAD_INPUT, err);
+        for (int i = 0; i < nq; ++i) {
+            q[i].cand_offset = hb.q[i].cand_off;
+            q[i].stage_offset = hb.q[i].stage_off;
+        }
+        if (total_candidates) *total_candidates = hb.ncand;
+        if (total_stages) *total_stages = hb.nstage;
+        return BP_OK;
+    } catch (const std::bad_alloc&) {
+        return fail(c, BP_OUT_OF_MEMORY, "host allocation failed");
+    }
+}
+
+bp_batch* bp_batch_prepare(bp_ctx* c, const bp_query* q, int nq, int want_details, void* stream) {
+    if (!c || (!q && nq > 0) || nq < 0) { fail(c, BP_BAD_INPUT, "bad arguments"); return nullptr; }
+    try {
+        cudaSetDevice(c->device);
+        bp_batch* B = new bp_batch();
+        cudaStream_t st = (cudaStream_t)stream;
+        if (prepare(c, B, q, nq, want_details, st) != BP_OK || upload_inputs(c, B, st) != BP_OK) {
+            bp_batch_free(c, B);
+            return nullptr;
+        }
+        if (cudaStreamSynchronize(st) != cudaSuccess) {
+            bp_batch_free(c, B);
+            fail(c, BP_CUDA_ERROR, "prepare sync");
+            return nullptr;
+        }
+        return B;
+    } catch (const std::bad_alloc&) {
+        fail(c, BP_OUT_OF_MEMORY, "host allocation failed");
+        return nullptr;
+    }
+}
+
+int bp_batch_run(bp_ctx* c, bp_batch* B, void* stream) {
+    if (!c || !B) return fail(c, BP_BAD_INPUT, "bad arguments");
+    cudaSetDevice(c->device);
+    return run(c, B, (cudaStream_t)stream);
+}
+
+int bp_batch_fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_stage* stages,
+                   void* stream) {
+    if (!c || !B) return fail(c, BP_BAD_INPUT, "bad arguments");
+    cudaSetDevice(c->device);
+    return fetch(c, B, res, cand, stages, (cudaStream_t)stream);
+}
+
+int bp_batch_best(bp_ctx* c, bp_batch* B, void* dev_out, int64_t query_base, void* stream) {
+    if (!c || !B || !dev_out) return fail(c, BP_BAD_INPUT, "bad arguments");
+    cudaSetDevice(c->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    timed(c, "best", st, [&] { launch_best(B->dev, (bp_best_record*)dev_out, query_base, nullptr, st); });
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BP_OK : cuda_fail(c, e, "best");
+}
+
+void bp_batch_free(bp_ctx* c, bp_batch* B) {
+    if (!B) return;
+    if (c) cudaSetDevice(c->device);
+    B->mem.release();
+    B->stage_in.release();
+    delete B;
+}
+
+int bp_explore_batch(bp_ctx* c, const bp_query* q, int nq, bp_query_result* res, bp_candidate* cand,
+                     bp_stage* stages, void* stream) {
+    if (!c || (!q && nq > 0) || nq < 0 || !res) return fail(c, BP_BAD_INPUT, "bad arguments");
+    try {
+        cudaSetDevice(c->device);
+        cudaStream_t st = (cudaStream_t)stream;
+        if (!c->cached) c->cached = new bp_batch();
+        bp_batch* B = c->cached;
+        int rc = prepare(c, B, q, nq, stages != nullptr, st);
+        if (rc == BP_OK) rc = upload_inputs(c, B, st);
+        if (rc == BP_OK) rc = run(c, B, st);
+        if (rc == BP_OK) rc = fetch(c, B, res, cand, stages, st);
+        return rc;
+    } catch (const std::bad_alloc&) {
+        return fail(c, BP_OUT_OF_MEMORY, "host allocation failed");
+    }
+}
+
+int64_t bp_launch_count(const bp_ctx* c) { return c ? c->launches : 0; }
+
+int bp_set_profiling(bp_ctx* c, int enable) {
+    if (!c) return BP_BAD_INPUT;
+    c->prof = enable != 0;
+    if (enable) c->stats.clear();
+    return BP_OK;
+}
+
+int bp_kernel_stats(const bp_ctx* c, char* names48, double* ms, int64_t* launches, double* work, int cap) {
+    if (!c) return 0;
+    int i = 0;
+    for (auto& kv : c->stats) {
+        if (i >= cap) break;
+        if (names48) {
+            std::memset(names48 + 48 * i, 0, 48);
+            std::strncpy(names48 + 48 * i, kv.first.c_str(), 47);
+        }
+        if (ms) ms[i] = kv.second.ms;
+        if (launches) launches[i] = kv.second.launches;
+        if (work) work[i] = kv.second.work;
+        ++i;
+    }
+    return i;
+}
+
+int bp_best_less(const bp_best_record* a, const bp_best_record* b) {
+    if (a->valid != b->valid) return a->valid > b->valid;
+    if (!a->valid) return a->query_id < b->query_id;
+    auto lt = [](bp_rat x, bp_rat y) { return (__int128)x.num * y.den < (__int128)y.num * x.den; };
+    auto eq = [](bp_rat x, bp_rat y) { return x.num == y.num && x.den == y.den; };
+    if (!eq(a->makespan, b->makespan)) return lt(a->makespan, b->makespan);
+    if (!eq(a->peak_memory, b->peak_memory)) return lt(a->peak_memory, b->peak_memory);
+    if (!eq(a->max_bw, b->max_bw)) return lt(a->max_bw, b->max_bw);
+    if (a->M != b->M) return a->M < b->M;
+    if (a->kind != b->kind) return a->kind < b->kind;
+    return a->query_id < b->query_id;
+}
+
+}  // extern "C"

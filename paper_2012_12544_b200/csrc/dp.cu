@@ -38,12 +38,6 @@ struct DPSmem {
 __device__ __forceinline__ int64_t dmax(int64_t a, int64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ int64_t dmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
-// Bytes of dynamic shared memory for an instance with U units, N stages, T type slots.
-__host__ __device__ inline size_t dp_smem_bytes(int64_t U, int64_t N, int T) {
-    size_t words = (size_t)((U + 1 + 31) / 32);
-    return (size_t)(U + 1) * 8 * (size_t)(T + 4) + (size_t)(N + 1) * words * 4 + (size_t)(U + 1) * 4 + 64;
-}
-
 __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which, int max_units, int T_slots) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int64_t s_red[DP_THREADS / 32];
@@ -281,22 +275,19 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
     }
 }
 
-void launch_partition(const BatchDev& B, int which, int grid, int max_units, int T_slots, cudaStream_t st) {
-    size_t bytes = dp_smem_bytes(max_units, 0, T_slots);
-    // feas rows: sized for the largest N in the batch (max_units bounds N)
-    bytes += (size_t)(max_units + 2) * (((size_t)max_units + 1 + 31) / 32) * 4;
-    static bool configured = false;
-    if (!configured) {
-        cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        configured = true;
-    }
+void launch_partition(const BatchDev& B, int which, int grid, int max_units, int max_N, int T_slots,
+                      cudaStream_t st) {
+    size_t bytes = partition_smem_bytes(max_units, max_N, T_slots);
+    cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     k_partition<<<grid, DP_THREADS, bytes, st>>>(B, which, max_units, T_slots);
 }
 
+// Layout of k_partition's dynamic shared memory (must match DPSmem above).
 size_t partition_smem_bytes(int max_units, int max_N, int T_slots) {
     size_t words = ((size_t)max_units + 1 + 31) / 32;
-    return (size_t)(max_units + 1) * 8 * (size_t)(T_slots + 4) + (size_t)(max_units + 1) * 4 + 64 +
-           (size_t)(max_N + 1) * words * 4;
+    size_t b = (size_t)(max_units + 1) * 8 * (size_t)(T_slots + 4) + (size_t)(max_units + 1) * 4;
+    b = (b + 15) & ~(size_t)15;
+    return b + (size_t)(max_N + 1) * words * 4;
 }
 
 }  // namespace bpk

@@ -1,0 +1,24 @@
+// kernels.h -- launchers for the explore() pipeline kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "batch.cuh"
+
+namespace bpk {
+
+// K1 cost_prefix: per network, prefix sums of fp, bp, fp+bp per type and of w.
+void launch_cost_prefix(const NetDesc* nets, int n_nets, const int64_t* fp, const int64_t* bp, const int64_t* w,
+                        int64_t* Pfp, int64_t* Pbp, int64_t* Pc, int64_t* Pw, cudaStream_t st, int max_T);
+void launch_setup(const BatchDev& B, cudaStream_t st);
+void launch_partition(const BatchDev& B, int which, int grid, int max_units, int max_N, int T_slots,
+                      cudaStream_t st);
+size_t partition_smem_bytes(int max_units, int max_N, int T_slots);
+void launch_bottleneck(const BatchDev& B, cudaStream_t st);
+void launch_refine(const BatchDev& B, cudaStream_t st);
+void launch_prune(const BatchDev& B, cudaStream_t st);
+void launch_sim(const BatchDev& B, cudaStream_t st);
+void launch_rank(const BatchDev& B, cudaStream_t st);
+void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,
+                 cudaStream_t st);
+
+}  // namespace bpk

@@ -18,11 +18,23 @@
 // CPU against the oracle; the product runs it only inside the kernels.
 #ifdef __CUDACC__
 #define BPK_HD __host__ __device__ __forceinline__
-#define BPK_HDNI __host__ __device__ __noinline__
+#define BPK_HDNI static __host__ __device__ __noinline__
 #else
 #define BPK_HD inline
-#define BPK_HDNI inline
-static inline int __ffsll(long long x) { return __builtin_ffsll(x); }
+#define BPK_HDNI static inline
+#endif
+
+// find-first-set (1-based, 0 for 0) on both sides
+#ifdef __CUDACC__
+__host__ __device__ __forceinline__ int bpk_ffs64(long long x) {
+#ifdef __CUDA_ARCH__
+    return __ffsll(x);
+#else
+    return __builtin_ffsll(x);
+#endif
+}
+#else
+inline int bpk_ffs64(long long x) { return __builtin_ffsll(x); }
 #endif
 
 namespace bpk {
@@ -57,10 +69,10 @@ BPK_HD Rat R(int64_t v) { return Rat{v, 1}; }
 BPK_HD uint64_t gcd_u64(uint64_t u, uint64_t v) {
     if (u == 0) return v;
     if (v == 0) return u;
-    int shift = __ffsll((long long)(u | v)) - 1;
-    u >>= (__ffsll((long long)u) - 1);
+    int shift = bpk_ffs64((long long)(u | v)) - 1;
+    u >>= (bpk_ffs64((long long)u) - 1);
     do {
-        v >>= (__ffsll((long long)v) - 1);
+        v >>= (bpk_ffs64((long long)v) - 1);
         if (u > v) { uint64_t t = u; u = v; v = t; }
         v -= u;
     } while (v != 0);
@@ -69,8 +81,8 @@ BPK_HD uint64_t gcd_u64(uint64_t u, uint64_t v) {
 
 BPK_HD int ctz128(u128 x) {
     uint64_t lo = (uint64_t)x;
-    if (lo) return __ffsll((long long)lo) - 1;
-    return 64 + __ffsll((long long)(uint64_t)(x >> 64)) - 1;
+    if (lo) return bpk_ffs64((long long)lo) - 1;
+    return 64 + bpk_ffs64((long long)(uint64_t)(x >> 64)) - 1;
 }
 
 BPK_HDNI u128 gcd_u128(u128 u, u128 v) {
