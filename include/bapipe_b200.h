@@ -244,6 +244,8 @@ int bp_set_profiling(bp_ctx* ctx, int enable);
  * launch counts and algorithmic work units.  Returns the entry count. */
 int bp_kernel_stats(const bp_ctx* ctx, char* names48, double* ms, int64_t* launches,
                     double* work, int cap);
+/* Bytes copied host->device and device->host since creation. */
+int bp_transfer_stats(const bp_ctx* ctx, int64_t* h2d_bytes, int64_t* d2h_bytes);
 
 /* Deterministic argmin order for bp_best_record (makespan, peak_memory,
  * max_bw, M, kind, query_id); the first five keys are explorer.hpp:144-151. */

@@ -94,7 +94,7 @@ PRODUCT_SYMBOLS = (
     "bp_create", "bp_destroy", "bp_last_error", "bp_abi_version", "bp_set_networks",
     "bp_set_clusters", "bp_layout", "bp_explore_batch", "bp_batch_prepare", "bp_batch_run",
     "bp_batch_fetch", "bp_batch_best", "bp_batch_free", "bp_launch_count", "bp_set_profiling",
-    "bp_kernel_stats", "bp_best_less",
+    "bp_kernel_stats", "bp_transfer_stats", "bp_best_less",
 )
 
 
@@ -127,6 +127,7 @@ def bind_product(lib: C.CDLL) -> C.CDLL:
     _sig(lib, "bp_set_profiling", C.c_int, [vp, C.c_int])
     _sig(lib, "bp_kernel_stats", C.c_int,
          [vp, C.c_char_p, C.POINTER(C.c_double), P64, C.POINTER(C.c_double), C.c_int])
+    _sig(lib, "bp_transfer_stats", C.c_int, [vp, P64, P64])
     _sig(lib, "bp_best_less", C.c_int, [C.POINTER(bp_best_record), C.POINTER(bp_best_record)])
     return lib
 

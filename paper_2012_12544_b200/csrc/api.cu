@@ -95,6 +95,7 @@ struct bp_ctx {
     int sm_count = 148;
     std::string err;
     int64_t launches = 0;
+    int64_t h2d = 0, d2h = 0;
     HostNets hn;
     HostCls hc;
     bool have_nets = false, have_cls = false;
@@ -133,7 +134,7 @@ cudaEvent_t get_event(bp_ctx* c) {
 
 // Launch wrapper: counts launches, brackets them with events when profiling.
 template <class F>
-void timed(bp_ctx* c, const char* name, cudaStream_t st, F&& f) {
+void timed(bp_ctx* c, const char* name, cudaStream_t st, F&& f, int n_kernels = 1) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (c->prof) {
         a = get_event(c);
@@ -141,7 +142,7 @@ void timed(bp_ctx* c, const char* name, cudaStream_t st, F&& f) {
         cudaEventRecord(a, st);
     }
     f();
-    ++c->launches;
+    c->launches += n_kernels;
     if (c->prof) {
         cudaEventRecord(b, st);
         c->pending.push_back({name, {a, b}});
@@ -184,6 +185,7 @@ int upload_networks(bp_ctx* c) {
     if (!c->nets_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(networks)");
     void* b = c->nets_mem.p;
     auto up = [&](size_t off, const void* src, size_t bytes) {
+        c->h2d += (int64_t)bytes;
         return bytes ? cudaMemcpy(dptr<char>(b, off), src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
     };
     cudaError_t e = cudaSuccess;
@@ -233,6 +235,7 @@ int upload_clusters(bp_ctx* c) {
     if (!c->cls_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(clusters)");
     void* b = c->cls_mem.p;
     auto up = [&](size_t off, const void* src, size_t bytes) {
+        c->h2d += (int64_t)bytes;
         return bytes ? cudaMemcpy(dptr<char>(b, off), src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
     };
     cudaError_t e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(ClDesc));
@@ -268,6 +271,8 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     size_t o_M = L.take<int64_t>(hb.Mpool.size());
     size_t o_items = L.take<DPItem>(nqs + nms);
     size_t o_cnt = L.take<int32_t>(4);
+    size_t o_qord = L.take<int32_t>(nqs);
+    size_t o_cperm = L.take<int32_t>(nc);
     size_t in_end = L.off;
     // outputs
     size_t o_res = L.take<bp_query_result>(nqs);
@@ -282,9 +287,11 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     size_t o_clo = L.take<int32_t>(ns), o_chi = L.take<int32_t>(ns);
     size_t o_sF = L.take<Rat>(ns), o_sB = L.take<Rat>(ns), o_sW = L.take<Rat>(ns), o_sM = L.take<Rat>(ns);
     size_t o_sA = L.take<int64_t>(ns), o_sSR = L.take<int64_t>(ns);
-    size_t o_sim = L.take<Rat>(9 * ns);
+    size_t o_sim = L.take<char>(sim_exact_state_bytes(c->sm_count, std::max(1, hb.max_N)));
+    size_t o_xkey = L.take<int32_t>(nc), o_xsorted = L.take<int32_t>(nc), o_xhist = L.take<int32_t>(XBUCKETS);
     size_t o_cq = L.take<int32_t>(nc), o_co = L.take<int32_t>(nc);
     size_t o_work = L.take<unsigned long long>(8);
+    size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(SIM_CLASSES);
     if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
     void* b = B->mem.p;
     // stage the inputs in pinned memory and copy once
@@ -295,6 +302,8 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     if (!hb.whole_items.empty()) std::memcpy(h + o_items, hb.whole_items.data(), hb.whole_items.size() * sizeof(DPItem));
     int32_t cnt[4] = {(int32_t)hb.whole_items.size(), 0, 0, 0};
     std::memcpy(h + o_cnt, cnt, sizeof(cnt));
+    if (nqs) std::memcpy(h + o_qord, hb.qorder.data(), nqs * 4);
+    if (nc) std::memcpy(h + o_cperm, hb.cperm.data(), nc * 4);
     B->in_off = 0;
     B->in_bytes = in_end;
     B->res_off = o_res;
@@ -331,11 +340,19 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.sA = dptr<int64_t>(b, o_sA);
     D.sSR = dptr<int64_t>(b, o_sSR);
     D.simbuf = dptr<Rat>(b, o_sim);
+    D.xkey = dptr<int32_t>(b, o_xkey);
+    D.xsorted = dptr<int32_t>(b, o_xsorted);
+    D.xhist = dptr<int32_t>(b, o_xhist);
+    D.max_N = std::max(1, hb.max_N);
     D.cq = dptr<int32_t>(b, o_cq);
     D.corder = dptr<int32_t>(b, o_co);
     D.dp_items = dptr<DPItem>(b, o_items);
     D.dp_count = dptr<int32_t>(b, o_cnt);
     D.work = dptr<unsigned long long>(b, o_work);
+    D.qorder = dptr<int32_t>(b, o_qord);
+    D.cperm = dptr<int32_t>(b, o_cperm);
+    D.sim_list = dptr<int32_t>(b, o_slist);
+    D.sim_count = dptr<int32_t>(b, o_scnt);
     D.details = details ? 1 : 0;
     // DP launch geometry: blocks resident per SM bounded by shared memory
     int max_units = std::max(1, c->hn.max_L);
@@ -351,6 +368,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
 
 int upload_inputs(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     cudaError_t e = cudaMemcpyAsync(B->mem.p, B->stage_in.p, B->in_bytes, cudaMemcpyHostToDevice, st);
+    c->h2d += (int64_t)B->in_bytes;
     if (e != cudaSuccess) return cuda_fail(c, e, "H2D batch inputs");
     return BP_OK;
 }
@@ -376,7 +394,11 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
         timed(c, "minmax_dp_coarse", st, [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, st); });
     timed(c, "refine", st, [&] { launch_refine(D, st); });
     timed(c, "prune", st, [&] { launch_prune(D, st); });
-    timed(c, "simulate", st, [&] { launch_sim(D, st); });
+    timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); });
+    static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
+                                        "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
+    for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
+    timed(c, "sim_exact", st, [&] { launch_sim_exact(D, c->sm_count, st); }, 4);
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "kernel launch");
@@ -387,6 +409,9 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
     const HostBatch& hb = B->hb;
     cudaError_t e = cudaSuccess;
     if (res) e = cudaMemcpyAsync(res, B->dev.res, (size_t)B->nq * sizeof(bp_query_result), cudaMemcpyDeviceToHost, st);
+    if (res) c->d2h += (int64_t)B->nq * (int64_t)sizeof(bp_query_result);
+    if (cand) c->d2h += hb.ncand * (int64_t)sizeof(bp_candidate);
+    if (stages && B->dev.stages) c->d2h += hb.nstage * (int64_t)sizeof(bp_stage);
     if (e == cudaSuccess && cand && hb.ncand)
         e = cudaMemcpyAsync(cand, B->dev.cand, (size_t)hb.ncand * sizeof(bp_candidate), cudaMemcpyDeviceToHost, st);
     if (e == cudaSuccess && stages && B->dev.stages && hb.nstage)
@@ -397,6 +422,12 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
         unsigned long long work[8];
         if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess)
             c->stats["minmax_dp"].work += (double)work[0];
+        int32_t cnt[SIM_CLASSES];
+        static const char* names[SIM_CLASSES] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
+                                                 "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4",
+                                                 "sim_fast_g32s8", "sim_exact"};
+        if (cudaMemcpy(cnt, B->dev.sim_count, sizeof(cnt), cudaMemcpyDeviceToHost) == cudaSuccess)
+            for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work += cnt[k];
         collect(c);
     }
     return BP_OK;
@@ -589,6 +620,13 @@ int bp_kernel_stats(const bp_ctx* c, char* names48, double* ms, int64_t* launche
         ++i;
     }
     return i;
+}
+
+int bp_transfer_stats(const bp_ctx* c, int64_t* h2d, int64_t* d2h) {
+    if (!c) return BP_BAD_INPUT;
+    if (h2d) *h2d = c->h2d;
+    if (d2h) *d2h = c->d2h;
+    return BP_OK;
 }
 
 int bp_best_less(const bp_best_record* a, const bp_best_record* b) {

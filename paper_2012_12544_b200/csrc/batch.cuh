@@ -51,6 +51,12 @@ struct MState {
 // Per-candidate plan kinds.
 enum { PLAN_NONE = 0, PLAN_REFINED = 1, PLAN_WHOLE = 2 };
 
+// Simulator classes: 0..4 = lanes per candidate 2, 4, 8, 16, 32 (one stage
+// per lane); 5, 6, 7 = 32 lanes with 2, 4, 8 stages per lane; 8 = exact
+// (Rat) slow path, thread per candidate.
+enum { SIM_CLASSES = 9, SIM_EXACT = 8 };
+enum { XBUCKETS = 8192, XSIM_WARPS_PER_SM = 8 };
+
 // Per-candidate device state (beyond the bp_candidate output record).
 struct CState {
     int32_t plan_kind;
@@ -90,6 +96,15 @@ struct BatchDev {
     Rat* simbuf;              // exact simulator state, 9 Rats per stage slot
     int32_t* cq;              // candidate -> query
     int32_t* corder;          // ranking scratch, one slot per candidate
+    const int32_t* qorder;    // scheduling order of queries (host_prep.hpp)
+    const int32_t* cperm;     // scheduling order of candidates
+    int32_t* sim_list;        // [SIM_CLASSES][ncand] candidate lists per simulator class
+    int32_t* sim_count;       // [SIM_CLASSES]
+    // exact-simulator scheduling: counting sort of its list by (N, log2 M)
+    int32_t* xkey;            // [ncand]
+    int32_t* xsorted;         // [ncand]
+    int32_t* xhist;           // [XBUCKETS] counts, then running offsets
+    int max_N;                // largest stage count in the batch (exact-sim state sizing)
     int details;              // write bp_stage records
     // DP work lists
     DPItem* dp_items;

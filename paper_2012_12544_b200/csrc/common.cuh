@@ -126,7 +126,7 @@ BPK_HD bool kind_async(int kind) { return kind == KIND_AS || kind == KIND_FBP; }
 // whether any of them overflows; its reduced denominator is that of
 // lead * v_lo (adding integers keeps the denominator).
 //   P: prefix sums of v over layers (P[j] = v_1 + ... + v_j).
-BPK_HD Rat stage_sum_frac(int64_t lo, int64_t hi, Rat lead, Rat trail,
+BPK_HDNI Rat stage_sum_frac(int64_t lo, int64_t hi, Rat lead, Rat trail,
                                               const int64_t* P, Err& e) {
     if (lo > hi) return Rat{0, 1};
     if (lo == hi) {

@@ -113,19 +113,16 @@ __global__ void k_bottleneck(BatchDev B) {
     }
 }
 
+// Queries / candidates are visited in the host's scheduling order
+// (host_prep.hpp) so that the lanes of a warp run similar work.
 __global__ void k_refine(BatchDev B) {
-    int qi = blockIdx.x * blockDim.x + threadIdx.x;
-    if (qi < B.nq) refine_query(B, qi);
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < B.nq) refine_query(B, B.qorder[i]);
 }
 
 __global__ void k_prune(BatchDev B) {
-    int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (ci < B.ncand) prune_candidate(B, ci);
-}
-
-__global__ void k_sim(BatchDev B) {
-    int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (ci < B.ncand) sim_exact(B, ci);
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < B.ncand) prune_candidate(B, B.cperm[i]);
 }
 
 __global__ void k_rank(BatchDev B) {
@@ -199,9 +196,6 @@ void launch_refine(const BatchDev& B, cudaStream_t st) {
 }
 void launch_prune(const BatchDev& B, cudaStream_t st) {
     if (B.ncand) k_prune<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
-}
-void launch_sim(const BatchDev& B, cudaStream_t st) {
-    if (B.ncand) k_sim<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
 }
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);

@@ -366,13 +366,17 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
     const Rat zero{0, 1};
     const Rat step{1, 1024};
     auto T = [&](int s) -> Rat {
-        if (dirty[s]) {
+        if (dirty[s] & 1) {
             stage_times(v, c, s, lo, hi, lead, trail, tF[s], tB[s], e);
             tT[s] = rat_add(tF[s], tB[s], e);
-            dirty[s] = 0;
+            dirty[s] &= (uint8_t)~1u;
         }
         return tT[s];
     };
+    // bit 1 of dirty[b]: boundary b (stages b, b+1) was evaluated without a
+    // move and neither stage changed since.  A boundary step is a pure
+    // function of its two stages, so the reference would recompute the same
+    // values and again not move: skipping it is exact.
     bool changed = true;
     int guard = 0;
     while (changed && ++guard < 1000) {
@@ -381,6 +385,8 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < N - 1; ++i) {
                 int n0 = (pass == 0) ? i : (N - 2 - i);
+                if (dirty[n0] & 2) continue;
+                dirty[n0] |= 2;   // cleared below if this step moves
                 Rat t_a = T(n0);
                 if (e.bad()) return;
                 Rat t_b = T(n0 + 1);
@@ -454,7 +460,8 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
                     }
                 }
                 if (e.bad()) return;
-                dirty[a] = dirty[b] = 1;
+                dirty[a] = dirty[b] = 1;                 // stage times stale, boundaries a, b unstable
+                if (a > 0) dirty[a - 1] &= 1;            // boundary a-1 touches stage a
                 changed = true;
             }
         }

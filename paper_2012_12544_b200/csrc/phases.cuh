@@ -314,13 +314,110 @@ BPK_HD StageOp op_at(int64_t p, int64_t w, int64_t M) {
     return StageOp{0, (M - w) + (r - 2 * (M - w)) + 1};
 }
 
-BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci) {
-    const CState& cs = B.cs[ci];
-    if (!cs.sim_ready) return;
+// simulate() entry: validate_plan (plan.hpp:41-85), then choose the
+// simulator.  Returns the class (see SIM_CLASSES) or -1 when the candidate
+// is finished (InvalidPlan / error).
+//   Fast path: every event time is an exact multiple of 1/D, D = lcm of the
+//   stage F/B denominators; if D * (M * sum(F+B) + 2M * sum(SR)) < 2^61 --
+//   an upper bound on every path length, hence on every event -- all events
+//   are int64 multiples of 1/D, and no reduced numerator/denominator can
+//   exceed int64, so the reference cannot overflow there (rational.hpp:90).
+//   Otherwise the exact Rat simulator decides (slow path).
+BPK_HDNI int sim_classify(const BatchDev& B, int64_t ci) {
+    CState& cs = B.cs[ci];
+    if (!cs.sim_ready) return -1;
     bp_candidate& cd = B.cand[ci];
     const int qi = B.cq[ci];
     const QDesc Q = B.q[qi];
     const QState& qs = B.qs[qi];
+    const int64_t local = ci - Q.cand_off;
+    const int N = Q.N;
+    const int64_t M = cd.M, micro = cd.micro;
+    NetView v = net_view(B.P, Q.net);
+    ChainView c = chain_view(B.P, Q.cl, N);
+    const int64_t slot = Q.stage_off + local * N;
+    const int64_t qo = Q.qstage_off;
+    const int32_t* hi = cs.plan_kind == PLAN_REFINED ? B.qhi + qo : B.chi + slot;
+    const int32_t* lo = cs.plan_kind == PLAN_REFINED ? B.qlo + qo : B.clo + slot;
+    if (cs.plan_kind == PLAN_REFINED) {
+        if (qs.vcode) {
+            cd.status = BP_C_ERR_INVALID_PLAN;
+            cd.detail = qs.vcode;
+            cd.detail2 = qs.vwhere;
+            cd.aux = bp_rat{qs.vaux.n, qs.vaux.d};
+            return -1;
+        }
+        if (qs.verr) { cd.status = status_of_err(qs.verr); return -1; }
+    } else {
+        int64_t where = 0;
+        int vc = validate_whole(lo, hi, N, v.L, &where);
+        if (vc) {
+            cd.status = BP_C_ERR_INVALID_PLAN;
+            cd.detail = vc;
+            cd.detail2 = where;
+            return -1;
+        }
+    }
+    int64_t D;
+    u128 sumFB;
+    if (cs.plan_kind == PLAN_REFINED) {
+        D = qs.D;
+        if (D == 0 || qs.sumFB_D < 0) return SIM_EXACT;
+        sumFB = (u128)qs.sumFB_D;
+    } else {
+        D = 1;
+        sumFB = 0;
+        for (int s = 0; s < N; ++s) {
+            int32_t t = c.type[s];
+            sumFB += (u128)stage_sum_whole(lo[s], hi[s], v.Pc + (int64_t)t * (v.L + 1));
+        }
+    }
+    u128 sumSR = 0;
+    for (int k = 0; k + 1 < N; ++k) {
+        int64_t a = v.a[hi[k] - 1] * micro;
+        sumSR += (u128)(a == 0 ? 0 : ceil_div64(a, c.bw[k]));
+    }
+    u128 bound = (u128)M * sumFB + (u128)(2 * M) * (u128)D * sumSR;
+    cs.D = D;
+    if (bound >= ((u128)1 << 61)) return SIM_EXACT;
+    if (N <= 2) return 0;
+    if (N <= 4) return 1;
+    if (N <= 8) return 2;
+    if (N <= 16) return 3;
+    if (N <= 32) return 4;
+    if (N <= 64) return 5;
+    if (N <= 128) return 6;
+    if (N <= 256) return 7;
+    return SIM_EXACT;
+}
+
+// Per-stage state of the exact simulator, element s at base[s * stride]
+// (stride 32 on the GPU interleaves a warp's lanes for coalescing).
+struct SimState {
+    Rat *fr, *pF, *pB, *F, *B;
+    int64_t *SR, *A;
+    int stride;
+    BPK_HD Rat& f(int s) const { return fr[(int64_t)s * stride]; }
+    BPK_HD Rat& mf(int s) const { return pF[(int64_t)s * stride]; }
+    BPK_HD Rat& mb(int s) const { return pB[(int64_t)s * stride]; }
+    BPK_HD Rat& dF(int s) const { return F[(int64_t)s * stride]; }
+    BPK_HD Rat& dB(int s) const { return B[(int64_t)s * stride]; }
+    BPK_HD int64_t& sr(int s) const { return SR[(int64_t)s * stride]; }
+    BPK_HD int64_t& act(int s) const { return A[(int64_t)s * stride]; }
+};
+
+// Exact simulator body.  Positions are walked in order; at each position
+// the F ops run in ascending stage order and the B ops in descending order
+// (a topological order of the reference's sorted op list).  An arrival goes
+// into the receiving stage's one-slot mailbox unless the receiver consumes it
+// at the same position (a chain); the carry register defers the mailbox
+// write until the receiver has read its own input, which is what keeps one
+// slot sufficient (at most one arrival is outstanding per link direction).
+BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S) {
+    const CState& cs = B.cs[ci];
+    bp_candidate& cd = B.cand[ci];
+    const int qi = B.cq[ci];
+    const QDesc Q = B.q[qi];
     const int64_t local = ci - Q.cand_off;
     const int N = Q.N;
     const int kind = cd.kind;
@@ -330,94 +427,95 @@ BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci) {
     const int64_t slot = Q.stage_off + local * N;
     const int64_t qo = Q.qstage_off;
     const int32_t* hi = cs.plan_kind == PLAN_REFINED ? B.qhi + qo : B.chi + slot;
-    // validate_plan (plan.hpp:41-85)
-    if (cs.plan_kind == PLAN_REFINED) {
-        if (qs.vcode) {
-            cd.status = BP_C_ERR_INVALID_PLAN;
-            cd.detail = qs.vcode;
-            cd.detail2 = qs.vwhere;
-            cd.aux = bp_rat{qs.vaux.n, qs.vaux.d};
-            return;
-        }
-        if (qs.verr) { cd.status = status_of_err(qs.verr); return; }
-    } else {
-        int64_t where = 0;
-        int vc = validate_whole(B.clo + slot, B.chi + slot, N, v.L, &where);
-        if (vc) {
-            cd.status = BP_C_ERR_INVALID_PLAN;
-            cd.detail = vc;
-            cd.detail2 = where;
-            return;
-        }
-    }
     Err e{ERR_NONE};
     // chain_instance (simulator.hpp:248-262): F, B per stage; SR per link.
-    Rat* F = B.sF + slot;
-    Rat* Bd = B.sB + slot;
-    int64_t* SR = B.sSR + slot;
-    int64_t* A = B.sA + slot;
     for (int s = 0; s < N; ++s) {
-        if (cs.plan_kind == PLAN_REFINED) { F[s] = B.qF[qo + s]; Bd[s] = B.qB[qo + s]; }
+        if (cs.plan_kind == PLAN_REFINED) { S.dF(s) = B.qF[qo + s]; S.dB(s) = B.qB[qo + s]; }
         else {
             int32_t t = c.type[s];
-            F[s] = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pfp + (int64_t)t * (v.L + 1)));
-            Bd[s] = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pbp + (int64_t)t * (v.L + 1)));
+            S.dF(s) = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pfp + (int64_t)t * (v.L + 1)));
+            S.dB(s) = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pbp + (int64_t)t * (v.L + 1)));
         }
-        A[s] = (s >= 1 ? v.a[hi[s - 1] - 1] : v.a[hi[0] - 1]) * micro;
+        S.act(s) = (s >= 1 ? v.a[hi[s - 1] - 1] : v.a[hi[0] - 1]) * micro;
+        int64_t sr = 0;
         if (s + 1 < N) {
             int64_t a = v.a[hi[s] - 1] * micro;
-            SR[s] = a == 0 ? 0 : ceil_div64(a, c.bw[s]);
+            sr = a == 0 ? 0 : ceil_div64(a, c.bw[s]);
         }
+        S.sr(s) = sr;
+        S.f(s) = Rat{0, 1};
     }
     const bool async = kind_async(kind);
-    Rat* fr = B.simbuf + 9 * slot;     // free[N]
-    Rat* rf = fr + N;                  // ringF[N][4]: arrivals on link s -> s+1
-    Rat* rb = rf + 4 * N;              // ringB[N][4]: arrivals on link s+1 -> s
-    for (int s = 0; s < N; ++s) fr[s] = Rat{0, 1};
     for (int64_t p = 0; p < 2 * M && !e.bad(); ++p) {
-        for (int s = 0; s < N; ++s) {
+        bool carry = false;
+        int64_t cm = 0;
+        Rat cv{0, 1};
+        for (int s = 0; s < N; ++s) {             // F ops, ascending
             int64_t w = warmup_depth(kind, N, s + 1);
             if (w > M) w = M;
             StageOp op = op_at(p, w, M);
-            if (!op.is_f) continue;
-            Rat ready = fr[s];
-            if (s > 0) {
-                Rat arr = rf[4 * (s - 1) + (op.m & 3)];
-                if (rat_gt(arr, ready)) ready = arr;
+            bool chain = carry && op.is_f && op.m == cm;
+            bool out = false;
+            Rat ov{0, 1};
+            if (op.is_f) {
+                Rat ready = S.f(s);
+                if (s > 0) {
+                    Rat arr = chain ? cv : S.mf(s);
+                    if (rat_gt(arr, ready)) ready = arr;
+                }
+                Rat end = rat_add(ready, S.dF(s), e);
+                S.f(s) = end;
+                if (s + 1 < N) {
+                    ov = async ? end : rat_add(end, R(S.sr(s)), e);
+                    out = true;
+                }
             }
-            Rat end = rat_add(ready, F[s], e);
-            fr[s] = end;
-            if (s + 1 < N) rf[4 * s + (op.m & 3)] = async ? end : rat_add(end, R(SR[s]), e);
+            if (carry && !chain) S.mf(s) = cv;    // deliver s-1's output to the mailbox
+            carry = out;
+            cm = op.m;
+            cv = ov;
         }
-        for (int s = N - 1; s >= 0; --s) {
+        carry = false;
+        for (int s = N - 1; s >= 0; --s) {        // B ops, descending
             int64_t w = warmup_depth(kind, N, s + 1);
             if (w > M) w = M;
             StageOp op = op_at(p, w, M);
-            if (op.is_f) continue;
-            Rat ready = fr[s];   // >= endF(m, s): F(m, s) ran earlier on this stage
-            if (s + 1 < N) {
-                Rat arr = rb[4 * s + (op.m & 3)];
-                if (rat_gt(arr, ready)) ready = arr;
+            bool chain = carry && !op.is_f && op.m == cm;
+            bool out = false;
+            Rat ov{0, 1};
+            if (!op.is_f) {
+                Rat ready = S.f(s);   // >= endF(m, s): F(m, s) ran earlier on this stage
+                if (s + 1 < N) {
+                    Rat arr = chain ? cv : S.mb(s);
+                    if (rat_gt(arr, ready)) ready = arr;
+                }
+                Rat end = rat_add(ready, S.dB(s), e);
+                S.f(s) = end;
+                if (s > 0) {
+                    ov = async ? end : rat_add(end, R(S.sr(s - 1)), e);
+                    out = true;
+                }
             }
-            Rat end = rat_add(ready, Bd[s], e);
-            fr[s] = end;
-            if (s > 0) rb[4 * (s - 1) + (op.m & 3)] = async ? end : rat_add(end, R(SR[s - 1]), e);
+            if (carry && !chain) S.mb(s) = cv;
+            carry = out;
+            cm = op.m;
+            cv = ov;
         }
     }
     if (e.bad()) { fail(cd, e); return; }
     Rat mk{0, 1};
     for (int s = 0; s < N; ++s)
-        if (rat_gt(fr[s], mk)) mk = fr[s];
+        if (rat_gt(S.f(s), mk)) mk = S.f(s);
     // feature high-water = min(M, depth) * a (simulator.hpp:219-238): the
     // in-flight count on a 1F1B stage peaks right after its warm-up.
     for (int s = 0; s < N; ++s) {
         int64_t w = warmup_depth(kind, N, s + 1);
         if (w > M) w = M;
-        if ((i128)w * A[s] > (i128)INT64_MAX) { e.set(ERR_OVERFLOW); break; }
+        if ((i128)w * S.act(s) > (i128)INT64_MAX) { e.set(ERR_OVERFLOW); break; }
     }
     // link busy fraction Rat(M * SR) / makespan (239-244)
     for (int k = 0; k + 1 < N && !e.bad(); ++k)
-        if (!rat_eq(mk, Rat{0, 1})) (void)rat_div(R(M * SR[k]), mk, e);
+        if (!rat_eq(mk, Rat{0, 1})) (void)rat_div(R(M * S.sr(k)), mk, e);
     if (e.bad()) { fail(cd, e); return; }
     cd.makespan = bp_rat{mk.n, mk.d};
     cd.status = BP_C_OK;

@@ -65,18 +65,68 @@ struct Rat {
 
 BPK_HD Rat R(int64_t v) { return Rat{v, 1}; }
 
-// ---- gcd ---------------------------------------------------------------
-BPK_HD uint64_t gcd_u64(uint64_t u, uint64_t v) {
+// ---- integer helpers ----------------------------------------------------
+// GPUs have no native 64-bit divide; the helpers below keep the common cases
+// (operands below 2^32, exact quotients) off the generic software routines.
+BPK_HD int ctz32(uint32_t x) { return bpk_ffs64((long long)x) - 1; }
+
+BPK_HD uint32_t gcd_u32(uint32_t u, uint32_t v) {
     if (u == 0) return v;
     if (v == 0) return u;
+    int shift = ctz32(u | v);
+    u >>= ctz32(u);
+    do {
+        v >>= ctz32(v);
+        uint32_t lo = u < v ? u : v, hi = u < v ? v : u;
+        u = lo;
+        v = hi - lo;
+    } while (v != 0);
+    return u << shift;
+}
+
+BPK_HD uint64_t umod64(uint64_t a, uint64_t b) {
+    if (((a | b) >> 32) == 0) return (uint32_t)a % (uint32_t)b;
+    return a % b;
+}
+
+BPK_HD uint64_t gcd_u64(uint64_t u, uint64_t v) {
+    if (((u | v) >> 32) == 0) return gcd_u32((uint32_t)u, (uint32_t)v);
+    if (u == 0) return v;
+    if (v == 0) return u;
+    if (u < v) { uint64_t t = u; u = v; v = t; }
+    if ((v >> 32) == 0) {              // one Euclid step brings both below 2^32
+        uint64_t r = umod64(u, v);
+        return r == 0 ? v : gcd_u32((uint32_t)v, (uint32_t)r);
+    }
     int shift = bpk_ffs64((long long)(u | v)) - 1;
     u >>= (bpk_ffs64((long long)u) - 1);
     do {
         v >>= (bpk_ffs64((long long)v) - 1);
-        if (u > v) { uint64_t t = u; u = v; v = t; }
-        v -= u;
+        uint64_t lo = u < v ? u : v, hi = u < v ? v : u;
+        u = lo;
+        v = hi - lo;
     } while (v != 0);
     return u << shift;
+}
+
+// a / g for g dividing a exactly: shift out the twos, multiply by the
+// inverse of the odd part modulo 2^64 (Newton: 3 -> 6 -> 12 -> 24 -> 48 -> 96 bits).
+BPK_HD uint64_t udiv_exact64(uint64_t a, uint64_t g) {
+    if (g == 1) return a;
+    if (((a | g) >> 32) == 0) return (uint32_t)a / (uint32_t)g;
+    int tz = bpk_ffs64((long long)g) - 1;
+    a >>= tz;
+    g >>= tz;
+    uint64_t x = (3 * g) ^ 2;
+    x *= 2 - g * x;
+    x *= 2 - g * x;
+    x *= 2 - g * x;
+    x *= 2 - g * x;
+    return a * x;
+}
+
+BPK_HD int64_t sdiv_exact64(int64_t a, uint64_t g) {
+    return a < 0 ? -(int64_t)udiv_exact64((uint64_t)0 - (uint64_t)a, g) : (int64_t)udiv_exact64((uint64_t)a, g);
 }
 
 BPK_HD int ctz128(u128 x) {
@@ -132,54 +182,69 @@ BPK_HD uint64_t uabs64(int64_t x) {
 }
 
 // Rat(n, d) constructor -> normalize() (rational.hpp:18, 100-106).
-BPK_HD Rat rat_nd(int64_t n, int64_t d, Err& e) {
+BPK_HDNI Rat rat_nd(int64_t n, int64_t d, Err& e) {
     if (d == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
     if (d < 0) { n = -n; d = -d; }
     uint64_t g = gcd_u64(uabs64(n), (uint64_t)d);
-    if (g > 1) { n /= (int64_t)g; d /= (int64_t)g; }
+    if (g > 1) { n = sdiv_exact64(n, g); d = (int64_t)udiv_exact64((uint64_t)d, g); }
     return Rat{n, d};
 }
 
-// a + s*b with s = +1 / -1 (operator+ / operator-).
-BPK_HD Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
+BPK_HD bool fits64(i128 x) { return x <= (i128)INT64_MAX && x >= (i128)INT64_MIN; }
+
+// a + s*b with s = +1 / -1 (operator+ / operator-), Knuth 4.5.1: with
+// g = gcd(a.d, b.d), t = a.n*(b.d/g) + b.n*(a.d/g) and g2 = gcd(t, g) the
+// reduced result is (t/g2) / ((a.d/g)*(b.d/g2)).
+// Out of line on purpose: inlining every Rat operation into the refine and
+// simulator loops produced ~1 MB of SASS and the kernels stalled on
+// instruction fetch (ncu: "no_instruction" 17.5 cycles per issue).
+BPK_HDNI Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
     i128 bn = s > 0 ? (i128)b.n : -(i128)b.n;
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n + bn, 1, e);
     if (a.d == 1) return fit128((i128)a.n * b.d + bn, b.d, e);        // gcd(num, b.d) = 1
     if (b.d == 1) return fit128((i128)bn * a.d + a.n, a.d, e);
     uint64_t g = gcd_u64((uint64_t)a.d, (uint64_t)b.d);
     if (g == 1) return fit128((i128)a.n * b.d + bn * a.d, (i128)a.d * b.d, e);
-    int64_t ad = a.d / (int64_t)g, bd = b.d / (int64_t)g;
+    int64_t ad = (int64_t)udiv_exact64((uint64_t)a.d, g), bd = (int64_t)udiv_exact64((uint64_t)b.d, g);
     i128 t = (i128)a.n * bd + bn * ad;
     if (t == 0) return Rat{0, 1};
-    // g2 = gcd(t, g): reduce t mod g first (g < 2^63)
-    i128 tm = t % (i128)g;
-    uint64_t g2 = gcd_u64(uabs128(tm) > 0 ? (uint64_t)uabs128(tm) : 0, g);
-    if (g2 == 0) g2 = g;  // t divisible by g
-    i128 num = t / (i128)g2;
-    i128 den = (i128)ad * (i128)(b.d / (int64_t)g2);
+    const bool small = fits64(t);
+    uint64_t tm = small ? umod64(uabs64((int64_t)t), g) : (uint64_t)(uabs128(t) % (u128)g);
+    uint64_t g2 = tm == 0 ? g : gcd_u64(tm, g);
+    i128 num = small ? (i128)sdiv_exact64((int64_t)t, g2) : t / (i128)g2;
+    i128 den = (i128)ad * (i128)udiv_exact64((uint64_t)b.d, g2);
     return fit128(num, den, e);
 }
 
-BPK_HD Rat operator_add(Rat a, Rat b, Err& e) { return rat_addsub(a, b, +1, e); }
-
-BPK_HD Rat rat_add(Rat a, Rat b, Err& e) { return rat_addsub(a, b, +1, e); }
-BPK_HD Rat rat_sub(Rat a, Rat b, Err& e) { return rat_addsub(a, b, -1, e); }
+BPK_HD Rat rat_add(Rat a, Rat b, Err& e) {
+    if (a.d == 1 && b.d == 1) return fit128((i128)a.n + b.n, 1, e);
+    return rat_addsub(a, b, +1, e);
+}
+BPK_HD Rat rat_sub(Rat a, Rat b, Err& e) {
+    if (a.d == 1 && b.d == 1) return fit128((i128)a.n - b.n, 1, e);
+    return rat_addsub(a, b, -1, e);
+}
 
 // operator* (rational.hpp:33-35).
-BPK_HD Rat rat_mul(Rat a, Rat b, Err& e) {
+BPK_HDNI Rat rat_mul_nl(Rat a, Rat b, Err& e) {
     if (a.n == 0 || b.n == 0) return Rat{0, 1};
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n * b.n, 1, e);
     uint64_t g1 = (b.d == 1) ? 1 : gcd_u64(uabs64(a.n), (uint64_t)b.d);
     uint64_t g2 = (a.d == 1) ? 1 : gcd_u64(uabs64(b.n), (uint64_t)a.d);
-    int64_t an = g1 > 1 ? a.n / (int64_t)g1 : a.n;
-    int64_t bd = g1 > 1 ? b.d / (int64_t)g1 : b.d;
-    int64_t bn = g2 > 1 ? b.n / (int64_t)g2 : b.n;
-    int64_t ad = g2 > 1 ? a.d / (int64_t)g2 : a.d;
+    int64_t an = sdiv_exact64(a.n, g1);
+    int64_t bd = (int64_t)udiv_exact64((uint64_t)b.d, g1);
+    int64_t bn = sdiv_exact64(b.n, g2);
+    int64_t ad = (int64_t)udiv_exact64((uint64_t)a.d, g2);
     return fit128((i128)an * bn, (i128)ad * bd, e);
 }
 
 // operator/ (rational.hpp:36-39): b == 0 -> domain_error.
-BPK_HD Rat rat_div(Rat a, Rat b, Err& e) {
+BPK_HD Rat rat_mul(Rat a, Rat b, Err& e) {
+    if (a.d == 1 && b.d == 1) return fit128((i128)a.n * b.n, 1, e);
+    return rat_mul_nl(a, b, e);
+}
+
+BPK_HDNI Rat rat_div(Rat a, Rat b, Err& e) {
     if (b.n == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
     // a / b = a * (b.d / b.n); keep the sign on the numerator.
     if (b.n == INT64_MIN) return from128((i128)a.n * b.d, (i128)a.d * b.n, e);

@@ -1,0 +1,381 @@
+// sim.cu -- K4 sim_wavefront: the 1F1B-family schedule simulation
+// (simulator.hpp:81-246) for every candidate that passed its estimate.
+//
+// Fast path (k_sim_fast): a group of G lanes owns one candidate, S stages per
+// lane; time is scaled by D (lcm of the stage denominators) so every event is
+// an exact int64 (sim_classify proves no reference Rat can overflow there).
+// The groups walk the sequence positions p = 0..2M-1 in lockstep.  At each
+// position every stage runs exactly one op (F or B, fixed by its warm-up
+// depth, simulator.hpp:87-100):
+//     endF(m,s) = max(free_s, arrival_F) + F_s     arrival from stage s-1
+//     endB(m,s) = max(free_s, arrival_B) + B_s     arrival from stage s+1
+// An arrival produced at an earlier position waits in a one-slot mailbox
+// (at most one is ever outstanding per link direction); arrivals produced at
+// the same position form a chain along the stages (warm-up F chains, drain B
+// chains).  y_s = max(a_s, y_{s-1} + b_s) is max-plus affine, so a chain is
+// resolved by a segmented inclusive scan over the lanes (shuffles, width G):
+// ascending for F, descending for B.  This is the reference's sorted-op
+// recurrence (the (pos, sub) order is a topological order of the same DAG),
+// computed position-parallel instead of op-serial.
+//
+// Slow path (k_sim_exact): thread per candidate, exact Rat events
+// (phases.cuh:sim_exact), for candidates whose scaled times could exceed int64
+// -- exactly where the reference's Rats might overflow.
+#include "kernels.h"
+#include "phases.cuh"
+
+namespace bpk {
+
+constexpr int64_t NEGV = -((int64_t)1 << 61);   // values stay below 2^61 (sim_classify)
+constexpr int SIM_THREADS = 128;
+
+__device__ __forceinline__ int64_t smax(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int64_t sat(int64_t x) { return x < NEGV ? NEGV : x; }
+
+__global__ void k_sim_prep(BatchDev B) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.ncand) return;
+    int64_t ci = B.cperm[i];
+    int cls = sim_classify(B, ci);
+    if (cls < 0) return;
+    int pos = atomicAdd(&B.sim_count[cls], 1);
+    B.sim_list[(int64_t)cls * B.ncand + pos] = (int32_t)ci;
+}
+
+// ---- exact path scheduling: counting sort of the exact list by
+// (stage count, log2 M), heaviest bucket first, so that the 32 lanes of a
+// warp run candidates with the same N and similar M (same loop structure).
+__device__ __forceinline__ int xbucket(int N, int64_t M) {
+    int lg = 63 - __clzll((long long)M);
+    if (lg > 31) lg = 31;
+    int n = N > 255 ? 255 : N;
+    return XBUCKETS - 1 - (n * 32 + lg);
+}
+
+__global__ void k_xsort_count(BatchDev B) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.sim_count[SIM_EXACT]) return;
+    int32_t ci = B.sim_list[(int64_t)SIM_EXACT * B.ncand + i];
+    int k = xbucket(B.cand[ci].n_stages, B.cand[ci].M);
+    B.xkey[i] = k;
+    atomicAdd(&B.xhist[k], 1);
+}
+
+__global__ void __launch_bounds__(1024) k_xsort_scan(BatchDev B) {
+    __shared__ int32_t part[1024];
+    const int per = XBUCKETS / 1024;
+    int base = threadIdx.x * per, s = 0;
+    for (int k = 0; k < per; ++k) s += B.xhist[base + k];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    int run = part[threadIdx.x] - s;   // exclusive
+    for (int k = 0; k < per; ++k) {
+        int c = B.xhist[base + k];
+        B.xhist[base + k] = run;
+        run += c;
+    }
+}
+
+__global__ void k_xsort_scatter(BatchDev B) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.sim_count[SIM_EXACT]) return;
+    int pos = atomicAdd(&B.xhist[B.xkey[i]], 1);
+    B.xsorted[pos] = B.sim_list[(int64_t)SIM_EXACT * B.ncand + i];
+}
+
+// Persistent warps walk the sorted exact list in chunks of 32; each lane runs
+// one candidate's exact simulation with its per-stage state interleaved
+// across the warp (element (s, lane) at s*32 + lane: coalesced accesses).
+__global__ void __launch_bounds__(256) k_sim_exact(BatchDev B) {
+    const int count = B.sim_count[SIM_EXACT];
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t per_stage = 32;                    // lanes interleaved
+    const int64_t arr = per_stage * (int64_t)B.max_N; // one array of a warp's state
+    Rat* base = B.simbuf + warp * 5 * arr;
+    int64_t* ibase = reinterpret_cast<int64_t*>(B.simbuf + nwarps * 5 * arr) + warp * 2 * arr;
+    SimState S{base + lane, base + arr + lane, base + 2 * arr + lane, base + 3 * arr + lane, base + 4 * arr + lane,
+               ibase + lane, ibase + arr + lane, 32};
+    for (int64_t chunk = warp; chunk * 32 < count; chunk += nwarps) {
+        int64_t i = chunk * 32 + lane;
+        if (i < count) sim_exact(B, B.xsorted[i], S);
+    }
+}
+
+template <int G, int S>
+__global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
+    const unsigned FULL = 0xffffffffu;
+    const int count = B.sim_count[cls];
+    const int lane = threadIdx.x & 31;
+    const int r = lane % G;
+    const int gpw = 32 / G;
+    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
+    const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+    // persistent: each warp walks groups base, base + warps_total*gpw, ...
+    for (int64_t base = warp_global * gpw; base < count; base += warps_total * gpw) {
+    const int64_t gid = base + lane / G;
+    const bool active = gid < count;
+    int64_t ci = active ? B.sim_list[(int64_t)cls * B.ncand + gid] : -1;
+    int N = 1, kind = 0;
+    int64_t M = 0, micro = 1, D = 1;
+    bool async = true;
+    int64_t Fd[S], Bd[S], SRin[S], SRout[S], fr[S], pF[S], pB[S], A[S];
+    int64_t wv[S], wprev[S], wnext[S];
+    bool has[S];
+#pragma unroll
+    for (int i = 0; i < S; ++i) {
+        has[i] = false;
+        Fd[i] = Bd[i] = SRin[i] = SRout[i] = fr[i] = A[i] = 0;
+        pF[i] = pB[i] = NEGV;
+        wv[i] = wprev[i] = wnext[i] = 0;
+    }
+    int64_t slot = 0, qo = 0;
+    int plan_kind = PLAN_WHOLE;
+    if (active) {
+        const bp_candidate& cd = B.cand[ci];
+        const CState cs = B.cs[ci];
+        const int qi = B.cq[ci];
+        const QDesc Q = B.q[qi];
+        N = Q.N;
+        kind = cd.kind;
+        M = cd.M;
+        micro = cd.micro;
+        D = cs.D;
+        async = kind_async(kind);
+        plan_kind = cs.plan_kind;
+        NetView v = net_view(B.P, Q.net);
+        ChainView c = chain_view(B.P, Q.cl, N);
+        slot = Q.stage_off + (ci - Q.cand_off) * N;
+        qo = Q.qstage_off;
+        const int32_t* hi = plan_kind == PLAN_REFINED ? B.qhi + qo : B.chi + slot;
+        const int32_t* lo = plan_kind == PLAN_REFINED ? B.qlo + qo : B.clo + slot;
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            const int s = r * S + i;
+            if (s >= N) continue;
+            has[i] = true;
+            if (plan_kind == PLAN_REFINED) {
+                Rat f = B.qF[qo + s], b = B.qB[qo + s];
+                Fd[i] = f.n * (D / f.d);
+                Bd[i] = b.n * (D / b.d);
+            } else {
+                int32_t t = c.type[s];
+                Fd[i] = stage_sum_whole(lo[s], hi[s], v.Pfp + (int64_t)t * (v.L + 1));
+                Bd[i] = stage_sum_whole(lo[s], hi[s], v.Pbp + (int64_t)t * (v.L + 1));
+            }
+            if (s > 0) {
+                int64_t a = v.a[hi[s - 1] - 1] * micro;
+                SRin[i] = (a == 0 ? 0 : ceil_div64(a, c.bw[s - 1])) * D;
+                A[i] = a;
+            } else {
+                A[i] = v.a[hi[0] - 1] * micro;
+            }
+            if (s + 1 < N) {
+                int64_t a = v.a[hi[s] - 1] * micro;
+                SRout[i] = (a == 0 ? 0 : ceil_div64(a, c.bw[s])) * D;
+            }
+            int64_t w = warmup_depth(kind, N, s + 1);
+            wv[i] = w < M ? w : M;
+            if (s > 0) { w = warmup_depth(kind, N, s); wprev[i] = w < M ? w : M; }
+            if (s + 1 < N) { w = warmup_depth(kind, N, s + 2); wnext[i] = w < M ? w : M; }
+        }
+    }
+    int64_t Mloop = active ? M : 0;
+    for (int o = 16; o > 0; o >>= 1) Mloop = smax(Mloop, __shfl_xor_sync(FULL, Mloop, o));
+    const int64_t syncF = async ? 0 : 1;
+    for (int64_t p = 0; p < 2 * Mloop; ++p) {
+        const bool live = active && p < 2 * M;
+        bool isF[S], isB[S], chF[S], chB[S];
+        int64_t mm[S];
+        bool anyF = false, anyB = false;
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            isF[i] = isB[i] = chF[i] = chB[i] = false;
+            mm[i] = 0;
+            if (has[i] && live) {
+                const int s = r * S + i;
+                StageOp op = op_at(p, wv[i], M);
+                mm[i] = op.m;
+                isF[i] = op.is_f;
+                isB[i] = !op.is_f;
+                if (isF[i] && s > 0) {
+                    StageOp q = op_at(p, wprev[i], M);
+                    chF[i] = q.is_f && q.m == op.m;
+                }
+                if (isB[i] && s + 1 < N) {
+                    StageOp q = op_at(p, wnext[i], M);
+                    chB[i] = !q.is_f && q.m == op.m;
+                }
+            }
+            anyF |= chF[i];
+            anyB |= chB[i];
+        }
+        const unsigned balF = __ballot_sync(FULL, anyF), balB = __ballot_sync(FULL, anyB);
+        // ---- forward ops (ascending stages)
+        int64_t eF[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            const int s = r * S + i;
+            int64_t dep = (isF[i] && !chF[i] && s > 0) ? pF[i] : NEGV;
+            eF[i] = isF[i] ? smax(fr[i], dep) + Fd[i] : NEGV;
+        }
+        if (balF) {
+            // local inclusive composition of f_i(y) = max(a_i, y + b_i)
+            int64_t cA[S], cB[S];
+#pragma unroll
+            for (int i = 0; i < S; ++i) {
+                int64_t a = eF[i];
+                int64_t b = chF[i] ? SRin[i] * syncF + Fd[i] : NEGV;
+                if (i == 0) { cA[i] = a; cB[i] = b; }
+                else { cA[i] = smax(a, sat(cA[i - 1] + b)); cB[i] = sat(cB[i - 1] + b); }
+            }
+            int64_t gA = cA[S - 1], gB = cB[S - 1];
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {
+                int64_t pa = __shfl_up_sync(FULL, gA, o, G), pb = __shfl_up_sync(FULL, gB, o, G);
+                if (r >= o) { gA = smax(gA, sat(pa + gB)); gB = sat(pb + gB); }
+            }
+            int64_t xA = __shfl_up_sync(FULL, gA, 1, G);
+            if (r == 0) xA = NEGV;
+#pragma unroll
+            for (int i = 0; i < S; ++i) eF[i] = smax(cA[i], sat(xA + cB[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+            if (isF[i]) fr[i] = eF[i];
+        // ---- backward ops (descending stages)
+        int64_t eB[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            const int s = r * S + i;
+            int64_t dep = (isB[i] && !chB[i] && s + 1 < N) ? pB[i] : NEGV;
+            eB[i] = isB[i] ? smax(fr[i], dep) + Bd[i] : NEGV;
+        }
+        if (balB) {
+            int64_t cA[S], cB[S];
+#pragma unroll
+            for (int i = S - 1; i >= 0; --i) {
+                int64_t a = eB[i];
+                int64_t b = chB[i] ? SRout[i] * syncF + Bd[i] : NEGV;
+                if (i == S - 1) { cA[i] = a; cB[i] = b; }
+                else { cA[i] = smax(a, sat(cA[i + 1] + b)); cB[i] = sat(cB[i + 1] + b); }
+            }
+            int64_t gA = cA[0], gB = cB[0];
+#pragma unroll
+            for (int o = 1; o < G; o <<= 1) {
+                int64_t pa = __shfl_down_sync(FULL, gA, o, G), pb = __shfl_down_sync(FULL, gB, o, G);
+                if (r + o < G) { gA = smax(gA, sat(pa + gB)); gB = sat(pb + gB); }
+            }
+            int64_t xA = __shfl_down_sync(FULL, gA, 1, G);
+            if (r == G - 1) xA = NEGV;
+#pragma unroll
+            for (int i = 0; i < S; ++i) eB[i] = smax(cA[i], sat(xA + cB[i]));
+        }
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+            if (isB[i]) fr[i] = eB[i];
+        // ---- mailboxes: F from stage s-1, B from stage s+1
+        {
+            int64_t vF = isF[S - 1] ? eF[S - 1] + SRout[S - 1] * syncF : 0;
+            int64_t mF = isF[S - 1] ? mm[S - 1] : -1;
+            int64_t inF = __shfl_up_sync(FULL, vF, 1, G), inFm = __shfl_up_sync(FULL, mF, 1, G);
+            int64_t vB = isB[0] ? eB[0] + SRin[0] * syncF : 0;
+            int64_t mB = isB[0] ? mm[0] : -1;
+            int64_t inB = __shfl_down_sync(FULL, vB, 1, G), inBm = __shfl_down_sync(FULL, mB, 1, G);
+#pragma unroll
+            for (int i = 0; i < S; ++i) {
+                const int s = r * S + i;
+                if (!has[i] || !live) continue;
+                // from s-1
+                int64_t v_in, m_in;
+                if (i > 0) { v_in = isF[i - 1] ? eF[i - 1] + SRout[i - 1] * syncF : 0; m_in = isF[i - 1] ? mm[i - 1] : -1; }
+                else { v_in = inF; m_in = r > 0 ? inFm : -1; }
+                if (s > 0 && m_in >= 0 && !(chF[i] && mm[i] == m_in)) pF[i] = v_in;
+                // from s+1
+                if (i + 1 < S) { v_in = isB[i + 1] ? eB[i + 1] + SRin[i + 1] * syncF : 0; m_in = isB[i + 1] ? mm[i + 1] : -1; }
+                else { v_in = inB; m_in = r + 1 < G ? inBm : -1; }
+                if (s + 1 < N && m_in >= 0 && !(chB[i] && mm[i] == m_in)) pB[i] = v_in;
+            }
+        }
+    }
+    // ---- makespan (simulator.hpp:173-180) and the post-simulation Rat checks
+    int64_t X = 0;
+#pragma unroll
+    for (int i = 0; i < S; ++i)
+        if (has[i]) X = smax(X, fr[i]);
+    for (int o = 1; o < G; o <<= 1) X = smax(X, __shfl_xor_sync(FULL, X, o, G));
+    Err e{ERR_NONE};
+    Rat mk{0, 1};
+    if (active) {
+        uint64_t g = gcd_u64((uint64_t)X, (uint64_t)D);
+        mk = Rat{X / (int64_t)g, D / (int64_t)g};
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            const int s = r * S + i;
+            if (!has[i]) continue;
+            // feature high-water: min(M, depth) * a (219-238)
+            if ((i128)wv[i] * A[i] > (i128)INT64_MAX) e.set(ERR_OVERFLOW);
+            // busy fraction Rat(M * SR) / makespan (239-244)
+            if (s + 1 < N && mk.n != 0) (void)rat_div(R(M * (SRout[i] / D)), mk, e);
+        }
+    }
+    unsigned bad = __ballot_sync(FULL, e.bad());
+    if (active && r == 0) {
+        bp_candidate& cd = B.cand[ci];
+        const unsigned gm = ((1u << G) - 1u) << (lane - r);
+        if (bad & (G == 32 ? FULL : gm)) {
+            cd.status = BP_C_ERR_OVERFLOW;
+        } else {
+            cd.makespan = bp_rat{mk.n, mk.d};
+            cd.status = BP_C_OK;
+        }
+    }
+    }  // persistent loop
+}
+
+static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
+
+void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
+    cudaMemsetAsync(B.sim_count, 0, SIM_CLASSES * sizeof(int32_t), st);
+    if (B.ncand) k_sim_prep<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+}
+
+void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st) {
+    const int grid = sms * 8;   // persistent warps
+    switch (cls) {
+        case 0: k_sim_fast<2, 1><<<grid, SIM_THREADS, 0, st>>>(B, 0); break;
+        case 1: k_sim_fast<4, 1><<<grid, SIM_THREADS, 0, st>>>(B, 1); break;
+        case 2: k_sim_fast<8, 1><<<grid, SIM_THREADS, 0, st>>>(B, 2); break;
+        case 3: k_sim_fast<16, 1><<<grid, SIM_THREADS, 0, st>>>(B, 3); break;
+        case 4: k_sim_fast<32, 1><<<grid, SIM_THREADS, 0, st>>>(B, 4); break;
+        case 5: k_sim_fast<32, 2><<<grid, SIM_THREADS, 0, st>>>(B, 5); break;
+        case 6: k_sim_fast<32, 4><<<grid, SIM_THREADS, 0, st>>>(B, 6); break;
+        case 7: k_sim_fast<32, 8><<<grid, SIM_THREADS, 0, st>>>(B, 7); break;
+        default: break;
+    }
+}
+
+// Bytes of exact-simulator state for `sms` SMs (5 Rat + 2 int64 arrays per
+// stage per lane per persistent warp).
+size_t sim_exact_state_bytes(int sms, int max_N) {
+    const size_t warps = (size_t)sms * XSIM_WARPS_PER_SM;
+    return warps * 32 * (size_t)(max_N > 0 ? max_N : 1) * (5 * sizeof(Rat) + 2 * sizeof(int64_t));
+}
+
+void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st) {
+    if (!B.ncand) return;
+    cudaMemsetAsync(B.xhist, 0, XBUCKETS * sizeof(int32_t), st);
+    k_xsort_count<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);
+    k_xsort_scan<<<1, 1024, 0, st>>>(B);
+    k_xsort_scatter<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);
+    k_sim_exact<<<sms * XSIM_WARPS_PER_SM / 8, 256, 0, st>>>(B);
+}
+
+}  // namespace bpk

@@ -184,7 +184,44 @@ class Problem:
     def c_queries(self):
         return self.queries.ctypes.data_as(C.POINTER(abi.bp_query))
 
-    def alloc_outputs(self, details=True):
+    def pin(self):
+        """Move every host array into page-locked memory (torch pinned
+        buffers) so host<->device copies run at full PCIe/NVLink-C2C rate."""
+        import torch
+
+        def pinned(a):
+            if a.dtype.names is None:
+                t = torch.empty(a.shape, dtype=getattr(torch, a.dtype.name), pin_memory=True)
+                out = t.numpy()
+            else:
+                t = torch.empty(max(a.nbytes, 1), dtype=torch.uint8, pin_memory=True)
+                out = t.numpy()[:a.nbytes].view(a.dtype).reshape(a.shape)
+            out[...] = a
+            self._pinned.append(t)
+            return out
+
+        self._pinned = []
+        for n in self.networks:
+            n.fp, n.bp, n.w, n.a = pinned(n.fp), pinned(n.bp), pinned(n.w), pinned(n.a)
+        for c in self.clusters:
+            c.types, c.cap, c.bw, c.min_micro = pinned(c.types), pinned(c.cap), pinned(c.bw), pinned(c.min_micro)
+        ml = [pinned(m) for m in self.m_lists]
+        q = pinned(self.queries)
+        j = 0
+        for i in range(q.size):
+            if q["n_m"][i] > 0:
+                q["m_list"][i] = ml[j].ctypes.data
+                j += 1
+        self.m_lists, self.queries = ml, q
+        return self
+
+    def alloc_outputs(self, details=True, pinned=False):
+        if pinned:
+            import torch
+            r = torch.empty(self.queries.size * RESULT_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
+            self._pinned_res = r
+            res = r.numpy().view(RESULT_DTYPE)
+            return res, None, None
         res = np.zeros(self.queries.size, dtype=RESULT_DTYPE)
         cand = np.zeros(self.total_candidates, dtype=CAND_DTYPE) if details else None
         st = np.zeros(self.total_stages, dtype=STAGE_DTYPE) if details else None

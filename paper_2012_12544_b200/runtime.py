@@ -89,6 +89,11 @@ class Explorer:
     def launches(self) -> int:
         return int(self.lib.bp_launch_count(self.ctx))
 
+    def transfers(self):
+        h, d = C.c_int64(0), C.c_int64(0)
+        self.lib.bp_transfer_stats(self.ctx, C.byref(h), C.byref(d))
+        return h.value, d.value
+
     def profiling(self, on=True):
         self.lib.bp_set_profiling(self.ctx, 1 if on else 0)
 

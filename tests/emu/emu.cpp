@@ -4,6 +4,8 @@
 // batch entry point.  It lets tests/test_emu.py check the exact-emulation
 // logic against the reference without a GPU; the product itself only ever
 // runs these phases inside CUDA kernels (libbapipe_b200.so).
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -225,7 +227,25 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
             if (bottleneck_slot(B, i, m)) host_partition(B, DPItem{i, m, B.ms[HB.q[i].mslot_off + m].a_th}, work);
     for (int i = 0; i < nq; ++i) refine_query(B, i);
     for (int64_t c = 0; c < HB.ncand; ++c) prune_candidate(B, c);
-    for (int64_t c = 0; c < HB.ncand; ++c) sim_exact(B, c);
+    int64_t exact_n = 0, exact_ovf = 0, fast_n = 0;
+    const size_t mn = (size_t)std::max(1, HB.max_N);
+    std::vector<Rat> s_fr(mn), s_pf(mn), s_pb(mn), s_f(mn), s_b(mn);
+    std::vector<int64_t> s_sr(mn), s_a(mn);
+    SimState S{s_fr.data(), s_pf.data(), s_pb.data(), s_f.data(), s_b.data(), s_sr.data(), s_a.data(), 1};
+    for (int64_t c = 0; c < HB.ncand; ++c) {
+        int cls = sim_classify(B, c);
+        if (cls < 0) continue;
+        sim_exact(B, c, S);
+        if (cls == SIM_EXACT) {
+            ++exact_n;
+            exact_ovf += B.cand[c].status == BP_C_ERR_OVERFLOW;
+        } else {
+            ++fast_n;
+        }
+    }
+    if (getenv("BPEMU_STATS"))
+        fprintf(stderr, "emu sim: fast %lld exact %lld (overflow %lld)\n", (long long)fast_n, (long long)exact_n,
+                (long long)exact_ovf);
     for (int i = 0; i < nq; ++i) rank_query(B, i);
     std::memcpy(res, B.res, sizeof(bp_query_result) * (size_t)nq);
     if (cand) std::memcpy(cand, B.cand, sizeof(bp_candidate) * (size_t)HB.ncand);
