@@ -1,0 +1,107 @@
+"""Parity of the CUDA product (libbapipe_b200.so, sm_100a) with the reference.
+
+Every test calls through the C ABI.  Bit-exact on every output record: cut
+points, fractions, schedule kind, M, ranked order, rejection reasons, exact
+rational makespan / estimate / memory / bandwidth values, and the query
+outcome (including the reference's overflow_error / InvalidPlan escapes and
+its undefined-behaviour cases, which must be reported, not computed).
+"""
+import os
+
+import numpy as np
+import pytest
+import scenarios
+from conftest import ROOT, assert_same
+
+from paper_2012_12544_b200 import workloads as W
+from paper_2012_12544_b200.problem import BEST_DTYPE, RESULT_DTYPE
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ex():
+    from paper_2012_12544_b200.runtime import Explorer
+    e = Explorer(0)
+    yield e
+    e.close()
+
+
+@pytest.fixture(scope="module")
+def c5(ex):
+    p = W.config_c5()
+    res, cand, _ = ex.explore(p, details=False)
+    return p, res
+
+
+@pytest.mark.parametrize("name", [n for n, _ in scenarios.SCENARIOS])
+def test_product_matches_reference_fixtures(ex, golden, name):
+    p = scenarios.build(name)
+    res, cand, st = ex.explore(p, details=True)
+    g = golden[name]
+    assert_same(res, g["res"], name + "/res")
+    assert_same(cand, g["cand"], name + "/cand")
+    if "stages" in g:
+        assert_same(st, g["stages"], name + "/stages")
+
+
+@pytest.mark.parametrize("seed", [31, 32, 33])
+def test_product_matches_oracle_on_random_batches(ex, port, seed):
+    p = W.random_problem(seed, n_queries=120, max_L=40, max_N=16, cap_range=(500, 80000), bw_range=(1, 800),
+                         act_max=3000)
+    for x, y, part in zip(ex.explore(p), port.explore(p), ("res", "cand", "stages")):
+        assert_same(x, y, f"seed {seed} {part}")
+
+
+def test_full_c5_sweep_matches_reference(c5):
+    """All 65,536 queries of the 2^20-candidate sweep against the reference's
+    own explore() run on the full sweep (tests/golden/make_c5_full.py)."""
+    path = os.path.join(ROOT, "tests", "golden", "c5_full_ref.npz")
+    if not os.path.exists(path):
+        pytest.skip("c5_full_ref.npz not generated")
+    p, res = c5
+    want = np.load(path)["res"].view(RESULT_DTYPE)
+    assert np.array_equal(res["status"], want["status"])
+    ok = want["status"] == 0
+    for f in ("best_kind", "best_M", "best_micro", "best_makespan", "best_peak_memory", "best_max_bw"):
+        assert res[f][ok].tobytes() == want[f][ok].tobytes(), f
+
+
+def test_full_c5_sweep_properties(ex, c5):
+    """Size-independent properties at full size: determinism, the split
+    (device-resident) API agrees with the host API, every ranked list is
+    sorted by the reference's 5 keys, and the device best-record reduction
+    matches its host mirror."""
+    p, res = c5
+    res2, _, _ = ex.explore(p, details=False)
+    assert res.tobytes() == res2.tobytes()
+    b = ex.prepare(p, details=False)
+    ex.run(b)
+    res3, _, _ = ex.fetch(b, p)
+    assert res.tobytes() == res3.tobytes()
+    import torch
+
+    from paper_2012_12544_b200.sweep import best_record_from_results
+    rec = torch.zeros(BEST_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
+    ex.best(b, rec.data_ptr())
+    torch.cuda.synchronize()
+    sub = np.arange(0, p.queries.size)
+    want = best_record_from_results(res, sub)
+    assert rec.cpu().numpy().tobytes() == want.tobytes()
+    ex.free(b)
+
+
+def test_ranked_lists_sorted_on_c5_sample(ex):
+    from fractions import Fraction as Fr
+    p = scenarios.c5_sample(257)
+    res, cand, _ = ex.explore(p, details=False)
+    for qi in range(p.queries.size):
+        lo = int(p.queries["cand_offset"][qi])
+        cs = cand[lo:lo + int(p.n_candidates[qi])]
+        ranked = sorted([c for c in cs if c["rank"] >= 0], key=lambda c: c["rank"])
+        keys = [(Fr(int(c["makespan"]["num"]), int(c["makespan"]["den"])),
+                 Fr(int(c["peak_memory"]["num"]), int(c["peak_memory"]["den"])),
+                 Fr(int(c["max_bw_demand"]["num"]), int(c["max_bw_demand"]["den"])), int(c["M"]), int(c["kind"]))
+                for c in ranked]
+        assert keys == sorted(keys)
+        assert (res[qi]["status"] == 0) == bool(ranked)
