@@ -27,7 +27,7 @@ struct QState {
     int32_t refine_err;    // Err code of refine + refined-plan stage sums
     int32_t refined;       // refine ran
     int64_t target;        // max stage compute time of the DP plan (integer)
-    int64_t refine_iters;
+    int64_t refine_iters, refine_evals, refine_moves, refine_exact;
     // validate_plan (plan.hpp:41-85) of the refined plan, raised at simulate()
     int32_t vcode;         // BP_IP_* or 0
     int32_t verr;          // Err code of the coverage Rat sums

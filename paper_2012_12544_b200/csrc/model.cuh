@@ -357,10 +357,83 @@ BPK_HD void stage_times(const NetView& v, const ChainView& c, int s, const int32
     B = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pbp + (int64_t)t * (v.L + 1), e);
 }
 
+// One boundary step of intra_layer_refine (partition.hpp:302-327) decided on
+// scaled integers.  With D = lcm(den t_hi, den t_lo), every Rat the reference
+// forms in the step (t_hi - t_lo, x, x*1024, the quantization scores, t -
+// x*c) has a value whose denominator divides D*cs, D*1024 or D*den(x); when
+// those scales and the scaled numerators stay below 2^62, no reduced value
+// can exceed int64, so the reference cannot overflow and the decisions can
+// be made with integer compares.  Returns FS_FALLBACK when a bound fails (the
+// caller then runs the exact Rat step), FS_NOMOVE, or FS_MOVE with the
+// reduced x and the two new stage times.  ~4 gcds instead of ~60.
+enum { FS_FALLBACK = 0, FS_NOMOVE = 1, FS_MOVE = 2 };
+
+BPK_HD Rat reduce_pos(i128 n, i128 d) {       // n >= 0, d > 0, both < 2^62
+    uint64_t g = gcd_u64((uint64_t)n, (uint64_t)d);
+    return Rat{(int64_t)udiv_exact64((uint64_t)n, g), (int64_t)udiv_exact64((uint64_t)d, g)};
+}
+
+BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh, Rat& nl) {
+    const i128 B62 = (i128)1 << 62;
+    if (t_hi.n < 0 || t_lo.n < 0 || avail.n <= 0) return FS_FALLBACK;
+    const uint64_t g = gcd_u64((uint64_t)t_hi.d, (uint64_t)t_lo.d);
+    const int64_t mh = (int64_t)udiv_exact64((uint64_t)t_lo.d, g), ml = (int64_t)udiv_exact64((uint64_t)t_hi.d, g);
+    const i128 D = (i128)t_hi.d * mh;
+    const int64_t cs = c_from + c_to;
+    if (D * cs >= B62 || D * 1024 >= B62) return FS_FALLBACK;
+    const i128 Th = (i128)t_hi.n * mh, Tl = (i128)t_lo.n * ml;
+    if (Th >= B62 || Tl >= B62) return FS_FALLBACK;
+    // x = (t_hi - t_lo) / (c_from + c_to), reduced
+    x = reduce_pos(Th - Tl, D * cs);
+    if (!rat_lt(x, avail)) {
+        // x = avail - Rat(1, 1024)
+        if ((i128)avail.d * 1024 >= B62 || (i128)avail.n * 1024 >= B62) return FS_FALLBACK;
+        Err le{ERR_NONE};
+        x = rat_sub(avail, Rat{1, 1024}, le);
+        if (le.bad()) return FS_FALLBACK;
+        if (x.n <= 0) return FS_NOMOVE;
+    }
+    if (x.d > 1024) {                                     // quantize (257-265)
+        if ((i128)x.n * 1024 >= B62) return FS_FALLBACK;
+        const int64_t num = x.n * 1024;
+        const int64_t k = num / x.d, kc = k + (num % x.d != 0 ? 1 : 0);
+        Err le{ERR_NONE};
+        const Rat qlo = rat_nd(k, 1024, le), qhi = rat_nd(kc, 1024, le);
+        if (rat_ge(qhi, avail)) {
+            x = qlo;
+        } else {
+            // score(f) = max(t_hi - f*c_from, t_lo + f*c_to), all scaled by D*1024
+            const i128 a1 = Th * 1024 - (i128)k * c_from * D, a2 = Tl * 1024 + (i128)k * c_to * D;
+            const i128 b1 = Th * 1024 - (i128)kc * c_from * D, b2 = Tl * 1024 + (i128)kc * c_to * D;
+            if (a1 >= B62 || a2 >= B62 || b1 >= B62 || b2 >= B62 || a1 <= -B62 || b1 <= -B62) return FS_FALLBACK;
+            const i128 s_lo = a1 > a2 ? a1 : a2, s_hi = b1 > b2 ? b1 : b2;
+            x = s_lo <= s_hi ? qlo : qhi;
+        }
+    }
+    if (x.n <= 0 || !rat_lt(x, avail)) return FS_NOMOVE;
+    // acceptance: max(t_hi - x*c_from, t_lo + x*c_to) < t_hi, scaled by D*den(x)
+    const i128 Dx = D * x.d;
+    if (Dx >= B62 || (i128)x.n * c_from >= B62 || (i128)x.n * c_to >= B62) return FS_FALLBACK;
+    const i128 TH = Th * x.d, NH = TH - (i128)x.n * c_from * D, NL = Tl * x.d + (i128)x.n * c_to * D;
+    if (TH >= B62 || NL >= B62 || NH <= -B62) return FS_FALLBACK;
+    if ((NH > NL ? NH : NL) >= TH) return FS_NOMOVE;
+    if (NH < 0) return FS_FALLBACK;
+    nh = reduce_pos(NH, Dx);
+    nl = reduce_pos(NL, Dx);
+    return FS_MOVE;
+}
+
+// True when recomputing the stage time from the plan (stage_fp_time +
+// stage_bp_time, plan.hpp:90-113) cannot overflow: every partial sum is at
+// most t and its reduced denominator divides den(lead) * den(trail).
+BPK_HD bool stage_time_safe(Rat t, Rat lead, Rat trail) {
+    return (i128)t.n * lead.d * trail.d < ((i128)1 << 62) * t.d;
+}
+
 BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail,
-                       Rat* tF, Rat* tB, Rat* tT, uint8_t* dirty, int* iters, Err& e) {
+                       Rat* tF, Rat* tB, Rat* tT, uint8_t* dirty, int64_t* stats, Err& e) {
     const int N = c.N;
-    *iters = 0;
+    stats[0] = stats[1] = stats[2] = stats[3] = 0;   // iterations, evaluated steps, moves, exact steps
     if (N <= 1) return;
     for (int s = 0; s < N; ++s) dirty[s] = 1;
     const Rat zero{0, 1};
@@ -381,12 +454,13 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
     int guard = 0;
     while (changed && ++guard < 1000) {
         changed = false;
-        ++*iters;
+        ++stats[0];
         for (int pass = 0; pass < 2; ++pass) {
             for (int i = 0; i < N - 1; ++i) {
                 int n0 = (pass == 0) ? i : (N - 2 - i);
                 if (dirty[n0] & 2) continue;
                 dirty[n0] |= 2;   // cleared below if this step moves
+                ++stats[1];
                 Rat t_a = T(n0);
                 if (e.bad()) return;
                 Rat t_b = T(n0 + 1);
@@ -407,37 +481,44 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
                 int64_t c_from = fpbp_at(v, j, c.type[from]);
                 int64_t c_to = fpbp_at(v, j, c.type[to]);
                 Rat t_hi = rat_max(t_a, t_b), t_lo = rat_min(t_a, t_b);
-                Rat x = rat_div(rat_sub(t_hi, t_lo, e), rat_add(R(c_from), R(c_to), e), e);
                 // avail = owned_fraction(from, j) (plan.hpp:33-39)
                 Rat avail;
                 if (lo[from] == hi[from]) avail = rat_sub(rat_add(lead[from], trail[from], e), R(1), e);
                 else if (j == lo[from]) avail = lead[from];
                 else avail = trail[from];
-                if (rat_ge(x, avail)) x = rat_sub(avail, step, e);
                 if (e.bad()) return;
-                if (!rat_gt(x, zero)) continue;
-                // quantize (257-265)
-                if (x.d > 1024) {
-                    Rat y = rat_mul(x, R(1024), e);
+                Rat x, nh, nl;
+                const int fs = refine_fast_step(t_hi, t_lo, c_from, c_to, avail, x, nh, nl);
+                if (fs == FS_NOMOVE) continue;
+                if (fs == FS_FALLBACK) {                   // the reference's Rat step, verbatim
+                    ++stats[3];
+                    x = rat_div(rat_sub(t_hi, t_lo, e), rat_add(R(c_from), R(c_to), e), e);
+                    if (rat_ge(x, avail)) x = rat_sub(avail, step, e);
                     if (e.bad()) return;
-                    Rat qlo = rat_nd(rat_floor(y), 1024, e);
-                    Rat qhi = rat_nd(rat_ceil(y), 1024, e);
-                    if (rat_ge(qhi, avail)) {
-                        x = qlo;
-                    } else {
-                        Rat s_lo = rat_max(rat_sub(t_hi, rat_mul(qlo, R(c_from), e), e),
-                                           rat_add(t_lo, rat_mul(qlo, R(c_to), e), e));
-                        Rat s_hi = rat_max(rat_sub(t_hi, rat_mul(qhi, R(c_from), e), e),
-                                           rat_add(t_lo, rat_mul(qhi, R(c_to), e), e));
+                    if (!rat_gt(x, zero)) continue;
+                    // quantize (257-265)
+                    if (x.d > 1024) {
+                        Rat y = rat_mul(x, R(1024), e);
                         if (e.bad()) return;
-                        x = rat_le(s_lo, s_hi) ? qlo : qhi;
+                        Rat qlo = rat_nd(rat_floor(y), 1024, e);
+                        Rat qhi = rat_nd(rat_ceil(y), 1024, e);
+                        if (rat_ge(qhi, avail)) {
+                            x = qlo;
+                        } else {
+                            Rat s_lo = rat_max(rat_sub(t_hi, rat_mul(qlo, R(c_from), e), e),
+                                               rat_add(t_lo, rat_mul(qlo, R(c_to), e), e));
+                            Rat s_hi = rat_max(rat_sub(t_hi, rat_mul(qhi, R(c_from), e), e),
+                                               rat_add(t_lo, rat_mul(qhi, R(c_to), e), e));
+                            if (e.bad()) return;
+                            x = rat_le(s_lo, s_hi) ? qlo : qhi;
+                        }
                     }
+                    if (!rat_gt(x, zero) || rat_ge(x, avail)) continue;
+                    nh = rat_sub(t_hi, rat_mul(x, R(c_from), e), e);
+                    nl = rat_add(t_lo, rat_mul(x, R(c_to), e), e);
+                    if (e.bad()) return;
+                    if (rat_ge(rat_max(nh, nl), t_hi)) continue;
                 }
-                if (!rat_gt(x, zero) || rat_ge(x, avail)) continue;
-                Rat nh = rat_sub(t_hi, rat_mul(x, R(c_from), e), e);
-                Rat nl = rat_add(t_lo, rat_mul(x, R(c_to), e), e);
-                if (e.bad()) return;
-                if (rat_ge(rat_max(nh, nl), t_hi)) continue;
                 // apply_move (269-292)
                 int a = n0, b = n0 + 1;
                 if (dir > 0) {
@@ -462,7 +543,14 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
                 if (e.bad()) return;
                 dirty[a] = dirty[b] = 1;                 // stage times stale, boundaries a, b unstable
                 if (a > 0) dirty[a - 1] &= 1;            // boundary a-1 touches stage a
+                // The new stage times are nh (from) and nl (to) exactly; keep
+                // them unless recomputing from the plan could overflow, in
+                // which case the lazy exact recomputation decides (as the
+                // reference does at its next use).
+                if (stage_time_safe(nh, lead[from], trail[from])) { tT[from] = nh; dirty[from] &= (uint8_t)~1u; }
+                if (stage_time_safe(nl, lead[to], trail[to])) { tT[to] = nl; dirty[to] &= (uint8_t)~1u; }
                 changed = true;
+                ++stats[2];
             }
         }
     }

@@ -134,10 +134,13 @@ BPK_HDNI void refine_query(const BatchDev& B, int qi) {
     Rat* trail = B.qtrail + o;
     for (int s = 0; s < Q.N; ++s) { lead[s] = R(1); trail[s] = R(1); }
     Err e{ERR_NONE};
-    int iters = 0;
-    refine(v, c, lo, hi, lead, trail, B.qF + o, B.qB + o, B.qT + o, B.qdirty + o, &iters, e);
+    int64_t rs[4];
+    refine(v, c, lo, hi, lead, trail, B.qF + o, B.qB + o, B.qT + o, B.qdirty + o, rs, e);
     qs.refined = 1;
-    qs.refine_iters = iters;
+    qs.refine_iters = rs[0];
+    qs.refine_evals = rs[1];
+    qs.refine_moves = rs[2];
+    qs.refine_exact = rs[3];
     // The refined plan's stage sums in estimate's order (stage_costs 103-119).
     int64_t D = 1;
     u128 sumFB = 0;

@@ -225,7 +225,21 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
     for (int i = 0; i < nq; ++i)
         for (int m = 0; m < HB.q[i].nbase; ++m)
             if (bottleneck_slot(B, i, m)) host_partition(B, DPItem{i, m, B.ms[HB.q[i].mslot_off + m].a_th}, work);
-    for (int i = 0; i < nq; ++i) refine_query(B, i);
+    int64_t r_it = 0, r_ev = 0, r_mv = 0, r_ex = 0, r_q = 0, r_max = 0;
+    for (int i = 0; i < nq; ++i) {
+        refine_query(B, i);
+        if (B.qs[i].refined) {
+            ++r_q;
+            r_it += B.qs[i].refine_iters;
+            r_ev += B.qs[i].refine_evals;
+            r_mv += B.qs[i].refine_moves;
+            r_ex += B.qs[i].refine_exact;
+            r_max = std::max<int64_t>(r_max, B.qs[i].refine_evals);
+        }
+    }
+    if (getenv("BPEMU_STATS"))
+        fprintf(stderr, "emu refine: queries %lld iterations %lld evaluated steps %lld (max %lld) moves %lld exact %lld\n",
+                (long long)r_q, (long long)r_it, (long long)r_ev, (long long)r_max, (long long)r_mv, (long long)r_ex);
     for (int64_t c = 0; c < HB.ncand; ++c) prune_candidate(B, c);
     int64_t exact_n = 0, exact_ovf = 0, fast_n = 0;
     const size_t mn = (size_t)std::max(1, HB.max_N);
@@ -239,6 +253,9 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
         if (cls == SIM_EXACT) {
             ++exact_n;
             exact_ovf += B.cand[c].status == BP_C_ERR_OVERFLOW;
+            if (getenv("BPEMU_STATS") && atoi(getenv("BPEMU_STATS")) > 1)
+                fprintf(stderr, "exact N=%d M=%lld kind=%d status=%d D=%lld\n", B.cand[c].n_stages,
+                        (long long)B.cand[c].M, B.cand[c].kind, B.cand[c].status, (long long)B.cs[c].D);
         } else {
             ++fast_n;
         }
