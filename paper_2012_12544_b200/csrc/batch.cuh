@@ -55,7 +55,7 @@ enum { PLAN_NONE = 0, PLAN_REFINED = 1, PLAN_WHOLE = 2 };
 // per lane); 5, 6, 7 = 32 lanes with 2, 4, 8 stages per lane; 8 = exact
 // (Rat) slow path, thread per candidate.
 enum { SIM_CLASSES = 9, SIM_EXACT = 8 };
-enum { XBUCKETS = 8192, XSIM_WARPS_PER_SM = 8 };
+enum { XBUCKETS = 32768, XSIM_WARPS_PER_SM = 32 };
 
 // Per-candidate device state (beyond the bp_candidate output record).
 struct CState {

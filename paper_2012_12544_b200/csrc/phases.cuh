@@ -244,17 +244,11 @@ BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci) {
     if (e.bad()) { fail(cd, e); return; }
     if (ft == FT_REJ) { cd.status = BP_C_REJ_FINETUNE; return; }
     if (ft == FT_NOCONV) { cd.status = BP_C_REJ_FINETUNE_NOCONV; return; }
-    // explore's estimate on the final plan (explorer.hpp:398-402)
+    // explore's estimate on the final plan (explorer.hpp:398-402).  The last
+    // estimate computed above (balance_partition's, or the one memory_fine_tune
+    // accepted its final plan on) is of this very plan: same values, same
+    // (absent) errors, so o and the scratch S are reused as is.
     bp_stage* st = B.details ? B.stages + slot : nullptr;
-    if (plan_kind == PLAN_REFINED) {
-        const int64_t qo = Q.qstage_off;
-        CachedPlan cp{B.qhi + qo, B.qF + qo, B.qB + qo, B.qW + qo};
-        estimate(cp, v, c, kind, M, micro, S, o, nullptr, e);
-    } else {
-        WholePlan wp{&v, &c, lo, hi};
-        estimate(wp, v, c, kind, M, micro, S, o, nullptr, e);
-    }
-    if (e.bad()) { fail(cd, e); return; }
     if (!o.feasible) { cd.status = BP_C_REJ_MEM_POST; return; }
     cd.est_minibatch = bp_rat{o.minibatch.n, o.minibatch.d};
     cd.bubble = bp_rat{o.bubble.n, o.bubble.d};

@@ -45,18 +45,18 @@ __global__ void k_sim_prep(BatchDev B) {
 // ---- exact path scheduling: counting sort of the exact list by
 // (stage count, log2 M), heaviest bucket first, so that the 32 lanes of a
 // warp run candidates with the same N and similar M (same loop structure).
-__device__ __forceinline__ int xbucket(int N, int64_t M) {
+__device__ __forceinline__ int xbucket(int N, int64_t M, int kind) {
     int lg = 63 - __clzll((long long)M);
     if (lg > 31) lg = 31;
     int n = N > 255 ? 255 : N;
-    return XBUCKETS - 1 - (n * 32 + lg);
+    return XBUCKETS - 1 - ((n * 32 + lg) * 4 + kind);
 }
 
 __global__ void k_xsort_count(BatchDev B) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B.sim_count[SIM_EXACT]) return;
     int32_t ci = B.sim_list[(int64_t)SIM_EXACT * B.ncand + i];
-    int k = xbucket(B.cand[ci].n_stages, B.cand[ci].M);
+    int k = xbucket(B.cand[ci].n_stages, B.cand[ci].M, B.cand[ci].kind);
     B.xkey[i] = k;
     atomicAdd(&B.xhist[k], 1);
 }
