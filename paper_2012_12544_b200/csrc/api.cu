@@ -107,6 +107,10 @@ struct bp_ctx {
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
     bp_batch* cached = nullptr;
+    // side stream + fork/join events: the comm-coarsened DP runs concurrently
+    // with the (latency-bound, low-occupancy) refine kernel
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
 };
 
 namespace {
@@ -390,9 +394,21 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
                              st);
         });
     timed(c, "bottleneck", st, [&] { launch_bottleneck(D, st); });
+    // fork: coarse DPs (side stream) || refine (main stream); both only read
+    // the whole-layer DP results and write disjoint state
+    if (!c->side) {
+        cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
+    }
+    cudaEventRecord(c->fork, st);
+    cudaStreamWaitEvent(c->side, c->fork, 0);
     if (hb.nmslot > 0)
-        timed(c, "minmax_dp_coarse", st, [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, st); });
+        timed(c, "minmax_dp_coarse", c->side,
+              [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, c->side); });
+    cudaEventRecord(c->join, c->side);
     timed(c, "refine", st, [&] { launch_refine(D, st); });
+    cudaStreamWaitEvent(st, c->join, 0);
     timed(c, "prune", st, [&] { launch_prune(D, st); });
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); });
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
@@ -477,6 +493,9 @@ void bp_destroy(bp_ctx* c) {
     c->nets_mem.release();
     c->cls_mem.release();
     for (auto e : c->event_pool) cudaEventDestroy(e);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->fork) cudaEventDestroy(c->fork);
+    if (c->join) cudaEventDestroy(c->join);
     delete c;
 }
 

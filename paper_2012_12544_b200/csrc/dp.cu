@@ -33,12 +33,74 @@ struct DPSmem {
     int64_t* r1;
     uint32_t* feas;  // [(N+1)][words]
     int32_t* pos;    // [U+1] layer index of unit boundary j
+    int32_t* fwd;    // [N+1] band upper bounds
+    int32_t* bwd;    // [N+1] band lower bounds
 };
 
 __device__ __forceinline__ int64_t dmax(int64_t a, int64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ int64_t dmin(int64_t a, int64_t b) { return a < b ? a : b; }
 
-__global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which, int max_units, int T_slots) {
+// Row bands under a threshold T (warp 0: forward, warp 1: backward).
+//   fwd[n]: farthest unit boundary n stages can reach with every segment
+//           <= T; bwd[n]: earliest boundary from which stages n+1..N can cover
+//           the rest with segments <= T.
+// Stages may take zero units in this relaxation, so fwd bounds the reachable
+// set from above and bwd the completable set from below, on heterogeneous
+// chains too.  A state (n, j) outside [bwd[n], fwd[n]] lies on no partition
+// with all segments <= T, so pass 1 (T = T_ub >= T_opt) and pass 2 / feas
+// (T = T_opt) may skip it without changing dp[N][U], g[N][U] or any feas bit
+// the reconstruction reads.  Each greedy step is a 32-ary search (C is
+// increasing along units): ceil(log32 U) ballot rounds per stage.
+__device__ void dp_bands(const DPSmem& S, const ChainView& c, int N, int U, int64_t T, int warp, int lane) {
+    const unsigned FULL = 0xffffffffu;
+    if (warp == 0) {
+        int cur = 0;
+        if (lane == 0) S.fwd[0] = 0;
+        for (int n = 1; n <= N; ++n) {
+            const int64_t* C = S.C + (size_t)c.type[n - 1] * (U + 1);
+            const int64_t target = C[cur] + T;
+            int a = cur, b = U - (N - n);          // answer in [a, b], C[a] <= target
+            if (b < a) b = a;
+            while (a < b) {
+                const int step = (b - a + 31) / 32;
+                const int j = a + (lane + 1) * step;
+                const unsigned m = __ballot_sync(FULL, j <= b && C[j] <= target);
+                if (m == 0) {
+                    b = a + step - 1;
+                } else {
+                    a += (32 - __clz(m)) * step;
+                    b = min(b, a + step - 1);
+                }
+            }
+            cur = a;
+            if (lane == 0) S.fwd[n] = cur;
+        }
+    } else if (warp == 1) {
+        int cur = U;
+        if (lane == 0) S.bwd[N] = U;
+        for (int n = N; n >= 1; --n) {
+            const int64_t* C = S.C + (size_t)c.type[n - 1] * (U + 1);
+            const int64_t target = C[cur] - T;
+            int a = n - 1, b = cur;                // answer in [a, b], C[b] >= target
+            if (a > b) a = b;
+            while (a < b) {
+                const int step = (b - a + 31) / 32;
+                const int k = b - (lane + 1) * step;
+                const unsigned m = __ballot_sync(FULL, k >= a && C[k] >= target);
+                if (m == 0) {
+                    a = b - step + 1;
+                } else {
+                    b -= (32 - __clz(m)) * step;
+                    a = max(a, b - step + 1);
+                }
+            }
+            cur = b;
+            if (lane == 0) S.bwd[n - 1] = cur;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which, int max_units, int max_N, int T_slots) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int64_t s_red[DP_THREADS / 32];
     __shared__ int32_t s_U, s_slot_of_type_n;
@@ -64,6 +126,9 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
             S.pos = (int32_t*)p; p += (size_t)(max_units + 1) * 4;
             p = (unsigned char*)(((uintptr_t)p + 15) & ~(uintptr_t)15);
             S.feas = (uint32_t*)p;
+            p += (size_t)(max_N + 1) * (((size_t)max_units + 1 + 31) / 32) * 4;
+            S.fwd = (int32_t*)p;
+            S.bwd = S.fwd + (max_N + 1);
         }
         if (item.a_th < 0) {
             for (int64_t j = tid; j <= L; j += DP_THREADS) S.pos[j] = (int32_t)j;
@@ -126,6 +191,8 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
         for (int w = 0; w < DP_THREADS / 32; ++w) T_ub = dmax(T_ub, s_red[w]);
         __syncthreads();
         unsigned long long work = 0;
+        dp_bands(S, c, N, U, T_ub, warp, lane);
+        __syncthreads();
         // ---- pass 1
         int64_t* prev = S.r0;
         int64_t* cur = S.r1;
@@ -133,7 +200,7 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
         __syncthreads();
         for (int n = 1; n <= N; ++n) {
             const int64_t* C = Cn(n);
-            const int jlo = n, jhi = U - (N - n);
+            const int jlo = max(n, S.bwd[n]), jhi = min(U - (N - n), S.fwd[n]);
             for (int j = tid; j <= U; j += DP_THREADS) {
                 int64_t best = DP_INF;
                 if (j >= jlo && j <= jhi) {
@@ -155,13 +222,14 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
         if (tid == 0) s_T = prev[U];
         __syncthreads();
         const int64_t T_opt = s_T;
+        dp_bands(S, c, N, U, T_opt, warp, lane);
         // ---- pass 2
         for (int j = tid; j <= U; j += DP_THREADS) prev[j] = (j == 0) ? 0 : DP_INF;
         __syncthreads();
         for (int n = 1; n <= N; ++n) {
             const int64_t* C = Cn(n);
             const int64_t cN = (int64_t)(N - n + 1);
-            const int jlo = n, jhi = U - (N - n);
+            const int jlo = max(n, S.bwd[n]), jhi = min(U - (N - n), S.fwd[n]);
             for (int j = tid; j <= U; j += DP_THREADS) {
                 int64_t best = DP_INF;
                 if (j >= jlo && j <= jhi) {
@@ -195,10 +263,11 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
             const int64_t* C = Cn(n + 1);
             const int64_t cN = (int64_t)(N - n);
             const uint32_t* nxt = S.feas + (size_t)(n + 1) * words;
+            const int jlo = max(n, S.bwd[n]), jhi = min(U, S.fwd[n]);
             for (int base = warp * 32; base <= U; base += DP_THREADS) {
                 int j = base + lane;
                 bool f = false;
-                if (j >= n && j <= U) {
+                if (j >= jlo && j <= jhi) {
                     const int64_t cj = C[j], wj = S.W[j];
                     for (int j2 = j + 1; j2 <= U; ++j2) {
                         if (C[j2] - cj > T_opt) break;
@@ -279,7 +348,7 @@ void launch_partition(const BatchDev& B, int which, int grid, int max_units, int
                       cudaStream_t st) {
     size_t bytes = partition_smem_bytes(max_units, max_N, T_slots);
     cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    k_partition<<<grid, DP_THREADS, bytes, st>>>(B, which, max_units, T_slots);
+    k_partition<<<grid, DP_THREADS, bytes, st>>>(B, which, max_units, max_N, T_slots);
 }
 
 // Layout of k_partition's dynamic shared memory (must match DPSmem above).
@@ -287,7 +356,7 @@ size_t partition_smem_bytes(int max_units, int max_N, int T_slots) {
     size_t words = ((size_t)max_units + 1 + 31) / 32;
     size_t b = (size_t)(max_units + 1) * 8 * (size_t)(T_slots + 4) + (size_t)(max_units + 1) * 4;
     b = (b + 15) & ~(size_t)15;
-    return b + (size_t)(max_N + 1) * words * 4;
+    return b + (size_t)(max_N + 1) * words * 4 + 2 * (size_t)(max_N + 1) * 4;
 }
 
 }  // namespace bpk

@@ -48,13 +48,41 @@ void host_partition(const BatchDev& B, const DPItem& item, uint64_t& work) {
         int64_t k = ((int64_t)(n - 1) * U) / N, j = ((int64_t)n * U) / N;
         T_ub = std::max(T_ub, Cn(n)[j] - Cn(n)[k]);
     }
+    // bands (mirror of dp_bands in csrc/dp.cu): row n can only matter for
+    // j in [bwd[n], fwd[n]] -- fwd = farthest greedy reach of n stages, bwd =
+    // earliest start from which stages n+1..N can cover the rest -- under T.
+    // Stages may take zero units in this relaxation, which makes fwd an upper
+    // bound of the reachable set's maximum and bwd a lower bound of the
+    // completable set's minimum even on heterogeneous chains.
+    std::vector<int> fwd(N + 1), bwd(N + 1);
+    auto bands = [&](int64_t T) {
+        int cur = 0;
+        fwd[0] = 0;
+        for (int n = 1; n <= N; ++n) {
+            const int64_t* Cc = Cn(n);
+            int hi = U - (N - n), j = cur;
+            while (j < hi && Cc[j + 1] - Cc[cur] <= T) ++j;
+            cur = std::max(j, cur);
+            fwd[n] = cur;
+        }
+        cur = U;
+        bwd[N] = U;
+        for (int n = N; n >= 1; --n) {
+            const int64_t* Cc = Cn(n);
+            int lo = n - 1, k = cur;
+            while (k > lo && Cc[cur] - Cc[k - 1] <= T) --k;
+            cur = k;
+            bwd[n - 1] = cur;
+        }
+    };
+    bands(T_ub);
     std::vector<int64_t> prev(U + 1), cur(U + 1);
     for (int j = 0; j <= U; ++j) prev[j] = j == 0 ? 0 : INF;
     for (int n = 1; n <= N; ++n) {
         const int64_t* Cc = Cn(n);
         for (int j = 0; j <= U; ++j) {
             int64_t best = INF;
-            if (j >= n && j <= U - (N - n)) {
+            if (j >= n && j <= U - (N - n) && j >= bwd[n] && j <= fwd[n]) {
                 for (int k = j - 1; k >= n - 1; --k) {
                     int64_t s = Cc[j] - Cc[k];
                     if (s > T_ub || s >= best) break;
@@ -68,13 +96,14 @@ void host_partition(const BatchDev& B, const DPItem& item, uint64_t& work) {
         std::swap(prev, cur);
     }
     const int64_t T_opt = prev[U];
+    bands(T_opt);
     for (int j = 0; j <= U; ++j) prev[j] = j == 0 ? 0 : INF;
     for (int n = 1; n <= N; ++n) {
         const int64_t* Cc = Cn(n);
         const int64_t cN = N - n + 1;
         for (int j = 0; j <= U; ++j) {
             int64_t best = INF;
-            if (j >= n && j <= U - (N - n)) {
+            if (j >= n && j <= U - (N - n) && j >= bwd[n] && j <= fwd[n]) {
                 for (int k = j - 1; k >= n - 1; --k) {
                     if (Cc[j] - Cc[k] > T_opt) break;
                     int64_t w2 = 2 * (W[j] - W[k]);
@@ -95,7 +124,7 @@ void host_partition(const BatchDev& B, const DPItem& item, uint64_t& work) {
     for (int n = N - 1; n >= 0; --n) {
         const int64_t* Cc = Cn(n + 1);
         const int64_t cN = N - n;
-        for (int j = n; j <= U; ++j) {
+        for (int j = std::max(n, bwd[n]); j <= U && j <= fwd[n]; ++j) {
             for (int j2 = j + 1; j2 <= U; ++j2) {
                 if (Cc[j2] - Cc[j] > T_opt) break;
                 ++work;
