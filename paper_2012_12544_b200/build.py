@@ -73,7 +73,7 @@ def build_oracles():
     reference sources are present (dev container only)."""
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/include"):
-        targets.append("ref")
+        targets += ["ref", "dropin"]
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")] + targets, check=True)
     emu = os.path.join(ROOT, "tests", "emu")
     if os.path.isdir(emu):
