@@ -52,7 +52,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--models", type=int, default=128, help="models per rank (128 = full 2^20 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample-stride", type=int, default=1021)
+    ap.add_argument("--cpu-sample-stride", type=int, default=127)
     return ap.parse_args()
 
 
@@ -121,6 +121,79 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+SMS, LANES = 148, 128          # B200: SMs x (4 SMSP x 32 lanes) issue slots per clock
+OPS_PER_TRANSITION = 3         # DP: sub, max, min (SURVEY.md 8d c_dp, int32/int64-in-one-op path)
+OPS_PER_EVENT = 3              # simulator: max, add, store-forward (SURVEY.md 8d c_sim)
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def kernel_work_ops(name, work):
+    """Algorithmic lane-ops of one launch of `name` from its work counter, or
+    None for kernels without a closed-form count (refine, prune, ...)."""
+    if name.startswith("minmax_dp"):
+        return work * OPS_PER_TRANSITION
+    if name.startswith("sim_"):
+        return work * OPS_PER_EVENT
+    return None
+
+
+def rooflines(stats, steps, clocks, problem, step_ms):
+    """Per-kernel issue rooflines and the sweep-level bound of SURVEY.md 8d.
+
+    Every kernel on this path is integer / exact-rational control flow (no
+    dense contraction, no streaming): the bound is the SM issue rate,
+    148 SMs x 128 lanes x f_clk, at the measured max SM clock.  `achieved` is
+    the kernel's ALGORITHMIC lane-ops per launch (work counter x ops/unit)
+    over its average launch time (CUDA events on its stream)."""
+    peaks, peak_kind = measured_peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    issue_peak = SMS * LANES * f_max / 1e9              # Gop/s
+    try:
+        with open(TRAFFIC_FILE) as f:
+            traffic = json.load(f)
+    except Exception:
+        traffic = {}
+    kern = {}
+    for k, v in stats.items():
+        ms = v["ms"] / max(1, v["launches"])
+        e = {"ms_per_step": v["ms"] / steps, "launches": v["launches"], "work_per_launch": v["work"]}
+        ops = kernel_work_ops(k, v["work"])
+        if ops is not None and ms > 0:
+            e["achieved_gops"] = ops / (ms * 1e6)
+            e["frac"] = e["achieved_gops"] / issue_peak
+        kern[k] = e
+    dom = max(stats, key=lambda k: stats[k]["ms"])
+    d = kern[dom]
+    units = {"minmax_dp": "DP transitions", "minmax_dp_coarse": "DP transitions"}.get(dom, "simulated events")
+    roof = {"kernel": dom, "bound": "issue", "unit": "Gop/s", "peak": issue_peak,
+            "achieved": d.get("achieved_gops"), "frac": d.get("frac"),
+            "traffic": traffic.get(dom),
+            "work": (f"{d['work_per_launch']:.4g} {units}/launch x "
+                     f"{OPS_PER_TRANSITION if dom.startswith('minmax_dp') else OPS_PER_EVENT} ops"
+                     if d.get("achieved_gops") is not None else f"{dom}: no closed-form work count"),
+            "peak_source": f"{SMS} SMs x {LANES} lanes x {f_max / 1e6:.0f} MHz (sm_max_mhz, {peak_kind} "
+                           f"MEASURED_PEAKS.json); HBM {peaks.get('hbm_gbs')} GB/s"}
+    # sweep bound (SURVEY.md 8d): t_roof = sum B_cost / BW + (X_dp * c_dp + X_sim * c_sim) / issue
+    q = problem.queries
+    U = np.array([problem.networks[i].L for i in q["network"]], dtype=np.float64)
+    N = q["n_stages"].astype(np.float64)
+    T = np.array([len(set(problem.clusters[c].types[:n].tolist())) for c, n in zip(q["cluster"], q["n_stages"])],
+                 dtype=np.float64)
+    b_cost = float(np.sum(8 * U * (2 * T + 2)))
+    x_dp_ref = float(np.sum(np.where(U >= N, N * (U - N + 1) * (U - N + 2), 0)))
+    x_sim = float(sum(v["work"] for k, v in stats.items() if k.startswith("sim_")))
+    x_dp = float(sum(v["work"] for k, v in stats.items() if k.startswith("minmax_dp")))
+    hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+    t_ref = b_cost / hbm + (x_dp_ref * OPS_PER_TRANSITION + x_sim * OPS_PER_EVENT) / (issue_peak * 1e9)
+    t_own = b_cost / hbm + (x_dp * OPS_PER_TRANSITION + x_sim * OPS_PER_EVENT) / (issue_peak * 1e9)
+    sweep = {"t_roof_ms_reference_dp": 1e3 * t_ref, "t_roof_ms_banded_dp": 1e3 * t_own, "t_measured_ms": step_ms,
+             "frac": 1e3 * t_ref / step_ms,
+             "x_dp_reference": x_dp_ref, "x_dp_performed": x_dp, "x_sim_events": x_sim, "b_cost_bytes": b_cost,
+             "formula": "t_roof = B_cost/HBM + (X_dp*3 + X_sim*3)/(148*128*f_max); frac = t_roof(reference X_dp) / "
+                        "t_measured (SURVEY.md 8d)"}
+    return roof, kern, sweep
+
+
 def cpu_baseline(problem, stride, threads):
     """The reference's own explore() (oracle/_ref) on a bounded C5 sample."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -152,7 +225,7 @@ def run_reference(args):
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import PortOracle, RefOracle, ref_available
     oracle = RefOracle() if ref_available() else PortOracle()
-    stride = 4093   # prime: ~16 queries (256 candidates) per step, rotating offsets
+    stride = 257    # prime: 255-256 queries (~4,096 candidates) per step, rotating offsets
     times, cands = [], []
     for step in range(args.warmup + args.steps):
         idx = np.arange(step % stride, p.queries.size, stride)
@@ -173,10 +246,10 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/exact-rational",
             "data": "synthetic (C5 generator, mt19937_64 seeds of SURVEY.md 8d)",
-            "config": {"workload": "C5 sweep sample: 1/4093 query stride per step (~16 queries, ~256 candidates), "
+            "config": {"workload": "C5 sweep sample: 1/257 query stride per step (~256 queries, ~4,096 candidates), "
                                    "rotating offsets", "models": args.models},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if oracle.kind == "reference" else 1,
-                             "kind": oracle.kind, "sample": "1/4093 query stride of C5 per step"},
+                             "kind": oracle.kind, "sample": "1/257 query stride of C5 per step, offset = step index"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -281,25 +354,9 @@ def run_b200(args):
             torch.distributed.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel
-    peaks, peak_kind = measured_peaks()
+    # ---- roofline of the dominant kernel (DESIGN.md "Rooflines")
     clocks = clk.summary()
-    dom = max(stats.items(), key=lambda kv: kv[1]["ms"])
-    f_clk = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    issue_peak = 148 * 128 * f_clk / 1e9          # lane-ops per ns == Gop/s
-    dp = stats.get("minmax_dp", {"ms": 0.0, "work": 0.0})
-    roof = {"kernel": dom[0], "bound": "issue", "unit": "Gop/s",
-            "peak": issue_peak, "peak_source": f"148 SMs x 128 lanes x {f_clk/1e6:.0f} MHz (SM clock sampled "
-                                                 f"during the timed region); {peak_kind} peaks file",
-            "traffic": None}
-    if dom[0] == "minmax_dp" and dp["ms"] > 0:
-        ops = dp["work"] * 3.0          # sub, max, min per DP transition (SURVEY.md 8d c_dp)
-        roof.update({"achieved": ops / (dp["ms"] * 1e6), "frac": ops / (dp["ms"] * 1e6) / issue_peak,
-                     "work": f"{dp['work']/args.steps:.4g} DP transitions/launch x 3 ops"})
-    else:
-        roof.update({"achieved": None, "frac": None,
-                     "work": f"dominant kernel {dom[0]} is latency-bound exact-rational code; see DESIGN.md"})
-    kern = {k: {"ms_per_step": v["ms"] / args.steps, "launches": v["launches"]} for k, v in stats.items()}
+    roof, kern, sweep = rooflines(stats, args.steps, clocks, p, total_ms / args.steps)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -315,6 +372,7 @@ def run_b200(args):
             "gpu_launches": launches,
             "clocks": clocks,
             "roofline": roof,
+            "sweep_roofline": sweep,
             "kernels": kern,
             "best": {"makespan": f"{int(best['makespan']['num'])}/{int(best['makespan']['den'])}",
                      "M": int(best["M"]), "kind": int(best["kind"]), "query_id": int(best["query_id"])},

@@ -294,7 +294,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     size_t o_sim = L.take<char>(sim_exact_state_bytes(c->sm_count, std::max(1, hb.max_N)));
     size_t o_xkey = L.take<int32_t>(nc), o_xsorted = L.take<int32_t>(nc), o_xhist = L.take<int32_t>(XBUCKETS);
     size_t o_cq = L.take<int32_t>(nc), o_co = L.take<int32_t>(nc);
-    size_t o_work = L.take<unsigned long long>(8);
+    size_t o_work = L.take<unsigned long long>(WORK_SLOTS);
     size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(SIM_CLASSES);
     if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
     void* b = B->mem.p;
@@ -384,7 +384,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     e = cudaMemsetAsync(D.cand, 0, (size_t)hb.ncand * sizeof(bp_candidate), st);
     if (e == cudaSuccess && D.stages) e = cudaMemsetAsync(D.stages, 0, (size_t)hb.nstage * sizeof(bp_stage), st);
     if (e == cudaSuccess) e = cudaMemsetAsync(D.dp_count + 1, 0, sizeof(int32_t), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(D.work, 0, 8 * sizeof(unsigned long long), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(D.work, 0, WORK_SLOTS * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_fail(c, e, "memset");
     const int T = c->max_T, maxN = std::max(1, hb.max_N);
     timed(c, "setup", st, [&] { launch_setup(D, st); });
@@ -414,6 +414,10 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
     for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
+    static const char* xwave_names[SIM_XWAVE_CLASSES] = {"sim_xwave_g4", "sim_xwave_g8", "sim_xwave_g16",
+                                                         "sim_xwave_g32", "sim_xwave_g32s2"};
+    for (int k = 0; k < SIM_XWAVE_CLASSES; ++k)
+        timed(c, xwave_names[k], st, [&] { launch_sim_xwave(D, k, c->sm_count, st); });
     timed(c, "sim_exact", st, [&] { launch_sim_exact(D, c->sm_count, st); }, 4);
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();
@@ -435,15 +439,18 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return cuda_fail(c, e, "fetch");
     if (c->prof) {
-        unsigned long long work[8];
-        if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess)
-            c->stats["minmax_dp"].work += (double)work[0];
-        int32_t cnt[SIM_CLASSES];
+        // algorithmic work of the most recent run (per launch, not summed):
+        // DP transitions of each partition launch, simulated events per class
+        unsigned long long work[WORK_SLOTS];
         static const char* names[SIM_CLASSES] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                                  "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4",
-                                                 "sim_fast_g32s8", "sim_exact"};
-        if (cudaMemcpy(cnt, B->dev.sim_count, sizeof(cnt), cudaMemcpyDeviceToHost) == cudaSuccess)
-            for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work += cnt[k];
+                                                 "sim_fast_g32s8", "sim_exact", "sim_xwave_g4", "sim_xwave_g8",
+                                                 "sim_xwave_g16", "sim_xwave_g32", "sim_xwave_g32s2"};
+        if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess) {
+            c->stats["minmax_dp"].work = (double)work[WORK_DP_WHOLE];
+            c->stats["minmax_dp_coarse"].work = (double)work[WORK_DP_COARSE];
+            for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work = (double)work[WORK_SIM_EVENTS + k];
+        }
         collect(c);
     }
     return BP_OK;

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
         }
         // instrumentation: transitions performed
         for (int o = 16; o > 0; o >>= 1) work += __shfl_xor_sync(0xffffffffu, work, o);
-        if (lane == 0) atomicAdd(&B.work[0], work);
+        if (lane == 0) atomicAdd(&B.work[which], work);
         __syncthreads();
     }
 }

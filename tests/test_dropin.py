@@ -89,6 +89,23 @@ def test_golden_regenerates_from_reference():
     assert got == want, _diff(got, want)
 
 
+REF_INC = "/root/reference/proj/include"
+JSON_DIR = os.path.join(ROOT, "oracle", "_ref", "vendor")
+
+
+def test_interop_with_reference_types(tmp_path):
+    """include/bapipe_b200/interop.hpp: reference-typed inputs and results
+    (explore_as) agree with bapipe::explore on every scenario."""
+    if not (os.path.isdir(REF_INC) and os.path.exists(os.path.join(JSON_DIR, "json.hpp"))):
+        pytest.skip("reference headers not present (dev container only)")
+    exe = str(tmp_path / "interop")
+    subprocess.run([CXX, "-std=c++20", "-O2", "-Wno-enum-compare", "-I" + os.path.join(ROOT, "include"),
+                    "-I" + REF_INC, "-I" + JSON_DIR, "-o", exe, os.path.join(CPP, "interop_check.cpp"),
+                    os.path.join(CPP, "emu_abi_shim.cpp")], check=True, capture_output=True, text=True)
+    out = _run(exe)
+    assert out.strip().endswith("0 mismatches"), out[-3000:]
+
+
 @pytest.mark.gpu
 def test_dropin_matches_reference_on_b200(tmp_path):
     so = os.path.join(PKG, "libbapipe_b200.so")

@@ -94,7 +94,7 @@ def test_full_c5_sweep_properties(ex, c5):
 def test_ranked_lists_sorted_on_c5_sample(ex):
     from fractions import Fraction as Fr
     p = scenarios.c5_sample(257)
-    res, cand, _ = ex.explore(p, details=False)
+    res, cand, _ = ex.explore(p, details=True)
     for qi in range(p.queries.size):
         lo = int(p.queries["cand_offset"][qi])
         cs = cand[lo:lo + int(p.n_candidates[qi])]
