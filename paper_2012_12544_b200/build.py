@@ -63,7 +63,7 @@ def build_product(force=False, verbose=False):
         if j.returncode:
             raise RuntimeError("nvcc failed")
     tmp = SO + ".tmp"
-    subprocess.run([_nvcc(), *ARCH, "-shared", "-ccbin", _host_cxx(), "-o", tmp, *objs], check=True)
+    subprocess.run([_nvcc(), *ARCH, "-shared", "-Xlinker", "--no-undefined", "-ccbin", _host_cxx(), "-o", tmp, *objs], check=True)
     os.replace(tmp, SO)
     return SO
 

@@ -292,7 +292,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     size_t o_sF = L.take<Rat>(ns), o_sB = L.take<Rat>(ns), o_sW = L.take<Rat>(ns), o_sM = L.take<Rat>(ns);
     size_t o_sA = L.take<int64_t>(ns), o_sSR = L.take<int64_t>(ns);
     size_t o_sim = L.take<char>(sim_exact_state_bytes(c->sm_count, std::max(1, hb.max_N)));
-    size_t o_xkey = L.take<int32_t>(nc), o_xsorted = L.take<int32_t>(nc), o_xhist = L.take<int32_t>(XBUCKETS);
+    size_t o_xkey = L.take<int32_t>(nc), o_xsorted = L.take<int32_t>(nc), o_xhist = L.take<int32_t>(XBUCKETS + 1);
     size_t o_cq = L.take<int32_t>(nc), o_co = L.take<int32_t>(nc);
     size_t o_work = L.take<unsigned long long>(WORK_SLOTS);
     size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(SIM_CLASSES);
@@ -414,10 +414,6 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
     for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
-    static const char* xwave_names[SIM_XWAVE_CLASSES] = {"sim_xwave_g4", "sim_xwave_g8", "sim_xwave_g16",
-                                                         "sim_xwave_g32", "sim_xwave_g32s2"};
-    for (int k = 0; k < SIM_XWAVE_CLASSES; ++k)
-        timed(c, xwave_names[k], st, [&] { launch_sim_xwave(D, k, c->sm_count, st); });
     timed(c, "sim_exact", st, [&] { launch_sim_exact(D, c->sm_count, st); }, 4);
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();
@@ -444,8 +440,7 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
         unsigned long long work[WORK_SLOTS];
         static const char* names[SIM_CLASSES] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                                  "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4",
-                                                 "sim_fast_g32s8", "sim_exact", "sim_xwave_g4", "sim_xwave_g8",
-                                                 "sim_xwave_g16", "sim_xwave_g32", "sim_xwave_g32s2"};
+                                                 "sim_fast_g32s8", "sim_exact"};
         if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess) {
             c->stats["minmax_dp"].work = (double)work[WORK_DP_WHOLE];
             c->stats["minmax_dp_coarse"].work = (double)work[WORK_DP_COARSE];

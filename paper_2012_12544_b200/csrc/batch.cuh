@@ -53,9 +53,8 @@ enum { PLAN_NONE = 0, PLAN_REFINED = 1, PLAN_WHOLE = 2 };
 
 // Simulator classes: 0..4 = lanes per candidate 2, 4, 8, 16, 32 (one stage
 // per lane); 5, 6, 7 = 32 lanes with 2, 4, 8 stages per lane; 8 = exact
-// (Rat) path, thread per candidate (N > 64); 9..13 = exact (Rat) wavefront,
-// lanes per candidate 4, 8, 16, 32, and 32 with 2 stages per lane.
-enum { SIM_CLASSES = 14, SIM_EXACT = 8, SIM_XWAVE = 9, SIM_XWAVE_CLASSES = 5 };
+// (Rat) slow path, thread per candidate.
+enum { SIM_CLASSES = 9, SIM_EXACT = 8 };
 // instrumentation slots of BatchDev::work (algorithmic work of one run)
 enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_SIM_EVENTS = 2, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
 enum { XBUCKETS = 32768, XSIM_WARPS_PER_SM = 32 };
@@ -106,7 +105,7 @@ struct BatchDev {
     // exact-simulator scheduling: counting sort of its list by (N, log2 M)
     int32_t* xkey;            // [ncand]
     int32_t* xsorted;         // [ncand]
-    int32_t* xhist;           // [XBUCKETS] counts, then running offsets
+    int32_t* xhist;           // [XBUCKETS] counts, then running offsets; [XBUCKETS] = chunk counter
     int max_N;                // largest stage count in the batch (exact-sim state sizing)
     int details;              // write bp_stage records
     // DP work lists

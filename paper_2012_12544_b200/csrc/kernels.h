@@ -19,7 +19,6 @@ void launch_prune(const BatchDev& B, cudaStream_t st);
 void launch_sim_prep(const BatchDev& B, cudaStream_t st);
 void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st);
 void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st);
-void launch_sim_xwave(const BatchDev& B, int k, int sms, cudaStream_t st);
 size_t sim_exact_state_bytes(int sms, int max_N);
 void launch_rank(const BatchDev& B, cudaStream_t st);
 void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,

@@ -192,6 +192,40 @@ BPK_HDNI Rat rat_nd(int64_t n, int64_t d, Err& e) {
 
 BPK_HD bool fits64(i128 x) { return x <= (i128)INT64_MAX && x >= (i128)INT64_MIN; }
 
+// Inverse of an odd m modulo 2^32 (Newton: 5 -> 10 -> 20 -> 40 correct bits)
+// and its lift to 2^64 (one more step).
+BPK_HD uint32_t inv32_odd(uint32_t m) {
+    uint32_t x = (3 * m) ^ 2;
+    x *= 2 - m * x;
+    x *= 2 - m * x;
+    x *= 2 - m * x;
+    return x;
+}
+BPK_HD uint64_t inv64_lift(uint32_t m, uint32_t x32) {
+    uint64_t x = x32;
+    return x * (2 - (uint64_t)m * x);
+}
+
+// x mod m for a 32-bit m without the 64-bit software remainder: a quotient
+// estimate from a double reciprocal (off by at most ~2^13), one exact
+// correction in double (|r| < 2^53), then integer fix-ups.  The result is
+// exact whatever the reciprocal's rounding, so host and device agree.
+BPK_HD uint32_t umod_u64_u32(uint64_t x, uint32_t m) {
+    if ((x >> 32) == 0) return (uint32_t)x % m;
+    if (m <= 1) return 0;
+#ifdef __CUDA_ARCH__
+    const double rm = __drcp_rn((double)m);
+#else
+    const double rm = 1.0 / (double)m;
+#endif
+    const uint64_t q = (uint64_t)((double)x * rm);
+    int64_t r = (int64_t)(x - q * (uint64_t)m);
+    r -= (int64_t)((double)r * rm) * (int64_t)m;
+    while (r < 0) r += m;
+    while (r >= (int64_t)m) r -= m;
+    return (uint32_t)r;
+}
+
 // a + s*b with s = +1 / -1 (operator+ / operator-), Knuth 4.5.1: with
 // g = gcd(a.d, b.d), t = a.n*(b.d/g) + b.n*(a.d/g) and g2 = gcd(t, g) the
 // reduced result is (t/g2) / ((a.d/g)*(b.d/g2)).
@@ -203,6 +237,36 @@ BPK_HDNI Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n + bn, 1, e);
     if (a.d == 1) return fit128((i128)a.n * b.d + bn, b.d, e);        // gcd(num, b.d) = 1
     if (b.d == 1) return fit128((i128)bn * a.d + a.n, a.d, e);
+    if (((uint64_t)(a.d | b.d) >> 32) == 0 && b.n != INT64_MIN) {
+        // Hot path (the simulator's and refine's common case): 32-bit
+        // denominators and a 64-bit t.  Exact quotients come from inverses
+        // mod 2^32 / 2^64 and t mod g from umod_u64_u32, so no 64-bit
+        // software division runs.
+        const uint32_t da = (uint32_t)a.d, db = (uint32_t)b.d;
+        const int64_t bs = s > 0 ? b.n : -b.n;
+        const uint32_t g = gcd_u32(da, db);
+        if (g == 1) return fit128((i128)a.n * db + (i128)bs * da, (i128)((uint64_t)da * db), e);
+        const int tz = ctz32(g);
+        const uint32_t ig = inv32_odd(g >> tz);
+        const uint32_t ad = (da >> tz) * ig, bd = (db >> tz) * ig;   // da / g, db / g
+        const i128 t = (i128)a.n * bd + (i128)bs * ad;
+        if (t == 0) return Rat{0, 1};
+        if (fits64(t)) {
+            const int64_t tt = (int64_t)t;
+            const uint64_t ut = uabs64(tt);
+            const uint32_t tm = umod_u64_u32(ut, g);
+            const uint32_t g2 = tm == 0 ? g : gcd_u32(tm, g);
+            const int tz2 = ctz32(g2);
+            const uint32_t i2 = inv32_odd(g2 >> tz2);
+            const uint64_t q = (ut >> tz2) * inv64_lift(g2 >> tz2, i2);      // |t| / g2
+            const uint64_t den = (uint64_t)ad * (uint32_t)((db >> tz2) * i2);  // (da/g) * (db/g2)
+            if (q > (tt < 0 ? (uint64_t)1 << 63 : (uint64_t)INT64_MAX) || den > (uint64_t)INT64_MAX) {
+                e.set(ERR_OVERFLOW);
+                return Rat{0, 1};
+            }
+            return Rat{tt < 0 ? (int64_t)((uint64_t)0 - q) : (int64_t)q, (int64_t)den};
+        }
+    }
     uint64_t g = gcd_u64((uint64_t)a.d, (uint64_t)b.d);
     if (g == 1) return fit128((i128)a.n * b.d + bn * a.d, (i128)a.d * b.d, e);
     int64_t ad = (int64_t)udiv_exact64((uint64_t)a.d, g), bd = (int64_t)udiv_exact64((uint64_t)b.d, g);

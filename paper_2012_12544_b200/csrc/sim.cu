@@ -39,12 +39,6 @@ __global__ void k_sim_prep(BatchDev B) {
     if (i < B.ncand) {
         int64_t ci = B.cperm[i];
         cls = sim_classify(B, ci);
-        if (cls == SIM_EXACT) {
-            // exact candidates with N <= 64 go to the Rat wavefront kernels
-            const int N = B.cand[ci].n_stages;
-            cls = N <= 4 ? SIM_XWAVE : N <= 8 ? SIM_XWAVE + 1 : N <= 16 ? SIM_XWAVE + 2
-                : N <= 32 ? SIM_XWAVE + 3 : N <= 64 ? SIM_XWAVE + 4 : SIM_EXACT;
-        }
         if (cls >= 0) {
             int pos = atomicAdd(&B.sim_count[cls], 1);
             B.sim_list[(int64_t)cls * B.ncand + pos] = (int32_t)ci;
@@ -110,9 +104,11 @@ __global__ void k_xsort_scatter(BatchDev B) {
     B.xsorted[pos] = B.sim_list[(int64_t)SIM_EXACT * B.ncand + i];
 }
 
-// Persistent warps walk the sorted exact list in chunks of 32; each lane runs
-// one candidate's exact simulation with its per-stage state interleaved
-// across the warp (element (s, lane) at s*32 + lane: coalesced accesses).
+// Persistent warps take chunks of 32 from the sorted exact list (heaviest
+// first) off a global counter, so the long candidates start first and the
+// rest fill in behind them; each lane runs one candidate's exact simulation
+// with its per-stage state interleaved across the warp (element (s, lane) at
+// s*32 + lane: coalesced accesses).
 __global__ void __launch_bounds__(256) k_sim_exact(BatchDev B) {
     const int count = B.sim_count[SIM_EXACT];
     const int lane = threadIdx.x & 31;
@@ -124,8 +120,13 @@ __global__ void __launch_bounds__(256) k_sim_exact(BatchDev B) {
     int64_t* ibase = reinterpret_cast<int64_t*>(B.simbuf + nwarps * 5 * arr) + warp * 2 * arr;
     SimState S{base + lane, base + arr + lane, base + 2 * arr + lane, base + 3 * arr + lane, base + 4 * arr + lane,
                ibase + lane, ibase + arr + lane, 32};
-    for (int64_t chunk = warp; chunk * 32 < count; chunk += nwarps) {
-        int64_t i = chunk * 32 + lane;
+    int32_t* next = B.xhist + XBUCKETS;   // chunk counter, zeroed with the histogram
+    for (;;) {
+        int chunk = 0;
+        if (lane == 0) chunk = atomicAdd(next, 1);
+        chunk = __shfl_sync(0xffffffffu, chunk, 0);
+        if ((int64_t)chunk * 32 >= count) break;
+        const int64_t i = (int64_t)chunk * 32 + lane;
         if (i < count) sim_exact(B, B.xsorted[i], S);
     }
 }
@@ -361,268 +362,7 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
     }  // persistent loop
 }
 
-// ---- exact wavefront: the fast kernel's position-parallel walk with exact
-// Rat events.  A group of G lanes owns one candidate, S stages per lane
-// (stage s = r*S + i).  At each position every stage runs one op; ops whose
-// arrival was produced at an earlier position read it from a one-slot
-// mailbox and run at once, and same-position chains (warm-up F, drain B) are
-// resolved in rounds: a lane runs once its predecessor's output is final.
-// Every Rat the reference computes (each op's end time, each arrival end+SR
-// in sync mode) is computed here with the same operands, so the candidate
-// overflows here iff it does in the reference; the only error a simulation
-// can raise is Rat: overflow, so the evaluation order inside a candidate does
-// not change its status.
-__device__ __forceinline__ Rat shfl_up_rat(Rat x, int o, int G) {
-    return Rat{(int64_t)__shfl_up_sync(0xffffffffu, (long long)x.n, o, G),
-               (int64_t)__shfl_up_sync(0xffffffffu, (long long)x.d, o, G)};
-}
-__device__ __forceinline__ Rat shfl_down_rat(Rat x, int o, int G) {
-    return Rat{(int64_t)__shfl_down_sync(0xffffffffu, (long long)x.n, o, G),
-               (int64_t)__shfl_down_sync(0xffffffffu, (long long)x.d, o, G)};
-}
-__device__ __forceinline__ Rat shfl_xor_rat(Rat x, int o, int G) {
-    return Rat{(int64_t)__shfl_xor_sync(0xffffffffu, (long long)x.n, o, G),
-               (int64_t)__shfl_xor_sync(0xffffffffu, (long long)x.d, o, G)};
-}
-
-template <int G, int S>
-__global__ void __launch_bounds__(SIM_THREADS) k_sim_xwave(BatchDev B, int cls) {
-    const unsigned FULL = 0xffffffffu;
-    const int count = B.sim_count[cls];
-    const int lane = threadIdx.x & 31;
-    const int r = lane % G;
-    const int gpw = 32 / G;
-    const unsigned gmask = G == 32 ? FULL : (((1u << G) - 1u) << (lane - r));
-    const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
-    const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    for (int64_t base = warp_global * gpw; base < count; base += warps_total * gpw) {
-    const int64_t gid = base + lane / G;
-    const bool active = gid < count;
-    const int64_t ci = active ? B.sim_list[(int64_t)cls * B.ncand + gid] : -1;
-    int N = 1, kind = 0;
-    int64_t M = 0, micro = 1;
-    Rat Fd[S], Bd[S], fr[S], pF[S], pB[S];
-    int64_t SRin[S], SRout[S], A[S], wv[S], wprev[S], wnext[S];
-    bool has[S];
-#pragma unroll
-    for (int i = 0; i < S; ++i) {
-        has[i] = false;
-        Fd[i] = Bd[i] = fr[i] = pF[i] = pB[i] = Rat{0, 1};
-        SRin[i] = SRout[i] = A[i] = wv[i] = wprev[i] = wnext[i] = 0;
-    }
-    if (active) {
-        const bp_candidate& cd = B.cand[ci];
-        const CState cs = B.cs[ci];
-        const QDesc Q = B.q[B.cq[ci]];
-        N = Q.N;
-        kind = cd.kind;
-        M = cd.M;
-        micro = cd.micro;
-        NetView v = net_view(B.P, Q.net);
-        ChainView c = chain_view(B.P, Q.cl, N);
-        const int64_t slot = Q.stage_off + (ci - Q.cand_off) * N;
-        const int64_t qo = Q.qstage_off;
-        const bool refined = cs.plan_kind == PLAN_REFINED;
-        const int32_t* hi = refined ? B.qhi + qo : B.chi + slot;
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-            const int s = r * S + i;
-            if (s >= N) continue;
-            has[i] = true;
-            if (refined) {
-                Fd[i] = B.qF[qo + s];
-                Bd[i] = B.qB[qo + s];
-            } else {   // chain_instance (simulator.hpp:248-262)
-                const int32_t t = c.type[s];
-                Fd[i] = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pfp + (int64_t)t * (v.L + 1)));
-                Bd[i] = R(stage_sum_whole(B.clo[slot + s], B.chi[slot + s], v.Pbp + (int64_t)t * (v.L + 1)));
-            }
-            if (s > 0) {
-                const int64_t a = v.a[hi[s - 1] - 1] * micro;
-                SRin[i] = a == 0 ? 0 : ceil_div64(a, c.bw[s - 1]);
-                A[i] = a;
-            } else {
-                A[i] = v.a[hi[0] - 1] * micro;
-            }
-            if (s + 1 < N) {
-                const int64_t a = v.a[hi[s] - 1] * micro;
-                SRout[i] = a == 0 ? 0 : ceil_div64(a, c.bw[s]);
-            }
-            int64_t w = warmup_depth(kind, N, s + 1);
-            wv[i] = w < M ? w : M;
-            if (s > 0) { w = warmup_depth(kind, N, s); wprev[i] = w < M ? w : M; }
-            if (s + 1 < N) { w = warmup_depth(kind, N, s + 2); wnext[i] = w < M ? w : M; }
-        }
-    }
-    const bool async = kind_async(kind);
-    Err e{ERR_NONE};
-    int64_t Mloop = active ? M : 0;
-    for (int o = 16; o > 0; o >>= 1) Mloop = smax(Mloop, __shfl_xor_sync(FULL, Mloop, o));
-    bool dead = false;   // this lane's group has overflowed: its outcome is decided
-    for (int64_t p = 0; p < 2 * Mloop; ++p) {
-        const bool live = active && !dead && p < 2 * M;
-        bool isF[S], isB[S], chF[S], chB[S];
-        int64_t mm[S];
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-            isF[i] = isB[i] = chF[i] = chB[i] = false;
-            mm[i] = 0;
-            if (has[i] && live) {
-                const int s = r * S + i;
-                const StageOp op = op_at(p, wv[i], M);
-                mm[i] = op.m;
-                isF[i] = op.is_f;
-                isB[i] = !op.is_f;
-                if (isF[i] && s > 0) {
-                    const StageOp q = op_at(p, wprev[i], M);
-                    chF[i] = q.is_f && q.m == op.m;
-                }
-                if (isB[i] && s + 1 < N) {
-                    const StageOp q = op_at(p, wnext[i], M);
-                    chB[i] = !q.is_f && q.m == op.m;
-                }
-            }
-        }
-        // ---- F ops, ascending; out = end (+ SR when sync) for stages s < N-1
-        Rat outF[S];
-        bool pend[S];
-        bool anyp = false;
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-            const int s = r * S + i;
-            outF[i] = Rat{0, 1};
-            pend[i] = isF[i] && chF[i];
-            anyp |= pend[i];
-            if (isF[i] && !chF[i]) {
-                Rat ready = fr[i];
-                if (s > 0 && rat_gt(pF[i], ready)) ready = pF[i];
-                fr[i] = rat_add(ready, Fd[i], e);
-                if (s + 1 < N) outF[i] = async ? fr[i] : rat_add(fr[i], R(SRout[i]), e);
-            }
-        }
-        while (__any_sync(FULL, anyp)) {
-            // lane r-1's last stage: its output and whether it is final
-            const Rat in = shfl_up_rat(outF[S - 1], 1, G);
-            const bool inDone = __shfl_up_sync(FULL, (int)!pend[S - 1], 1, G) != 0;
-            anyp = false;
-#pragma unroll
-            for (int i = 0; i < S; ++i) {
-                if (!pend[i]) continue;
-                const bool ok = i > 0 ? !pend[i - 1] : (r > 0 && inDone);
-                if (!ok) { anyp = true; continue; }
-                const int s = r * S + i;
-                const Rat arr = i > 0 ? outF[i - 1] : in;
-                Rat ready = fr[i];
-                if (rat_gt(arr, ready)) ready = arr;
-                fr[i] = rat_add(ready, Fd[i], e);
-                if (s + 1 < N) outF[i] = async ? fr[i] : rat_add(fr[i], R(SRout[i]), e);
-                pend[i] = false;
-            }
-        }
-        // ---- B ops, descending; out = end (+ SR when sync) for stages s > 0
-        Rat outB[S];
-        anyp = false;
-#pragma unroll
-        for (int i = S - 1; i >= 0; --i) {
-            const int s = r * S + i;
-            outB[i] = Rat{0, 1};
-            pend[i] = isB[i] && chB[i];
-            anyp |= pend[i];
-            if (isB[i] && !chB[i]) {
-                Rat ready = fr[i];
-                if (s + 1 < N && rat_gt(pB[i], ready)) ready = pB[i];
-                fr[i] = rat_add(ready, Bd[i], e);
-                if (s > 0) outB[i] = async ? fr[i] : rat_add(fr[i], R(SRin[i]), e);
-            }
-        }
-        while (__any_sync(FULL, anyp)) {
-            const Rat in = shfl_down_rat(outB[0], 1, G);
-            const bool inDone = __shfl_down_sync(FULL, (int)!pend[0], 1, G) != 0;
-            anyp = false;
-#pragma unroll
-            for (int i = S - 1; i >= 0; --i) {
-                if (!pend[i]) continue;
-                const bool ok = i + 1 < S ? !pend[i + 1] : (r + 1 < G && inDone);
-                if (!ok) { anyp = true; continue; }
-                const int s = r * S + i;
-                const Rat arr = i + 1 < S ? outB[i + 1] : in;
-                Rat ready = fr[i];
-                if (rat_gt(arr, ready)) ready = arr;
-                fr[i] = rat_add(ready, Bd[i], e);
-                if (s > 0) outB[i] = async ? fr[i] : rat_add(fr[i], R(SRin[i]), e);
-                pend[i] = false;
-            }
-        }
-        // ---- mailboxes: F from stage s-1, B from stage s+1 (unless consumed
-        // by this position's chain)
-        {
-            const Rat inF = shfl_up_rat(outF[S - 1], 1, G);
-            const int64_t inFm = __shfl_up_sync(FULL, isF[S - 1] ? mm[S - 1] : (int64_t)-1, 1, G);
-            const Rat inB = shfl_down_rat(outB[0], 1, G);
-            const int64_t inBm = __shfl_down_sync(FULL, isB[0] ? mm[0] : (int64_t)-1, 1, G);
-#pragma unroll
-            for (int i = 0; i < S; ++i) {
-                const int s = r * S + i;
-                if (!has[i] || !live) continue;
-                Rat v_in;
-                int64_t m_in;
-                if (i > 0) { v_in = outF[i - 1]; m_in = isF[i - 1] ? mm[i - 1] : -1; }
-                else { v_in = inF; m_in = r > 0 ? inFm : -1; }
-                if (s > 0 && m_in >= 0 && !(chF[i] && mm[i] == m_in)) pF[i] = v_in;
-                if (i + 1 < S) { v_in = outB[i + 1]; m_in = isB[i + 1] ? mm[i + 1] : -1; }
-                else { v_in = inB; m_in = r + 1 < G ? inBm : -1; }
-                if (s + 1 < N && m_in >= 0 && !(chB[i] && mm[i] == m_in)) pB[i] = v_in;
-            }
-        }
-        dead = (__ballot_sync(FULL, e.bad()) & gmask) != 0;
-    }
-    // ---- makespan (simulator.hpp:173-180) and the post-simulation Rat checks
-    Rat mk{0, 1};
-#pragma unroll
-    for (int i = 0; i < S; ++i)
-        if (has[i] && rat_gt(fr[i], mk)) mk = fr[i];
-    for (int o = 1; o < G; o <<= 1) {
-        const Rat y = shfl_xor_rat(mk, o, G);
-        if (rat_gt(y, mk)) mk = y;
-    }
-    if (active && !dead) {
-#pragma unroll
-        for (int i = 0; i < S; ++i) {
-            const int s = r * S + i;
-            if (!has[i]) continue;
-            // feature high-water: min(M, depth) * a (219-238)
-            if ((i128)wv[i] * A[i] > (i128)INT64_MAX) e.set(ERR_OVERFLOW);
-            // busy fraction Rat(M * SR) / makespan (239-244)
-            if (s + 1 < N && mk.n != 0) (void)rat_div(R(M * SRout[i]), mk, e);
-        }
-    }
-    const unsigned bad = __ballot_sync(FULL, e.bad());
-    if (active && r == 0) {
-        bp_candidate& cd = B.cand[ci];
-        if (bad & gmask) {
-            cd.status = BP_C_ERR_OVERFLOW;
-        } else {
-            cd.makespan = bp_rat{mk.n, mk.d};
-            cd.status = BP_C_OK;
-        }
-    }
-    }  // persistent loop
-}
-
 static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
-
-void launch_sim_xwave(const BatchDev& B, int k, int sms, cudaStream_t st) {
-    const int grid = sms * 8;   // persistent warps
-    const int cls = SIM_XWAVE + k;
-    switch (k) {
-        case 0: k_sim_xwave<4, 1><<<grid, SIM_THREADS, 0, st>>>(B, cls); break;
-        case 1: k_sim_xwave<8, 1><<<grid, SIM_THREADS, 0, st>>>(B, cls); break;
-        case 2: k_sim_xwave<16, 1><<<grid, SIM_THREADS, 0, st>>>(B, cls); break;
-        case 3: k_sim_xwave<32, 1><<<grid, SIM_THREADS, 0, st>>>(B, cls); break;
-        case 4: k_sim_xwave<32, 2><<<grid, SIM_THREADS, 0, st>>>(B, cls); break;
-        default: break;
-    }
-}
 
 void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.sim_count, 0, SIM_CLASSES * sizeof(int32_t), st);
@@ -653,7 +393,7 @@ size_t sim_exact_state_bytes(int sms, int max_N) {
 
 void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st) {
     if (!B.ncand) return;
-    cudaMemsetAsync(B.xhist, 0, XBUCKETS * sizeof(int32_t), st);
+    cudaMemsetAsync(B.xhist, 0, (XBUCKETS + 1) * sizeof(int32_t), st);
     k_xsort_count<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);
     k_xsort_scan<<<1, 1024, 0, st>>>(B);
     k_xsort_scatter<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);

@@ -38,9 +38,6 @@ def bench_name(kernel, seen):
     if k.startswith("k_sim_fast"):
         g = k.split("<")[1].rstrip(">").replace(" ", "").split(",")
         return f"sim_fast_g{g[0]}" + (f"s{g[1]}" if g[1] != "1" else "")
-    if k.startswith("k_sim_xwave"):
-        g = k.split("<")[1].rstrip(">").replace(" ", "").split(",")
-        return f"sim_xwave_g{g[0]}" + (f"s{g[1]}" if g[1] != "1" else "")
     return {"k_refine": "refine", "k_prune": "prune", "k_sim_exact": "sim_exact", "k_setup": "setup",
             "k_bottleneck": "bottleneck", "k_rank": "rank", "k_sim_prep": "sim_prep", "k_best": "best",
             "k_cost_prefix": "cost_prefix"}.get(k, k)
