@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbapipe_b200.so")
-SOURCES = ["api.cu", "kernels.cu", "dp.cu", "sim.cu"]
+SOURCES = ["api.cu", "kernels.cu", "dp.cu", "sim.cu", "xwave.cu"]
 HEADERS = ["rat.cuh", "common.cuh", "model.cuh", "batch.cuh", "phases.cuh", "kernels.h", "host_prep.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -295,6 +295,13 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     size_t o_xkey = L.take<int32_t>(nc), o_xsorted = L.take<int32_t>(nc), o_xhist = L.take<int32_t>(XBUCKETS + 1);
     size_t o_cq = L.take<int32_t>(nc), o_co = L.take<int32_t>(nc);
     size_t o_work = L.take<unsigned long long>(WORK_SLOTS);
+    int32_t dtab = 1;
+    while (dtab < 2 * std::max(1, nq)) dtab <<= 1;
+    size_t o_qrep = L.take<int32_t>(nqs), o_dkey = L.take<unsigned long long>((size_t)dtab),
+           o_drep = L.take<int32_t>((size_t)dtab);
+    int32_t stab = 1;
+    while (stab < 2 * std::max<int64_t>(1, hb.ncand)) stab <<= 1;
+    size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
     size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(SIM_CLASSES);
     if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
     void* b = B->mem.p;
@@ -353,6 +360,13 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.dp_items = dptr<DPItem>(b, o_items);
     D.dp_count = dptr<int32_t>(b, o_cnt);
     D.work = dptr<unsigned long long>(b, o_work);
+    D.qrep = dptr<int32_t>(b, o_qrep);
+    D.dkey = dptr<unsigned long long>(b, o_dkey);
+    D.drep = dptr<int32_t>(b, o_drep);
+    D.dmask = dtab - 1;
+    D.skey = dptr<unsigned long long>(b, o_skey);
+    D.srep = dptr<int32_t>(b, o_srep);
+    D.smask = stab - 1;
     D.qorder = dptr<int32_t>(b, o_qord);
     D.cperm = dptr<int32_t>(b, o_cperm);
     D.sim_list = dptr<int32_t>(b, o_slist);
@@ -388,11 +402,14 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(c, e, "memset");
     const int T = c->max_T, maxN = std::max(1, hb.max_N);
     timed(c, "setup", st, [&] { launch_setup(D, st); });
-    if (!hb.whole_items.empty())
+    timed(c, "dedup", st, [&] { launch_dedup(D, st); }, 2);
+    if (!hb.whole_items.empty()) {
         timed(c, "minmax_dp", st, [&] {
             launch_partition(D, 0, std::min<int>(B->dp_grid, (int)hb.whole_items.size()), B->dp_max_units, maxN, T,
                              st);
         });
+        timed(c, "dedup_copy", st, [&] { launch_dedup_copy_dp(D, st); });
+    }
     timed(c, "bottleneck", st, [&] { launch_bottleneck(D, st); });
     // fork: coarse DPs (side stream) || refine (main stream); both only read
     // the whole-layer DP results and write disjoint state
@@ -408,13 +425,17 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
               [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, c->side); });
     cudaEventRecord(c->join, c->side);
     timed(c, "refine", st, [&] { launch_refine(D, st); });
+    timed(c, "dedup_copy", st, [&] { launch_dedup_copy_refine(D, st); });
     cudaStreamWaitEvent(st, c->join, 0);
     timed(c, "prune", st, [&] { launch_prune(D, st); });
-    timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); });
+    timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
     for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
+    timed(c, "sim_flow32", st, [&] { launch_sim_flow(D, 0, c->sm_count, st); });
+    timed(c, "sim_flow64", st, [&] { launch_sim_flow(D, 1, c->sm_count, st); });
     timed(c, "sim_exact", st, [&] { launch_sim_exact(D, c->sm_count, st); }, 4);
+    timed(c, "sim_share", st, [&] { launch_sim_share(D, st); });
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "kernel launch");
@@ -440,7 +461,7 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
         unsigned long long work[WORK_SLOTS];
         static const char* names[SIM_CLASSES] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                                  "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4",
-                                                 "sim_fast_g32s8", "sim_exact"};
+                                                 "sim_fast_g32s8", "sim_exact", "sim_flow32", "sim_flow64"};
         if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess) {
             c->stats["minmax_dp"].work = (double)work[WORK_DP_WHOLE];
             c->stats["minmax_dp_coarse"].work = (double)work[WORK_DP_COARSE];

@@ -23,6 +23,7 @@ struct QDesc {
 // Per-query device state.
 struct QState {
     int32_t need_refine;
+    int32_t grp_refine;    // some query sharing this one's class needs refine (rep only)
     int32_t dp_shape;      // 1 = InfeasibleShape (U < N) for the whole-layer DP
     int32_t refine_err;    // Err code of refine + refined-plan stage sums
     int32_t refined;       // refine ran
@@ -53,8 +54,13 @@ enum { PLAN_NONE = 0, PLAN_REFINED = 1, PLAN_WHOLE = 2 };
 
 // Simulator classes: 0..4 = lanes per candidate 2, 4, 8, 16, 32 (one stage
 // per lane); 5, 6, 7 = 32 lanes with 2, 4, 8 stages per lane; 8 = exact
-// (Rat) slow path, thread per candidate.
-enum { SIM_CLASSES = 9, SIM_EXACT = 8 };
+// (Rat) path, thread per candidate; 9, 10 = exact (Rat) dataflow, block per
+// candidate, thread per stage (xwave.cu), for the heavy exact candidates with
+// N <= 32 / N <= 64.
+enum { SIM_CLASSES = 11, SIM_EXACT = 8, SIM_FLOW = 9, SIM_FLOW_CLASSES = 2 };
+// exact candidates with at least this many events (and 8 <= N <= 64) go to
+// the dataflow kernel: their serial walk would otherwise set the kernel time
+constexpr int64_t FLOW_MIN_EVENTS = 1024;
 // instrumentation slots of BatchDev::work (algorithmic work of one run)
 enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_SIM_EVENTS = 2, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
 enum { XBUCKETS = 32768, XSIM_WARPS_PER_SM = 32 };
@@ -64,6 +70,8 @@ struct CState {
     int32_t plan_kind;
     int32_t sim_ready;     // 1: passed estimate + memory check, needs simulate
     int64_t D;             // simulator scale for this candidate's plan
+    int32_t sim_cls;       // simulator class, -1 = not simulated
+    int32_t sim_rep;       // candidate whose identical simulation this one shares, -1 = none
 };
 
 // DP work item: a (query, a_th) pair; a_th < 0 = whole-layer partition.
@@ -107,6 +115,16 @@ struct BatchDev {
     int32_t* xsorted;         // [ncand]
     int32_t* xhist;           // [XBUCKETS] counts, then running offsets; [XBUCKETS] = chunk counter
     int max_N;                // largest stage count in the batch (exact-sim state sizing)
+    // batch-level deduplication of the whole-layer DP + refine (kernels.cu):
+    // qrep[q] = the query whose results q shares (q itself if none); NULL in
+    // the host emulation (no sharing)
+    int32_t* qrep;
+    unsigned long long* dkey; // [dmask+1] open-addressing table of class hashes
+    int32_t* drep;            // [dmask+1] smallest query index per hash
+    int32_t dmask;
+    unsigned long long* skey; // [smask+1] simulation-input hashes (sim.cu)
+    int32_t* srep;            // [smask+1] smallest candidate index per hash
+    int32_t smask;
     int details;              // write bp_stage records
     // DP work lists
     DPItem* dp_items;

@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
     const int n_items = B.dp_count[which];
     for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         DPItem item = B.dp_items[(which == 0 ? 0 : B.nq) + it];
+        if (which == 0 && B.qrep[item.q] != item.q) continue;   // shared: k_dedup_copy_dp
         const QDesc Q = B.q[item.q];
         NetView v = net_view(B.P, Q.net);
         ChainView c = chain_view(B.P, Q.cl, Q.N);

@@ -111,6 +111,119 @@ __global__ void k_bottleneck(BatchDev B) {
             B.dp_items[B.nq + idx] = DPItem{qi, m, B.ms[Q.mslot_off + m].a_th};
         }
     }
+    if (B.qs[qi].need_refine) atomicOr(&B.qs[B.qrep[qi]].grp_refine, 1);
+}
+
+// ---- batch-level deduplication of identical partition subproblems.
+// The whole-layer DP (partition.hpp:112-185) and intra_layer_refine (248-333)
+// are functions of (network, stage count, accelerator-type sequence of the
+// chain) only: link bandwidths, capacities, mode and micro-batching enter
+// later (bottleneck test, coarse DP, estimate, fine-tune, simulate).  Queries
+// of one batch that share the triple -- cluster mixes that differ only in
+// memory, links or mode -- are solved once, inside the run, by the smallest
+// such query index, and the results are copied.  The hash only groups: keys
+// are compared exactly, so the outputs equal per-query evaluation bit for bit.
+__device__ uint64_t class_hash(const BatchDev& B, int qi) {
+    const QDesc Q = B.q[qi];
+    const ChainView c = chain_view(B.P, Q.cl, Q.N);
+    uint64_t h = 0xcbf29ce484222325ull ^ ((uint64_t)(uint32_t)Q.net << 20) ^ (uint64_t)(uint32_t)Q.N;
+    for (int s = 0; s < Q.N; ++s) {
+        h ^= (uint64_t)(uint32_t)(c.type[s] + 1);
+        h *= 0x100000001b3ull;
+        h ^= h >> 29;
+    }
+    return h ? h : 1;
+}
+
+__device__ bool same_class(const BatchDev& B, int a, int b) {
+    const QDesc A = B.q[a], Q = B.q[b];
+    if (A.net != Q.net || A.N != Q.N) return false;
+    const ChainView ca = chain_view(B.P, A.cl, A.N), cb = chain_view(B.P, Q.cl, Q.N);
+    for (int s = 0; s < A.N; ++s)
+        if (ca.type[s] != cb.type[s]) return false;
+    return true;
+}
+
+__device__ __forceinline__ uint32_t class_slot(const BatchDev& B, uint64_t h) {
+    return (uint32_t)(h ^ (h >> 32)) & (uint32_t)B.dmask;
+}
+
+__global__ void k_dedup_insert(BatchDev B) {
+    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq || !B.q[qi].schema_ok) return;
+    const uint64_t h = class_hash(B, qi);
+    for (uint32_t slot = class_slot(B, h);; slot = (slot + 1) & (uint32_t)B.dmask) {
+        const unsigned long long prev = atomicCAS(&B.dkey[slot], 0ull, (unsigned long long)h);
+        if (prev == 0ull || prev == h) {
+            atomicMin(&B.drep[slot], qi);
+            return;
+        }
+    }
+}
+
+__global__ void k_dedup_resolve(BatchDev B) {
+    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    int rep = qi;
+    if (B.q[qi].schema_ok) {
+        const uint64_t h = class_hash(B, qi);
+        uint32_t slot = class_slot(B, h);
+        while (B.dkey[slot] != h) slot = (slot + 1) & (uint32_t)B.dmask;
+        const int r = B.drep[slot];
+        if (r != qi && same_class(B, qi, r)) rep = r;
+    }
+    B.qrep[qi] = rep;
+}
+
+// whole-layer DP results: plan ranges, max stage time, InfeasibleShape flag
+__global__ void k_dedup_copy_dp(BatchDev B) {
+    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    const int r = B.qrep[qi];
+    if (r == qi) return;
+    const QState& s = B.qs[r];
+    QState& d = B.qs[qi];
+    d.dp_shape = s.dp_shape;
+    d.target = s.target;
+    const int64_t o = B.q[qi].qstage_off, os = B.q[r].qstage_off;
+    for (int k = 0; k < B.q[qi].N; ++k) {
+        B.qlo[o + k] = B.qlo[os + k];
+        B.qhi[o + k] = B.qhi[os + k];
+    }
+}
+
+// refined plan, its stage sums and validate_plan outcome, simulator scale
+__global__ void k_dedup_copy_refine(BatchDev B) {
+    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    const int r = B.qrep[qi];
+    if (r == qi || !B.qs[qi].need_refine) return;
+    const QState& s = B.qs[r];
+    QState& d = B.qs[qi];
+    d.refine_err = s.refine_err;
+    d.refined = s.refined;
+    d.refine_iters = s.refine_iters;
+    d.refine_evals = s.refine_evals;
+    d.refine_moves = s.refine_moves;
+    d.refine_exact = s.refine_exact;
+    d.vcode = s.vcode;
+    d.verr = s.verr;
+    d.vwhere = s.vwhere;
+    d.vaux = s.vaux;
+    d.D = s.D;
+    d.sumFB_D = s.sumFB_D;
+    const int64_t o = B.q[qi].qstage_off, os = B.q[r].qstage_off;
+    for (int k = 0; k < B.q[qi].N; ++k) {
+        B.qlo[o + k] = B.qlo[os + k];
+        B.qhi[o + k] = B.qhi[os + k];
+        B.qlead[o + k] = B.qlead[os + k];
+        B.qtrail[o + k] = B.qtrail[os + k];
+        B.qF[o + k] = B.qF[os + k];
+        B.qB[o + k] = B.qB[os + k];
+        B.qW[o + k] = B.qW[os + k];
+        B.qT[o + k] = B.qT[os + k];
+        B.qdirty[o + k] = B.qdirty[os + k];
+    }
 }
 
 // Queries / candidates are visited in the host's scheduling order
@@ -187,6 +300,20 @@ void launch_cost_prefix(const NetDesc* nets, int n_nets, const int64_t* fp, cons
 
 void launch_setup(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_setup<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+}
+void launch_dedup(const BatchDev& B, cudaStream_t st) {
+    cudaMemsetAsync(B.dkey, 0, ((size_t)B.dmask + 1) * sizeof(unsigned long long), st);
+    cudaMemsetAsync(B.drep, 0x7f, ((size_t)B.dmask + 1) * sizeof(int32_t), st);
+    if (B.nq) {
+        k_dedup_insert<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+        k_dedup_resolve<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    }
+}
+void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st) {
+    if (B.nq) k_dedup_copy_dp<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+}
+void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st) {
+    if (B.nq) k_dedup_copy_refine<<<blocks(B.nq, 128), 128, 0, st>>>(B);
 }
 void launch_bottleneck(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_bottleneck<<<blocks(B.nq, 128), 128, 0, st>>>(B);

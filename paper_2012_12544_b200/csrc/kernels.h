@@ -14,11 +14,16 @@ void launch_partition(const BatchDev& B, int which, int grid, int max_units, int
                       cudaStream_t st);
 size_t partition_smem_bytes(int max_units, int max_N, int T_slots);
 void launch_bottleneck(const BatchDev& B, cudaStream_t st);
+void launch_dedup(const BatchDev& B, cudaStream_t st);
+void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st);
+void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
 void launch_refine(const BatchDev& B, cudaStream_t st);
 void launch_prune(const BatchDev& B, cudaStream_t st);
 void launch_sim_prep(const BatchDev& B, cudaStream_t st);
+void launch_sim_share(const BatchDev& B, cudaStream_t st);
 void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st);
 void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st);
+void launch_sim_flow(const BatchDev& B, int k, int sms, cudaStream_t st);
 size_t sim_exact_state_bytes(int sms, int max_N);
 void launch_rank(const BatchDev& B, cudaStream_t st);
 void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,

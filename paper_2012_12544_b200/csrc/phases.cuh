@@ -124,7 +124,10 @@ BPK_HD int64_t lcm_sat(int64_t D, int64_t d) {
 BPK_HDNI void refine_query(const BatchDev& B, int qi) {
     const QDesc Q = B.q[qi];
     QState& qs = B.qs[qi];
-    if (!Q.schema_ok || !qs.need_refine || qs.dp_shape || Q.N < 2) return;
+    // with batch dedup only the class representative refines (for its whole
+    // class); the emulation (qrep == NULL) refines every query that needs it
+    const bool need = B.qrep ? (B.qrep[qi] == qi && qs.grp_refine) : qs.need_refine;
+    if (!Q.schema_ok || !need || qs.dp_shape || Q.N < 2) return;
     NetView v = net_view(B.P, Q.net);
     ChainView c = chain_view(B.P, Q.cl, Q.N);
     const int64_t o = Q.qstage_off;
@@ -410,7 +413,10 @@ struct SimState {
 // at the same position (a chain); the carry register defers the mailbox
 // write until the receiver has read its own input, which is what keeps one
 // slot sufficient (at most one arrival is outstanding per link direction).
-BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S) {
+BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S_in) {
+    // a register copy: through the reference every access reloaded the
+    // seven base pointers from local memory (the Rat calls may alias them)
+    const SimState S = S_in;
     const CState& cs = B.cs[ci];
     bp_candidate& cd = B.cand[ci];
     const int qi = B.cq[ci];

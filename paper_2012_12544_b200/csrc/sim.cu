@@ -21,6 +21,8 @@
 // Slow path (k_sim_exact): thread per candidate, exact Rat events
 // (phases.cuh:sim_exact), for candidates whose scaled times could exceed int64
 // -- exactly where the reference's Rats might overflow.
+#include <cstdlib>
+
 #include "kernels.h"
 #include "phases.cuh"
 
@@ -32,13 +34,108 @@ constexpr int SIM_THREADS = 128;
 __device__ __forceinline__ int64_t smax(int64_t a, int64_t b) { return a > b ? a : b; }
 __device__ __forceinline__ int64_t sat(int64_t x) { return x < NEGV ? NEGV : x; }
 
+// ---- batch-level deduplication of identical simulations.  simulate()'s
+// inputs are the plan (layer ranges + fractions, through F/B per stage), the
+// chain's types, kind, M, micro and the link bandwidths (SR per link);
+// capacities only decide WHETHER a candidate is simulated.  Candidates whose
+// inputs coincide (e.g. cluster mixes differing only in memory) are
+// simulated once, by the smallest candidate index, inside the run; the hash
+// only groups, inputs are compared exactly.
+__device__ uint64_t sim_hash(const BatchDev& B, int64_t ci) {
+    const bp_candidate& cd = B.cand[ci];
+    const CState& cs = B.cs[ci];
+    const int qi = B.cq[ci];
+    const QDesc Q = B.q[qi];
+    const ChainView c = chain_view(B.P, Q.cl, Q.N);
+    uint64_t h = 0xcbf29ce484222325ull;
+    auto mix = [&](uint64_t x) { h ^= x; h *= 0x100000001b3ull; h ^= h >> 29; };
+    mix((uint64_t)(uint32_t)B.qrep[qi]);
+    mix((uint64_t)cs.plan_kind * 8 + (uint64_t)cd.kind);
+    mix((uint64_t)cd.M);
+    mix((uint64_t)cd.micro);
+    for (int k = 0; k + 1 < Q.N; ++k) mix((uint64_t)c.bw[k]);
+    if (cs.plan_kind != PLAN_REFINED) {
+        const int64_t slot = Q.stage_off + (ci - Q.cand_off) * Q.N;
+        for (int s = 0; s < Q.N; ++s) mix(((uint64_t)(uint32_t)B.clo[slot + s] << 32) | (uint32_t)B.chi[slot + s]);
+    }
+    return h ? h : 1;
+}
+
+__device__ bool same_sim(const BatchDev& B, int64_t a, int64_t b) {
+    const bp_candidate &x = B.cand[a], &y = B.cand[b];
+    const CState &cx = B.cs[a], &cy = B.cs[b];
+    const int qa = B.cq[a], qb = B.cq[b];
+    if (B.qrep[qa] != B.qrep[qb] || cx.plan_kind != cy.plan_kind || x.kind != y.kind || x.M != y.M ||
+        x.micro != y.micro)
+        return false;
+    const QDesc A = B.q[qa], Q = B.q[qb];   // same class: same network, N and stage types
+    const ChainView ca = chain_view(B.P, A.cl, A.N), cb = chain_view(B.P, Q.cl, Q.N);
+    for (int k = 0; k + 1 < A.N; ++k)
+        if (ca.bw[k] != cb.bw[k]) return false;
+    if (cx.plan_kind != PLAN_REFINED) {
+        const int64_t sa = A.stage_off + (a - A.cand_off) * A.N, sb = Q.stage_off + (b - Q.cand_off) * Q.N;
+        for (int s = 0; s < A.N; ++s)
+            if (B.clo[sa + s] != B.clo[sb + s] || B.chi[sa + s] != B.chi[sb + s]) return false;
+    }
+    return true;
+}
+
+__device__ __forceinline__ uint32_t sim_slot(const BatchDev& B, uint64_t h) {
+    return (uint32_t)(h ^ (h >> 32)) & (uint32_t)B.smask;
+}
+
+__global__ void k_sim_classify(BatchDev B) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.ncand) return;
+    const int64_t ci = B.cperm[i];
+    int cls = sim_classify(B, ci);
+    if (cls == SIM_EXACT) {
+        const bp_candidate& c = B.cand[ci];
+        const int64_t N = c.n_stages, ev = 2 * N * c.M + (c.kind >= 2 ? 2 * (N - 1) * c.M : 0);
+        if (N >= 8 && N <= 64 && ev >= FLOW_MIN_EVENTS) cls = SIM_FLOW + (N <= 32 ? 0 : 1);
+    }
+    B.cs[ci].sim_cls = cls;
+    B.cs[ci].sim_rep = -1;
+    if (cls < 0) return;
+    const uint64_t h = sim_hash(B, ci);
+    for (uint32_t slot = sim_slot(B, h);; slot = (slot + 1) & (uint32_t)B.smask) {
+        const unsigned long long prev = atomicCAS(&B.skey[slot], 0ull, (unsigned long long)h);
+        if (prev == 0ull || prev == h) {
+            atomicMin(&B.srep[slot], (int32_t)ci);
+            return;
+        }
+    }
+}
+
+// simulated candidates whose inputs equal an earlier candidate's copy its
+// outcome after the simulators ran
+__global__ void k_sim_share(BatchDev B) {
+    int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= B.ncand) return;
+    const int32_t r = B.cs[ci].sim_rep;
+    if (r < 0) return;
+    bp_candidate& cd = B.cand[ci];
+    cd.status = B.cand[r].status;
+    cd.makespan = B.cand[r].makespan;
+}
+
 __global__ void k_sim_prep(BatchDev B) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int cls = -1;
     uint64_t ev = 0;
     if (i < B.ncand) {
         int64_t ci = B.cperm[i];
-        cls = sim_classify(B, ci);
+        cls = B.cs[ci].sim_cls;
+        if (cls >= 0) {
+            const uint64_t h = sim_hash(B, ci);
+            uint32_t slot = sim_slot(B, h);
+            while (B.skey[slot] != h) slot = (slot + 1) & (uint32_t)B.smask;
+            const int32_t r = B.srep[slot];
+            if (r != ci && same_sim(B, ci, r)) {
+                B.cs[ci].sim_rep = r;
+                cls = -1;
+            }
+        }
         if (cls >= 0) {
             int pos = atomicAdd(&B.sim_count[cls], 1);
             B.sim_list[(int64_t)cls * B.ncand + pos] = (int32_t)ci;
@@ -351,8 +448,8 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
     unsigned bad = __ballot_sync(FULL, e.bad());
     if (active && r == 0) {
         bp_candidate& cd = B.cand[ci];
-        const unsigned gm = ((1u << G) - 1u) << (lane - r);
-        if (bad & (G == 32 ? FULL : gm)) {
+        const unsigned gm = G == 32 ? FULL : ((1u << (G & 31)) - 1u) << (lane - r);
+        if (bad & gm) {
             cd.status = BP_C_ERR_OVERFLOW;
         } else {
             cd.makespan = bp_rat{mk.n, mk.d};
@@ -366,7 +463,16 @@ static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); 
 
 void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.sim_count, 0, SIM_CLASSES * sizeof(int32_t), st);
-    if (B.ncand) k_sim_prep<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+    cudaMemsetAsync(B.skey, 0, ((size_t)B.smask + 1) * sizeof(unsigned long long), st);
+    cudaMemsetAsync(B.srep, 0x7f, ((size_t)B.smask + 1) * sizeof(int32_t), st);
+    if (B.ncand) {
+        k_sim_classify<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+        k_sim_prep<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+    }
+}
+
+void launch_sim_share(const BatchDev& B, cudaStream_t st) {
+    if (B.ncand) k_sim_share<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
 }
 
 void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st) {
@@ -397,7 +503,8 @@ void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st) {
     k_xsort_count<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);
     k_xsort_scan<<<1, 1024, 0, st>>>(B);
     k_xsort_scatter<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);
-    k_sim_exact<<<sms * XSIM_WARPS_PER_SM / 8, 256, 0, st>>>(B);
+    static const int wps = getenv("BP_XSIM_WPS") ? atoi(getenv("BP_XSIM_WPS")) : XSIM_WARPS_PER_SM;   // EXPERIMENT
+    k_sim_exact<<<sms * wps / 8, 256, 0, st>>>(B);
 }
 
 }  // namespace bpk
