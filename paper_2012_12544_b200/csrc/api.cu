@@ -302,6 +302,10 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     int32_t stab = 1;
     while (stab < 2 * std::max<int64_t>(1, hb.ncand)) stab <<= 1;
     size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
+    size_t o_rlist = L.take<int32_t>(nqs), o_rcount = L.take<int32_t>(1);
+    int32_t ctab = 1;
+    while (ctab < 2 * std::max<int64_t>(1, (int64_t)nms)) ctab <<= 1;
+    size_t o_ckey = L.take<unsigned long long>((size_t)ctab), o_crep = L.take<int32_t>((size_t)ctab);
     size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(SIM_CLASSES);
     if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
     void* b = B->mem.p;
@@ -367,6 +371,11 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.skey = dptr<unsigned long long>(b, o_skey);
     D.srep = dptr<int32_t>(b, o_srep);
     D.smask = stab - 1;
+    D.ckey = dptr<unsigned long long>(b, o_ckey);
+    D.crep = dptr<int32_t>(b, o_crep);
+    D.cmask = ctab - 1;
+    D.rlist = dptr<int32_t>(b, o_rlist);
+    D.rcount = dptr<int32_t>(b, o_rcount);
     D.qorder = dptr<int32_t>(b, o_qord);
     D.cperm = dptr<int32_t>(b, o_cperm);
     D.sim_list = dptr<int32_t>(b, o_slist);
@@ -410,7 +419,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
         });
         timed(c, "dedup_copy", st, [&] { launch_dedup_copy_dp(D, st); });
     }
-    timed(c, "bottleneck", st, [&] { launch_bottleneck(D, st); });
+    timed(c, "bottleneck", st, [&] { launch_bottleneck(D, st); }, 2);
     // fork: coarse DPs (side stream) || refine (main stream); both only read
     // the whole-layer DP results and write disjoint state
     if (!c->side) {
@@ -420,14 +429,18 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     }
     cudaEventRecord(c->fork, st);
     cudaStreamWaitEvent(c->side, c->fork, 0);
-    if (hb.nmslot > 0)
+    if (hb.nmslot > 0) {
         timed(c, "minmax_dp_coarse", c->side,
               [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, c->side); });
+        timed(c, "dedup_copy", c->side, [&] { launch_coarse_copy(D, c->side); });
+    }
     cudaEventRecord(c->join, c->side);
-    timed(c, "refine", st, [&] { launch_refine(D, st); });
+    timed(c, "refine", st, [&] { launch_refine(D, c->sm_count, st); }, 2);
     timed(c, "dedup_copy", st, [&] { launch_dedup_copy_refine(D, st); });
     cudaStreamWaitEvent(st, c->join, 0);
-    timed(c, "prune", st, [&] { launch_prune(D, st); });
+    // (pruning the coarse-plan candidates on the side stream during refine was
+    // measured slower: it takes issue slots from refine's single-lane warps)
+    timed(c, "prune", st, [&] { launch_prune(D, -1, st); });
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};

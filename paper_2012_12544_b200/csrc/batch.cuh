@@ -46,7 +46,9 @@ struct MState {
     int64_t a_th;
     int64_t K;             // coarse block count
     int32_t coarse_ok;     // coarse DP done
-    int32_t pad;
+    int32_t want;          // a coarse DP is needed (bottleneck, K >= N)
+    int32_t q;             // owning query
+    int32_t crep;          // mslot whose identical coarse DP this one shares, -1 = own
 };
 
 // Per-candidate plan kinds.
@@ -125,6 +127,11 @@ struct BatchDev {
     unsigned long long* skey; // [smask+1] simulation-input hashes (sim.cu)
     int32_t* srep;            // [smask+1] smallest candidate index per hash
     int32_t smask;
+    unsigned long long* ckey; // [cmask+1] coarse-DP (class, a_th) hashes
+    int32_t* crep;            // [cmask+1] smallest mslot index per hash
+    int32_t cmask;
+    int32_t* rlist;           // [nq] queries to refine this run (compacted)
+    int32_t* rcount;          // [1]
     int details;              // write bp_stage records
     // DP work lists
     DPItem* dp_items;

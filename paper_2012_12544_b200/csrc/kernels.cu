@@ -101,17 +101,81 @@ __global__ void k_setup(BatchDev B) {
     if (qi < B.nq) setup_query(B, qi);
 }
 
+__device__ __forceinline__ uint64_t coarse_hash(int32_t cls, int64_t a_th) {
+    uint64_t h = 0x9e3779b97f4a7c15ull ^ ((uint64_t)(uint32_t)cls * 0xbf58476d1ce4e5b9ull);
+    h ^= (uint64_t)a_th + 0x94d049bb133111ebull + (h << 6) + (h >> 2);
+    h *= 0xbf58476d1ce4e5b9ull;
+    h ^= h >> 31;
+    return h ? h : 1;
+}
+
 __global__ void k_bottleneck(BatchDev B) {
     int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi >= B.nq) return;
     const QDesc Q = B.q[qi];
     for (int m = 0; m < Q.nbase; ++m) {
+        MState& ms = B.ms[Q.mslot_off + m];
+        ms.q = qi;
+        ms.crep = -1;
         if (bottleneck_slot(B, qi, m)) {
-            int idx = atomicAdd(&B.dp_count[1], 1);
-            B.dp_items[B.nq + idx] = DPItem{qi, m, B.ms[Q.mslot_off + m].a_th};
+            // the coarse DP is a function of (class, a_th): group identical ones
+            ms.want = 1;
+            const uint64_t h = coarse_hash(B.qrep[qi], ms.a_th);
+            const int32_t id = (int32_t)(Q.mslot_off + m);
+            for (uint32_t slot = (uint32_t)(h ^ (h >> 32)) & (uint32_t)B.cmask;; slot = (slot + 1) & (uint32_t)B.cmask) {
+                const unsigned long long prev = atomicCAS(&B.ckey[slot], 0ull, (unsigned long long)h);
+                if (prev == 0ull || prev == h) {
+                    atomicMin(&B.crep[slot], id);
+                    break;
+                }
+            }
         }
     }
     if (B.qs[qi].need_refine) atomicOr(&B.qs[B.qrep[qi]].grp_refine, 1);
+}
+
+// queue one coarse DP per distinct (class, a_th); the others share its plan
+__global__ void k_coarse_queue(BatchDev B) {
+    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    const QDesc Q = B.q[qi];
+    for (int m = 0; m < Q.nbase; ++m) {
+        MState& ms = B.ms[Q.mslot_off + m];
+        if (!ms.want) continue;
+        const uint64_t h = coarse_hash(B.qrep[qi], ms.a_th);
+        uint32_t slot = (uint32_t)(h ^ (h >> 32)) & (uint32_t)B.cmask;
+        while (B.ckey[slot] != h) slot = (slot + 1) & (uint32_t)B.cmask;
+        const int32_t r = B.crep[slot], id = (int32_t)(Q.mslot_off + m);
+        if (r != id && B.qrep[B.ms[r].q] == B.qrep[qi] && B.ms[r].a_th == ms.a_th) {
+            ms.crep = r;
+        } else {
+            int idx = atomicAdd(&B.dp_count[1], 1);
+            B.dp_items[B.nq + idx] = DPItem{qi, m, ms.a_th};
+        }
+    }
+}
+
+// shared coarse plans: both kinds' candidate slots of the M slot
+__global__ void k_coarse_copy(BatchDev B) {
+    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    const QDesc Q = B.q[qi];
+    for (int m = 0; m < Q.nbase; ++m) {
+        MState& ms = B.ms[Q.mslot_off + m];
+        if (ms.crep < 0) continue;
+        const MState& rm = B.ms[ms.crep];
+        const QDesc R = B.q[rm.q];
+        const int rmm = (int)(ms.crep - R.mslot_off);
+        ms.coarse_ok = rm.coarse_ok;
+        for (int k = 0; k < 2; ++k) {
+            const int64_t o = Q.stage_off + ((int64_t)k * Q.nbase + m) * Q.N;
+            const int64_t ro = R.stage_off + ((int64_t)k * R.nbase + rmm) * R.N;
+            for (int s = 0; s < Q.N; ++s) {
+                B.clo[o + s] = B.clo[ro + s];
+                B.chi[o + s] = B.chi[ro + s];
+            }
+        }
+    }
 }
 
 // ---- batch-level deduplication of identical partition subproblems.
@@ -233,9 +297,41 @@ __global__ void k_refine(BatchDev B) {
     if (i < B.nq) refine_query(B, B.qorder[i]);
 }
 
-__global__ void k_prune(BatchDev B) {
+// intra_layer_refine is a long serial walk per query (up to ~3000 boundary
+// steps at N = 64); with its per-stage arrays in global memory every step
+// waits on L2 several times.  The queries that refine this run (class
+// representatives, see k_dedup_insert) are compacted and each gets a warp of
+// its own (lane 0 runs it: the queries' control flow diverges completely, so
+// packing them into lanes only serialises them) with its plan and stage-time
+// caches in shared memory; up to 32 such warps per SM hide each other's
+// latency.
+__global__ void k_refine_list(BatchDev B) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.nq) return;
+    const int qi = B.qorder[i];
+    if (refine_wanted(B, qi)) B.rlist[atomicAdd(B.rcount, 1)] = qi;
+}
+
+__global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm) {
+    extern __shared__ __align__(16) unsigned char rsm[];
+    if (threadIdx.x != 0) return;
+    unsigned char* base = rsm;
+    RefineScratch sc;
+    sc.lead = reinterpret_cast<Rat*>(base);
+    sc.trail = sc.lead + nm;
+    sc.tF = sc.trail + nm;
+    sc.tB = sc.tF + nm;
+    sc.tT = sc.tB + nm;
+    sc.lo = reinterpret_cast<int32_t*>(sc.tT + nm);
+    sc.hi = sc.lo + nm;
+    sc.dirty = reinterpret_cast<uint8_t*>(sc.hi + nm);
+    const int count = *B.rcount;
+    for (int i = blockIdx.x; i < count; i += gridDim.x) refine_query_at(B, B.rlist[i], &sc);
+}
+
+__global__ void k_prune(BatchDev B, int pass) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < B.ncand) prune_candidate(B, B.cperm[i]);
+    if (i < B.ncand) prune_candidate(B, B.cperm[i], pass);
 }
 
 __global__ void k_rank(BatchDev B) {
@@ -316,13 +412,41 @@ void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_dedup_copy_refine<<<blocks(B.nq, 128), 128, 0, st>>>(B);
 }
 void launch_bottleneck(const BatchDev& B, cudaStream_t st) {
-    if (B.nq) k_bottleneck<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    cudaMemsetAsync(B.ckey, 0, ((size_t)B.cmask + 1) * sizeof(unsigned long long), st);
+    cudaMemsetAsync(B.crep, 0x7f, ((size_t)B.cmask + 1) * sizeof(int32_t), st);
+    if (B.nq) {
+        k_bottleneck<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+        k_coarse_queue<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    }
 }
-void launch_refine(const BatchDev& B, cudaStream_t st) {
-    if (B.nq) k_refine<<<blocks(B.nq, 64), 64, 0, st>>>(B);
+void launch_coarse_copy(const BatchDev& B, cudaStream_t st) {
+    if (B.nq) k_coarse_copy<<<blocks(B.nq, 128), 128, 0, st>>>(B);
 }
-void launch_prune(const BatchDev& B, cudaStream_t st) {
-    if (B.ncand) k_prune<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
+size_t refine_region_bytes(int max_N) {
+    size_t r = (size_t)max_N * (5 * sizeof(Rat) + 2 * sizeof(int32_t) + 1);
+    r = (r + 7) & ~(size_t)7;
+    if (((r / 8) & 1) == 0) r += 8;
+    return r;
+}
+
+void launch_refine(const BatchDev& B, int sms, cudaStream_t st) {
+    if (!B.nq) return;
+    const size_t bytes = refine_region_bytes(B.max_N);
+    if (bytes > 200 * 1024) {   // very long chains: global-memory version
+        k_refine<<<blocks(B.nq, 64), 64, 0, st>>>(B);
+        return;
+    }
+    static size_t attr = 0;
+    if (bytes > attr) {
+        cudaFuncSetAttribute(k_refine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        attr = bytes;
+    }
+    cudaMemsetAsync(B.rcount, 0, sizeof(int32_t), st);
+    k_refine_list<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    k_refine_smem<<<sms * 32, 32, bytes, st>>>(B, B.max_N);
+}
+void launch_prune(const BatchDev& B, int pass, cudaStream_t st) {
+    if (B.ncand) k_prune<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
 }
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);

@@ -15,10 +15,11 @@ void launch_partition(const BatchDev& B, int which, int grid, int max_units, int
 size_t partition_smem_bytes(int max_units, int max_N, int T_slots);
 void launch_bottleneck(const BatchDev& B, cudaStream_t st);
 void launch_dedup(const BatchDev& B, cudaStream_t st);
+void launch_coarse_copy(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
-void launch_refine(const BatchDev& B, cudaStream_t st);
-void launch_prune(const BatchDev& B, cudaStream_t st);
+void launch_refine(const BatchDev& B, int sms, cudaStream_t st);
+void launch_prune(const BatchDev& B, int pass, cudaStream_t st);
 void launch_sim_prep(const BatchDev& B, cudaStream_t st);
 void launch_sim_share(const BatchDev& B, cudaStream_t st);
 void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st);

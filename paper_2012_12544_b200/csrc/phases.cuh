@@ -121,24 +121,52 @@ BPK_HD int64_t lcm_sat(int64_t D, int64_t d) {
     return (int64_t)l;
 }
 
-BPK_HDNI void refine_query(const BatchDev& B, int qi) {
+// Per-stage working arrays of one refine (the plan and the stage-time
+// caches).  The kernel keeps them in shared memory (k_refine_smem); NULL =
+// work in the query's global arrays.
+struct RefineScratch {
+    int32_t *lo, *hi;
+    Rat *lead, *trail, *tF, *tB, *tT;
+    uint8_t* dirty;
+};
+
+BPK_HD bool refine_wanted(const BatchDev& B, int qi) {
     const QDesc Q = B.q[qi];
-    QState& qs = B.qs[qi];
+    const QState& qs = B.qs[qi];
     // with batch dedup only the class representative refines (for its whole
     // class); the emulation (qrep == NULL) refines every query that needs it
     const bool need = B.qrep ? (B.qrep[qi] == qi && qs.grp_refine) : qs.need_refine;
-    if (!Q.schema_ok || !need || qs.dp_shape || Q.N < 2) return;
+    return Q.schema_ok && need && !qs.dp_shape && Q.N >= 2;
+}
+
+BPK_HDNI void refine_query_at(const BatchDev& B, int qi, const RefineScratch* sc) {
+    const QDesc Q = B.q[qi];
+    QState& qs = B.qs[qi];
+    if (!refine_wanted(B, qi)) return;
     NetView v = net_view(B.P, Q.net);
     ChainView c = chain_view(B.P, Q.cl, Q.N);
     const int64_t o = Q.qstage_off;
-    int32_t* lo = B.qlo + o;
-    int32_t* hi = B.qhi + o;
-    Rat* lead = B.qlead + o;
-    Rat* trail = B.qtrail + o;
-    for (int s = 0; s < Q.N; ++s) { lead[s] = R(1); trail[s] = R(1); }
+    int32_t* lo = sc ? sc->lo : B.qlo + o;
+    int32_t* hi = sc ? sc->hi : B.qhi + o;
+    Rat* lead = sc ? sc->lead : B.qlead + o;
+    Rat* trail = sc ? sc->trail : B.qtrail + o;
+    for (int s = 0; s < Q.N; ++s) {
+        lead[s] = R(1);
+        trail[s] = R(1);
+        if (sc) { lo[s] = B.qlo[o + s]; hi[s] = B.qhi[o + s]; }
+    }
     Err e{ERR_NONE};
     int64_t rs[4];
-    refine(v, c, lo, hi, lead, trail, B.qF + o, B.qB + o, B.qT + o, B.qdirty + o, rs, e);
+    if (sc) refine(v, c, lo, hi, lead, trail, sc->tF, sc->tB, sc->tT, sc->dirty, rs, e);
+    else refine(v, c, lo, hi, lead, trail, B.qF + o, B.qB + o, B.qT + o, B.qdirty + o, rs, e);
+    if (sc) {
+        for (int s = 0; s < Q.N; ++s) {
+            B.qlo[o + s] = lo[s];
+            B.qhi[o + s] = hi[s];
+            B.qlead[o + s] = lead[s];
+            B.qtrail[o + s] = trail[s];
+        }
+    }
     qs.refined = 1;
     qs.refine_iters = rs[0];
     qs.refine_evals = rs[1];
@@ -177,6 +205,8 @@ BPK_HDNI void refine_query(const BatchDev& B, int qi) {
     qs.vaux = aux;
 }
 
+BPK_HDNI void refine_query(const BatchDev& B, int qi) { refine_query_at(B, qi, nullptr); }
+
 // ---------------------------------------------------------------- K3b
 BPK_HD EstScratch cand_scratch(const BatchDev& B, int64_t slot) {
     EstScratch s;
@@ -191,7 +221,10 @@ BPK_HD EstScratch cand_scratch(const BatchDev& B, int64_t slot) {
 
 BPK_HD void fail(bp_candidate& cd, const Err& e) { cd.status = status_of_err(e.code); }
 
-BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci) {
+// pass: -1 = every candidate; 0 = candidates that do not use the refined plan
+// (N = 1, InfeasibleShape, comm-bottleneck M slots: they can run while refine
+// is still going); 1 = the refined-plan candidates.
+BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci, int pass = -1) {
     bp_candidate& cd = B.cand[ci];
     if (cd.status != C_PENDING) return;
     const int qi = B.cq[ci];
@@ -200,6 +233,10 @@ BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci) {
     const int64_t local = ci - Q.cand_off;
     const int m = (int)(local % Q.nbase);
     const int N = Q.N;
+    if (pass >= 0) {
+        const bool refined_path = N > 1 && !qs.dp_shape && !B.ms[Q.mslot_off + m].bott;
+        if (refined_path != (pass == 1)) return;
+    }
     const int kind = cd.kind;
     const int64_t M = cd.M, micro = cd.micro;
     NetView v = net_view(B.P, Q.net);
