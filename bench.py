@@ -127,14 +127,28 @@ OPS_PER_EVENT = 3              # simulator: max, add, store-forward (SURVEY.md 8
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")
 
 
-def kernel_work_ops(name, work):
-    """Algorithmic lane-ops of one launch of `name` from its work counter, or
-    None for kernels without a closed-form count (refine, prune, ...)."""
-    if name.startswith("minmax_dp"):
-        return work * OPS_PER_TRANSITION
+OPS_PER_REFINE_STEP = 3        # refine boundary step: compare t_a/t_b, t_hi - t_lo, / (c_from + c_to)
+OPS_PER_PRUNE_STAGE = 4        # estimate per stage: F+B, features + 2w, capacity test, link demand
+
+WORK_UNITS = {"minmax_dp": ("DP transitions", OPS_PER_TRANSITION),
+              "minmax_dp_coarse": ("DP transitions", OPS_PER_TRANSITION),
+              "refine": ("refine boundary steps", OPS_PER_REFINE_STEP),
+              "prune": ("candidate-stages estimated", OPS_PER_PRUNE_STAGE)}
+
+
+def work_unit(name):
+    if name in WORK_UNITS:
+        return WORK_UNITS[name]
     if name.startswith("sim_"):
-        return work * OPS_PER_EVENT
+        return ("simulated events", OPS_PER_EVENT)
     return None
+
+
+def kernel_work_ops(name, work):
+    """Algorithmic lane-ops of one launch of `name` from its work counter
+    (Rooflines), or None for kernels without a work count."""
+    u = work_unit(name)
+    return None if u is None else work * u[1]
 
 
 def rooflines(stats, steps, clocks, problem, step_ms):
@@ -164,13 +178,12 @@ def rooflines(stats, steps, clocks, problem, step_ms):
         kern[k] = e
     dom = max(stats, key=lambda k: stats[k]["ms"])
     d = kern[dom]
-    units = {"minmax_dp": "DP transitions", "minmax_dp_coarse": "DP transitions"}.get(dom, "simulated events")
+    u = work_unit(dom)
     roof = {"kernel": dom, "bound": "issue", "unit": "Gop/s", "peak": issue_peak,
             "achieved": d.get("achieved_gops"), "frac": d.get("frac"),
             "traffic": traffic.get(dom),
-            "work": (f"{d['work_per_launch']:.4g} {units}/launch x "
-                     f"{OPS_PER_TRANSITION if dom.startswith('minmax_dp') else OPS_PER_EVENT} ops"
-                     if d.get("achieved_gops") is not None else f"{dom}: no closed-form work count"),
+            "work": (f"{d['work_per_launch']:.4g} {u[0]}/launch x {u[1]} ops" if u and d.get("achieved_gops")
+                     is not None else f"{dom}: no work count"),
             "peak_source": f"{SMS} SMs x {LANES} lanes x {f_max / 1e6:.0f} MHz (sm_max_mhz, {peak_kind} "
                            f"MEASURED_PEAKS.json); HBM {peaks.get('hbm_gbs')} GB/s"}
     # sweep bound: t_roof = sum B_cost / BW + (X_dp * c_dp + X_sim * c_sim) / issue
@@ -308,6 +321,28 @@ def run_b200(args):
     cands_per_step = p.total_candidates * world
     value = cands_per_step * args.steps / (total_ms / 1e3)
 
+    # ---- the same steps with the batch dedup off (BP_OPT_DEDUP = 0: every
+    # query and candidate solved on its own; identical results)
+    ex.dedup(False)
+    with torch.cuda.stream(stream):
+        ex.run(batch, stream=sp)
+    nd_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.zero_()
+            nd_evs[i][0].record(stream)
+            ex.run(batch, stream=sp)
+            nd_evs[i][1].record(stream)
+    barrier()
+    ex.dedup(True)
+    nd_ms = sum(a.elapsed_time(b) for a, b in nd_evs)
+    if world > 1:
+        t = torch.tensor([nd_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        nd_ms = float(t.item())
+    value_nodedup = cands_per_step * args.steps / (nd_ms / 1e3)
+
     # ---- global best: per-rank record -> one allgather -> deterministic argmin
     rec = torch.zeros(BEST_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
     ex.best(batch, rec.data_ptr(), query_base=rank * p.queries.size, stream=sp)
@@ -369,6 +404,8 @@ def run_b200(args):
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_total / args.steps,
                     "h2d_bytes_per_step": (h2 - h1) // args.steps, "d2h_bytes_per_step": (d2 - d1) // args.steps},
+            "no_dedup": {"value": value_nodedup, "unit": UNIT, "ms_per_step": nd_ms / args.steps,
+                         "note": "same steps with BP_OPT_DEDUP=0: identical subproblems of the batch not shared"},
             "gpu_launches": launches,
             "clocks": clocks,
             "roofline": roof,

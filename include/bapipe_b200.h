@@ -240,6 +240,15 @@ void bp_batch_free(bp_ctx* ctx, bp_batch* b);
  * device time (CUDA events on the launching stream) when enabled. */
 int64_t bp_launch_count(const bp_ctx* ctx);
 int bp_set_profiling(bp_ctx* ctx, int enable);
+
+/* Engine options (results never depend on them).
+ *   BP_OPT_DEDUP (default 1): solve identical subproblems of a batch once --
+ *   the whole-layer DP and refine per (network, stage count, type chain), the
+ *   comm-coarsened DP per (that, a_th), simulations per identical inputs --
+ *   and share the results; 0 evaluates every query and candidate
+ *   independently. */
+enum { BP_OPT_DEDUP = 1 };
+int bp_set_option(bp_ctx* ctx, int option, int64_t value);
 /* Copies up to cap entries: names (NUL-separated, 48 bytes each), total ms,
  * launch counts and algorithmic work units.  Returns the entry count. */
 int bp_kernel_stats(const bp_ctx* ctx, char* names48, double* ms, int64_t* launches,

@@ -94,8 +94,9 @@ PRODUCT_SYMBOLS = (
     "bp_create", "bp_destroy", "bp_last_error", "bp_abi_version", "bp_set_networks",
     "bp_set_clusters", "bp_layout", "bp_explore_batch", "bp_batch_prepare", "bp_batch_run",
     "bp_batch_fetch", "bp_batch_best", "bp_batch_free", "bp_launch_count", "bp_set_profiling",
-    "bp_kernel_stats", "bp_transfer_stats", "bp_best_less",
+    "bp_kernel_stats", "bp_transfer_stats", "bp_best_less", "bp_set_option",
 )
+BP_OPT_DEDUP = 1
 
 
 def _sig(lib, name, res, args):
@@ -125,6 +126,7 @@ def bind_product(lib: C.CDLL) -> C.CDLL:
     _sig(lib, "bp_batch_free", None, [vp, vp])
     _sig(lib, "bp_launch_count", C.c_int64, [vp])
     _sig(lib, "bp_set_profiling", C.c_int, [vp, C.c_int])
+    _sig(lib, "bp_set_option", C.c_int, [vp, C.c_int, C.c_int64])
     _sig(lib, "bp_kernel_stats", C.c_int,
          [vp, C.c_char_p, C.POINTER(C.c_double), P64, C.POINTER(C.c_double), C.c_int])
     _sig(lib, "bp_transfer_stats", C.c_int, [vp, P64, P64])

@@ -103,6 +103,7 @@ struct bp_ctx {
     Pools P{};
     int max_T = 1;
     bool prof = false;
+    bool dedup = true;       // BP_OPT_DEDUP
     std::map<std::string, KStat> stats;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -403,6 +404,7 @@ int upload_inputs(bp_ctx* c, bp_batch* B, cudaStream_t st) {
 int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     BatchDev& D = B->dev;
     const HostBatch& hb = B->hb;
+    D.dedup = c->dedup ? 1 : 0;
     cudaError_t e;
     e = cudaMemsetAsync(D.cand, 0, (size_t)hb.ncand * sizeof(bp_candidate), st);
     if (e == cudaSuccess && D.stages) e = cudaMemsetAsync(D.stages, 0, (size_t)hb.nstage * sizeof(bp_stage), st);
@@ -478,6 +480,8 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
         if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess) {
             c->stats["minmax_dp"].work = (double)work[WORK_DP_WHOLE];
             c->stats["minmax_dp_coarse"].work = (double)work[WORK_DP_COARSE];
+            c->stats["refine"].work = (double)work[WORK_REFINE];
+            c->stats["prune"].work = (double)work[WORK_PRUNE];
             for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work = (double)work[WORK_SIM_EVENTS + k];
         }
         collect(c);
@@ -658,6 +662,14 @@ int bp_set_profiling(bp_ctx* c, int enable) {
     c->prof = enable != 0;
     if (enable) c->stats.clear();
     return BP_OK;
+}
+
+int bp_set_option(bp_ctx* c, int option, int64_t value) {
+    if (!c) return BP_BAD_INPUT;
+    switch (option) {
+        case BP_OPT_DEDUP: c->dedup = value != 0; return BP_OK;
+        default: return fail(c, BP_BAD_INPUT, "unknown option " + std::to_string(option));
+    }
 }
 
 int bp_kernel_stats(const bp_ctx* c, char* names48, double* ms, int64_t* launches, double* work, int cap) {

@@ -64,7 +64,9 @@ enum { SIM_CLASSES = 11, SIM_EXACT = 8, SIM_FLOW = 9, SIM_FLOW_CLASSES = 2 };
 // the dataflow kernel: their serial walk would otherwise set the kernel time
 constexpr int64_t FLOW_MIN_EVENTS = 1024;
 // instrumentation slots of BatchDev::work (algorithmic work of one run)
-enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_SIM_EVENTS = 2, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
+// refine: boundary steps evaluated; prune: candidate-stages estimated
+enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_REFINE = 2, WORK_PRUNE = 3, WORK_SIM_EVENTS = 4,
+       WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
 enum { XBUCKETS = 32768, XSIM_WARPS_PER_SM = 32 };
 
 // Per-candidate device state (beyond the bp_candidate output record).
@@ -130,6 +132,7 @@ struct BatchDev {
     unsigned long long* ckey; // [cmask+1] coarse-DP (class, a_th) hashes
     int32_t* crep;            // [cmask+1] smallest mslot index per hash
     int32_t cmask;
+    int32_t dedup;            // BP_OPT_DEDUP: share identical subproblems
     int32_t* rlist;           // [nq] queries to refine this run (compacted)
     int32_t* rcount;          // [1]
     int details;              // write bp_stage records

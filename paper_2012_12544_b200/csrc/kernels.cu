@@ -146,7 +146,7 @@ __global__ void k_coarse_queue(BatchDev B) {
         uint32_t slot = (uint32_t)(h ^ (h >> 32)) & (uint32_t)B.cmask;
         while (B.ckey[slot] != h) slot = (slot + 1) & (uint32_t)B.cmask;
         const int32_t r = B.crep[slot], id = (int32_t)(Q.mslot_off + m);
-        if (r != id && B.qrep[B.ms[r].q] == B.qrep[qi] && B.ms[r].a_th == ms.a_th) {
+        if (B.dedup && r != id && B.qrep[B.ms[r].q] == B.qrep[qi] && B.ms[r].a_th == ms.a_th) {
             ms.crep = r;
         } else {
             int idx = atomicAdd(&B.dp_count[1], 1);
@@ -229,7 +229,7 @@ __global__ void k_dedup_resolve(BatchDev B) {
     int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi >= B.nq) return;
     int rep = qi;
-    if (B.q[qi].schema_ok) {
+    if (B.dedup && B.q[qi].schema_ok) {
         const uint64_t h = class_hash(B, qi);
         uint32_t slot = class_slot(B, h);
         while (B.dkey[slot] != h) slot = (slot + 1) & (uint32_t)B.dmask;
@@ -294,7 +294,10 @@ __global__ void k_dedup_copy_refine(BatchDev B) {
 // (host_prep.hpp) so that the lanes of a warp run similar work.
 __global__ void k_refine(BatchDev B) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < B.nq) refine_query(B, B.qorder[i]);
+    if (i >= B.nq) return;
+    const int qi = B.qorder[i];
+    refine_query(B, qi);
+    if (B.qs[qi].refined) atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
 }
 
 // intra_layer_refine is a long serial walk per query (up to ~3000 boundary
@@ -326,12 +329,20 @@ __global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm) {
     sc.hi = sc.lo + nm;
     sc.dirty = reinterpret_cast<uint8_t*>(sc.hi + nm);
     const int count = *B.rcount;
-    for (int i = blockIdx.x; i < count; i += gridDim.x) refine_query_at(B, B.rlist[i], &sc);
+    for (int i = blockIdx.x; i < count; i += gridDim.x) {
+        const int qi = B.rlist[i];
+        refine_query_at(B, qi, &sc);
+        atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
+    }
 }
 
 __global__ void k_prune(BatchDev B, int pass) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < B.ncand) prune_candidate(B, B.cperm[i], pass);
+    if (i >= B.ncand) return;
+    const int64_t ci = B.cperm[i];
+    const bool pending = B.cand[ci].status == C_PENDING;
+    prune_candidate(B, ci, pass);
+    if (pending && B.cand[ci].status != C_PENDING) atomicAdd(&B.work[WORK_PRUNE], (unsigned long long)B.cand[ci].n_stages);
 }
 
 __global__ void k_rank(BatchDev B) {
@@ -401,7 +412,7 @@ void launch_dedup(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.dkey, 0, ((size_t)B.dmask + 1) * sizeof(unsigned long long), st);
     cudaMemsetAsync(B.drep, 0x7f, ((size_t)B.dmask + 1) * sizeof(int32_t), st);
     if (B.nq) {
-        k_dedup_insert<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+        if (B.dedup) k_dedup_insert<<<blocks(B.nq, 128), 128, 0, st>>>(B);
         k_dedup_resolve<<<blocks(B.nq, 128), 128, 0, st>>>(B);
     }
 }
@@ -432,7 +443,9 @@ size_t refine_region_bytes(int max_N) {
 void launch_refine(const BatchDev& B, int sms, cudaStream_t st) {
     if (!B.nq) return;
     const size_t bytes = refine_region_bytes(B.max_N);
-    if (bytes > 200 * 1024) {   // very long chains: global-memory version
+    // very long chains, or no dedup (tens of thousands of queries to refine:
+    // the packed global-memory version keeps more of them in flight)
+    if (bytes > 200 * 1024 || !B.dedup) {
         k_refine<<<blocks(B.nq, 64), 64, 0, st>>>(B);
         return;
     }

@@ -131,7 +131,7 @@ __global__ void k_sim_prep(BatchDev B) {
             uint32_t slot = sim_slot(B, h);
             while (B.skey[slot] != h) slot = (slot + 1) & (uint32_t)B.smask;
             const int32_t r = B.srep[slot];
-            if (r != ci && same_sim(B, ci, r)) {
+            if (B.dedup && r != ci && same_sim(B, ci, r)) {
                 B.cs[ci].sim_rep = r;
                 cls = -1;
             }

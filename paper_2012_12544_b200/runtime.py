@@ -97,6 +97,13 @@ class Explorer:
     def profiling(self, on=True):
         self.lib.bp_set_profiling(self.ctx, 1 if on else 0)
 
+    def dedup(self, on=True):
+        """BP_OPT_DEDUP: share identical subproblems within a batch (default
+        on; results are identical either way)."""
+        rc = self.lib.bp_set_option(self.ctx, abi.BP_OPT_DEDUP, 1 if on else 0)
+        if rc != 0:
+            raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
+
     def kernel_stats(self):
         cap = 64
         names = C.create_string_buffer(48 * cap)

@@ -91,6 +91,24 @@ def test_full_c5_sweep_properties(ex, c5):
     ex.free(b)
 
 
+def test_dedup_off_is_identical(ex, c5):
+    """BP_OPT_DEDUP only shares work: with it off every query / candidate is
+    evaluated on its own and every output byte is the same (full sweep:
+    per-query records; a sample: candidate and stage records too)."""
+    p, res = c5
+    s = scenarios.c5_sample(61)
+    on = ex.explore(s, details=True)
+    ex.dedup(False)
+    try:
+        off_full, _, _ = ex.explore(p, details=False)
+        off = ex.explore(s, details=True)
+    finally:
+        ex.dedup(True)
+    assert res.tobytes() == off_full.tobytes()
+    for x, y, part in zip(on, off, ("res", "cand", "stages")):
+        assert_same(x, y, "dedup on/off " + part)
+
+
 def test_ranked_lists_sorted_on_c5_sample(ex):
     from fractions import Fraction as Fr
     p = scenarios.c5_sample(257)
