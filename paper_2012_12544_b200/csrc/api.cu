@@ -304,6 +304,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     while (stab < 2 * std::max<int64_t>(1, hb.ncand)) stab <<= 1;
     size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
     size_t o_rlist = L.take<int32_t>(nqs), o_rcount = L.take<int32_t>(1);
+    size_t o_pkey = L.take<unsigned long long>((size_t)stab), o_pbest = L.take<unsigned long long>((size_t)stab);
     int32_t ctab = 1;
     while (ctab < 2 * std::max<int64_t>(1, (int64_t)nms)) ctab <<= 1;
     size_t o_ckey = L.take<unsigned long long>((size_t)ctab), o_crep = L.take<int32_t>((size_t)ctab);
@@ -377,6 +378,9 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.cmask = ctab - 1;
     D.rlist = dptr<int32_t>(b, o_rlist);
     D.rcount = dptr<int32_t>(b, o_rcount);
+    D.pkey = dptr<unsigned long long>(b, o_pkey);
+    D.pbest = dptr<unsigned long long>(b, o_pbest);
+    D.pmask = stab - 1;
     D.qorder = dptr<int32_t>(b, o_qord);
     D.cperm = dptr<int32_t>(b, o_cperm);
     D.sim_list = dptr<int32_t>(b, o_slist);
@@ -442,14 +446,21 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     cudaStreamWaitEvent(st, c->join, 0);
     // (pruning the coarse-plan candidates on the side stream during refine was
     // measured slower: it takes issue slots from refine's single-lane warps)
-    timed(c, "prune", st, [&] { launch_prune(D, -1, st); });
+    timed(c, "prune", st, [&] { launch_prune(D, -1, st); }, 3);
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
+    // the simulator classes are independent: the two exact ones on the side
+    // stream overlap the fast classes and the N <= 32 dataflow kernel, so
+    // their latency tails overlap instead of adding up
+    cudaEventRecord(c->fork, st);
+    cudaStreamWaitEvent(c->side, c->fork, 0);
+    timed(c, "sim_flow64", c->side, [&] { launch_sim_flow(D, 1, c->sm_count, c->side); });
+    timed(c, "sim_exact", c->side, [&] { launch_sim_exact(D, c->sm_count, c->side); }, 4);
+    cudaEventRecord(c->join, c->side);
     for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
     timed(c, "sim_flow32", st, [&] { launch_sim_flow(D, 0, c->sm_count, st); });
-    timed(c, "sim_flow64", st, [&] { launch_sim_flow(D, 1, c->sm_count, st); });
-    timed(c, "sim_exact", st, [&] { launch_sim_exact(D, c->sm_count, st); }, 4);
+    cudaStreamWaitEvent(st, c->join, 0);
     timed(c, "sim_share", st, [&] { launch_sim_share(D, st); });
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();

@@ -76,6 +76,8 @@ struct CState {
     int64_t D;             // simulator scale for this candidate's plan
     int32_t sim_cls;       // simulator class, -1 = not simulated
     int32_t sim_rep;       // candidate whose identical simulation this one shares, -1 = none
+    int32_t pshare;        // prune: first estimate may be shared (see k_prune_key)
+    int32_t est_first;     // prune: 1 = first estimate feasible, 2 = it raised (shareable outcomes)
 };
 
 // DP work item: a (query, a_th) pair; a_th < 0 = whole-layer partition.
@@ -135,6 +137,9 @@ struct BatchDev {
     int32_t dedup;            // BP_OPT_DEDUP: share identical subproblems
     int32_t* rlist;           // [nq] queries to refine this run (compacted)
     int32_t* rcount;          // [1]
+    unsigned long long* pkey; // [pmask+1] estimate-input hashes (prune dedup)
+    unsigned long long* pbest;// [pmask+1] max (capacity score, -index) per hash
+    int32_t pmask;
     int details;              // write bp_stage records
     // DP work lists
     DPItem* dp_items;

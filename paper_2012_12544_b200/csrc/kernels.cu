@@ -336,13 +336,173 @@ __global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm) {
     }
 }
 
+// ---- batch-level sharing of the first estimate (cost_models.hpp:124-166).
+// balance_partition's first estimate is a function of the plan (the class's
+// refined plan, or its coarse plan for a_th), kind, M, micro and the link
+// bandwidths; capacities only decide feasibility.  Candidates whose inputs
+// coincide (cluster mixes differing only in memory) share it: the member with
+// the largest capacities evaluates it; if it was feasible there, the others
+// copy its values and test their own capacities, and run the full prune
+// themselves when it is not feasible for them (memory fine-tune is
+// capacity-dependent).  An estimate that raises raises for all of them.
+__device__ bool est_key_of(const BatchDev& B, int64_t ci, uint64_t& h, int32_t& coarse) {
+    const bp_candidate& cd = B.cand[ci];
+    if (!B.dedup || cd.status != C_PENDING) return false;
+    const int qi = B.cq[ci];
+    const QDesc Q = B.q[qi];
+    if (Q.N < 2 || B.qs[qi].dp_shape) return false;
+    const int m = (int)((ci - Q.cand_off) % Q.nbase);
+    const MState& ms = B.ms[Q.mslot_off + m];
+    if (ms.bott) {
+        if (ms.err || ms.K < Q.N) return false;
+        coarse = ms.crep >= 0 ? ms.crep : (int32_t)(Q.mslot_off + m);
+    } else {
+        if (B.qs[qi].refine_err) return false;
+        coarse = -1;
+    }
+    const ChainView c = chain_view(B.P, Q.cl, Q.N);
+    h = 0xcbf29ce484222325ull;
+    auto mix = [&](uint64_t x) { h ^= x; h *= 0x100000001b3ull; h ^= h >> 29; };
+    mix((uint64_t)(uint32_t)B.qrep[qi]);
+    mix((uint64_t)(uint32_t)coarse);
+    mix((uint64_t)cd.kind);
+    mix((uint64_t)cd.M);
+    mix((uint64_t)cd.micro);
+    for (int k = 0; k + 1 < Q.N; ++k) mix((uint64_t)c.bw[k]);
+    if (!h) h = 1;
+    return true;
+}
+
+__device__ bool same_est(const BatchDev& B, int64_t a, int64_t b, int32_t ca, int32_t cb) {
+    const bp_candidate &x = B.cand[a], &y = B.cand[b];
+    const int qa = B.cq[a], qb = B.cq[b];
+    if (B.qrep[qa] != B.qrep[qb] || ca != cb || x.kind != y.kind || x.M != y.M || x.micro != y.micro) return false;
+    const QDesc A = B.q[qa], Q = B.q[qb];
+    const ChainView xa = chain_view(B.P, A.cl, A.N), xb = chain_view(B.P, Q.cl, Q.N);
+    for (int k = 0; k + 1 < A.N; ++k)
+        if (xa.bw[k] != xb.bw[k]) return false;
+    return true;
+}
+
+__device__ __forceinline__ uint32_t est_slot(const BatchDev& B, uint64_t h) {
+    return (uint32_t)(h ^ (h >> 32)) & (uint32_t)B.pmask;
+}
+
+// packed (capacity score, -index): the largest wins, ties to the smallest index
+__device__ uint64_t est_score(const BatchDev& B, int64_t ci) {
+    const QDesc Q = B.q[B.cq[ci]];
+    const ChainView c = chain_view(B.P, Q.cl, Q.N);
+    int64_t mn = INT64_MAX;
+    for (int s = 0; s < Q.N; ++s) mn = c.cap[s] < mn ? c.cap[s] : mn;
+    uint64_t capk = (uint64_t)mn >> 20;
+    if (capk > ((1ull << 41) - 1)) capk = (1ull << 41) - 1;
+    return (capk << 22) | (uint64_t)((1u << 22) - 1 - (uint32_t)(ci & ((1 << 22) - 1)));
+}
+
+__device__ int64_t est_rep(const BatchDev& B, uint64_t h) {
+    uint32_t slot = est_slot(B, h);
+    for (uint32_t n = 0; B.pkey[slot] != h; slot = (slot + 1) & (uint32_t)B.pmask)
+        if (++n > (uint32_t)B.pmask) __trap();   // key never inserted: a bug, fail loudly
+    return (int64_t)((1u << 22) - 1) - (int64_t)(B.pbest[slot] & ((1ull << 22) - 1));
+}
+
+__global__ void k_prune_key(BatchDev B) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= B.ncand) return;
+    uint64_t h;
+    int32_t coarse;
+    const bool ok = est_key_of(B, ci, h, coarse);
+    B.cs[ci].pshare = ok ? 1 : 0;
+    B.cs[ci].est_first = 0;
+    if (!ok) return;
+    const uint64_t sc = est_score(B, ci);
+    for (uint32_t slot = est_slot(B, h);; slot = (slot + 1) & (uint32_t)B.pmask) {
+        const unsigned long long prev = atomicCAS(&B.pkey[slot], 0ull, (unsigned long long)h);
+        if (prev == 0ull || prev == h) {
+            atomicMax(&B.pbest[slot], (unsigned long long)sc);
+            return;
+        }
+    }
+}
+
+__device__ __forceinline__ void count_prune(const BatchDev& B, int64_t ci) {
+    atomicAdd(&B.work[WORK_PRUNE], (unsigned long long)B.cand[ci].n_stages);
+}
+
+// representatives and unshareable candidates
 __global__ void k_prune(BatchDev B, int pass) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B.ncand) return;
     const int64_t ci = B.cperm[i];
-    const bool pending = B.cand[ci].status == C_PENDING;
+    if (B.cand[ci].status != C_PENDING) return;
+    if (B.cs[ci].pshare) {
+        uint64_t h;
+        int32_t coarse;
+        if (est_key_of(B, ci, h, coarse) && est_rep(B, h) != ci) return;   // deferred to k_prune_members
+    }
     prune_candidate(B, ci, pass);
-    if (pending && B.cand[ci].status != C_PENDING) atomicAdd(&B.work[WORK_PRUNE], (unsigned long long)B.cand[ci].n_stages);
+    count_prune(B, ci);
+}
+
+__global__ void k_prune_members(BatchDev B) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= B.ncand) return;
+    const int64_t ci = B.cperm[i];
+    if (!B.cs[ci].pshare) return;
+    uint64_t h;
+    int32_t coarse;
+    // representatives were pruned by k_prune: their status is no longer pending
+    if (!est_key_of(B, ci, h, coarse)) return;
+    const int64_t r = est_rep(B, h);
+    if (r == ci) return;
+    int32_t rc = -1;
+    {
+        const int qr = B.cq[r];
+        const QDesc Qr = B.q[qr];
+        const int mr = (int)((r - Qr.cand_off) % Qr.nbase);
+        const MState& msr = B.ms[Qr.mslot_off + mr];
+        rc = msr.bott ? (msr.crep >= 0 ? msr.crep : (int32_t)(Qr.mslot_off + mr)) : -1;
+    }
+    const int ef = B.cs[r].est_first;
+    if (ef != 0 && same_est(B, ci, r, coarse, rc)) {
+        bp_candidate& cd = B.cand[ci];
+        const bp_candidate& rd = B.cand[r];
+        if (ef == 2) {   // the estimate itself raised
+            cd.status = rd.status;
+            return;
+        }
+        // copy the estimate and test this candidate's own capacities
+        const QDesc Q = B.q[B.cq[ci]], Qr = B.q[B.cq[r]];
+        const int N = Q.N;
+        const int64_t so = Q.stage_off + (ci - Q.cand_off) * N, sr = Qr.stage_off + (r - Qr.cand_off) * N;
+        const ChainView c = chain_view(B.P, Q.cl, N);
+        bool feasible = true;
+        for (int s = 0; s < N; ++s)
+            if (rat_gt(B.sMem[sr + s], R(c.cap[s]))) feasible = false;
+        if (feasible) {
+            for (int s = 0; s < N; ++s) {
+                B.sF[so + s] = B.sF[sr + s];
+                B.sB[so + s] = B.sB[sr + s];
+                B.sW[so + s] = B.sW[sr + s];
+                B.sMem[so + s] = B.sMem[sr + s];
+                B.sA[so + s] = B.sA[sr + s];
+                B.sSR[so + s] = B.sSR[sr + s];
+                if (B.details) B.stages[so + s] = B.stages[sr + s];
+            }
+            cd.est_minibatch = rd.est_minibatch;
+            cd.bubble = rd.bubble;
+            cd.heuristic = rd.heuristic;
+            cd.peak_memory = rd.peak_memory;
+            cd.max_bw_demand = rd.max_bw_demand;
+            cd.plan_fractional = rd.plan_fractional;
+            B.cs[ci].plan_kind = B.cs[r].plan_kind;
+            B.cs[ci].est_first = 1;
+            B.cs[ci].sim_ready = 1;
+            return;
+        }
+    }
+    prune_candidate(B, ci);
+    count_prune(B, ci);
 }
 
 __global__ void k_rank(BatchDev B) {
@@ -459,7 +619,12 @@ void launch_refine(const BatchDev& B, int sms, cudaStream_t st) {
     k_refine_smem<<<sms * 32, 32, bytes, st>>>(B, B.max_N);
 }
 void launch_prune(const BatchDev& B, int pass, cudaStream_t st) {
-    if (B.ncand) k_prune<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
+    if (!B.ncand) return;
+    cudaMemsetAsync(B.pkey, 0, ((size_t)B.pmask + 1) * sizeof(unsigned long long), st);
+    cudaMemsetAsync(B.pbest, 0, ((size_t)B.pmask + 1) * sizeof(unsigned long long), st);
+    k_prune_key<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
+    k_prune<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
+    k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
 }
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);

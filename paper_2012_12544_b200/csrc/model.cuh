@@ -373,16 +373,22 @@ BPK_HD Rat reduce_pos(i128 n, i128 d) {       // n >= 0, d > 0, both < 2^62
     return Rat{(int64_t)udiv_exact64((uint64_t)n, g), (int64_t)udiv_exact64((uint64_t)d, g)};
 }
 
+// Every product below is formed from two int64 factors already checked
+// against 2^62 (64x64 -> 128-bit multiplies only: a 128x128 product is ~60
+// instructions and this step runs millions of times).
 BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh, Rat& nl) {
     const i128 B62 = (i128)1 << 62;
     if (t_hi.n < 0 || t_lo.n < 0 || avail.n <= 0) return FS_FALLBACK;
     const uint64_t g = gcd_u64((uint64_t)t_hi.d, (uint64_t)t_lo.d);
     const int64_t mh = (int64_t)udiv_exact64((uint64_t)t_lo.d, g), ml = (int64_t)udiv_exact64((uint64_t)t_hi.d, g);
-    const i128 D = (i128)t_hi.d * mh;
+    const i128 D128 = (i128)t_hi.d * mh;
+    if (D128 >= B62) return FS_FALLBACK;
+    const int64_t D = (int64_t)D128;
     const int64_t cs = c_from + c_to;
-    if (D * cs >= B62 || D * 1024 >= B62) return FS_FALLBACK;
-    const i128 Th = (i128)t_hi.n * mh, Tl = (i128)t_lo.n * ml;
-    if (Th >= B62 || Tl >= B62) return FS_FALLBACK;
+    if ((i128)D * cs >= B62 || (i128)D * 1024 >= B62) return FS_FALLBACK;
+    const i128 Th128 = (i128)t_hi.n * mh, Tl128 = (i128)t_lo.n * ml;
+    if (Th128 >= B62 || Tl128 >= B62) return FS_FALLBACK;
+    const int64_t Th = (int64_t)Th128, Tl = (int64_t)Tl128;
     // x = (t_hi - t_lo) / (c_from + c_to), reduced
     x = reduce_pos(Th - Tl, D * cs);
     if (!rat_lt(x, avail)) {
@@ -403,8 +409,10 @@ BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, 
             x = qlo;
         } else {
             // score(f) = max(t_hi - f*c_from, t_lo + f*c_to), all scaled by D*1024
-            const i128 a1 = Th * 1024 - (i128)k * c_from * D, a2 = Tl * 1024 + (i128)k * c_to * D;
-            const i128 b1 = Th * 1024 - (i128)kc * c_from * D, b2 = Tl * 1024 + (i128)kc * c_to * D;
+            const i128 kf = (i128)k * c_from, kt = (i128)k * c_to, kcf = (i128)kc * c_from, kct = (i128)kc * c_to;
+            if (kf >= B62 || kt >= B62 || kcf >= B62 || kct >= B62) return FS_FALLBACK;
+            const i128 a1 = (i128)Th * 1024 - (i128)(int64_t)kf * D, a2 = (i128)Tl * 1024 + (i128)(int64_t)kt * D;
+            const i128 b1 = (i128)Th * 1024 - (i128)(int64_t)kcf * D, b2 = (i128)Tl * 1024 + (i128)(int64_t)kct * D;
             if (a1 >= B62 || a2 >= B62 || b1 >= B62 || b2 >= B62 || a1 <= -B62 || b1 <= -B62) return FS_FALLBACK;
             const i128 s_lo = a1 > a2 ? a1 : a2, s_hi = b1 > b2 ? b1 : b2;
             x = s_lo <= s_hi ? qlo : qhi;
@@ -412,9 +420,10 @@ BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, 
     }
     if (x.n <= 0 || !rat_lt(x, avail)) return FS_NOMOVE;
     // acceptance: max(t_hi - x*c_from, t_lo + x*c_to) < t_hi, scaled by D*den(x)
-    const i128 Dx = D * x.d;
-    if (Dx >= B62 || (i128)x.n * c_from >= B62 || (i128)x.n * c_to >= B62) return FS_FALLBACK;
-    const i128 TH = Th * x.d, NH = TH - (i128)x.n * c_from * D, NL = Tl * x.d + (i128)x.n * c_to * D;
+    const i128 Dx = (i128)D * x.d;
+    const i128 xf = (i128)x.n * c_from, xt = (i128)x.n * c_to;
+    if (Dx >= B62 || xf >= B62 || xt >= B62) return FS_FALLBACK;
+    const i128 TH = (i128)Th * x.d, NH = TH - (i128)(int64_t)xf * D, NL = (i128)Tl * x.d + (i128)(int64_t)xt * D;
     if (TH >= B62 || NL >= B62 || NH <= -B62) return FS_FALLBACK;
     if ((NH > NL ? NH : NL) >= TH) return FS_NOMOVE;
     if (NH < 0) return FS_FALLBACK;

@@ -267,12 +267,14 @@ BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci, int pass = -1) {
             if (ms.K < N) { cd.status = BP_C_REJ_COARSEN; cd.detail = ms.K; return; }
             WholePlan wp{&v, &c, lo, hi};
             estimate(wp, v, c, kind, M, micro, S, o, nullptr, e);
+            cs.est_first = e.bad() ? 2 : o.feasible ? 1 : 0;
             if (!e.bad()) ft = memory_fine_tune(v, c, kind, M, micro, lo, hi, nullptr, nullptr, S, o, e);
         } else {                                                   // 469-473
             if (qs.refine_err) { cd.status = status_of_err(qs.refine_err); return; }
             const int64_t qo = Q.qstage_off;
             CachedPlan cp{B.qhi + qo, B.qF + qo, B.qB + qo, B.qW + qo};
             estimate(cp, v, c, kind, M, micro, S, o, nullptr, e);
+            cs.est_first = e.bad() ? 2 : o.feasible ? 1 : 0;
             if (!e.bad() && !o.feasible) {
                 for (int s = 0; s < N; ++s) { lo[s] = B.qlo[qo + s]; hi[s] = B.qhi[qo + s]; }
                 ft = memory_fine_tune(v, c, kind, M, micro, lo, hi, B.qlead + qo, B.qtrail + qo, S, o, e);
