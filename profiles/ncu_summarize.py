@@ -19,6 +19,7 @@ writes
                                names; bench.py reports it as roofline.traffic
 """
 import csv
+import re
 import json
 import os
 import subprocess
@@ -30,7 +31,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # CUDA kernel -> bench.py / bp_kernel_stats name.  k_partition runs twice per
 # step: the whole-layer DP first, then the coarse DPs.
 def bench_name(kernel, seen):
-    k = kernel.split("(")[0].replace("bpk::", "").replace("void ", "")
+    k = kernel.split("(")[0].replace("void ", "")
+    k = re.sub(r"^.*::", "", k.split("<")[0]) + (k[k.index("<"):] if "<" in k else "")
     if k.startswith("k_partition"):
         n = seen.get("k_partition", 0)
         seen["k_partition"] = n + 1
@@ -38,9 +40,17 @@ def bench_name(kernel, seen):
     if k.startswith("k_sim_fast"):
         g = k.split("<")[1].rstrip(">").replace(" ", "").split(",")
         return f"sim_fast_g{g[0]}" + (f"s{g[1]}" if g[1] != "1" else "")
-    return {"k_refine": "refine", "k_prune": "prune", "k_sim_exact": "sim_exact", "k_setup": "setup",
-            "k_bottleneck": "bottleneck", "k_rank": "rank", "k_sim_prep": "sim_prep", "k_best": "best",
-            "k_cost_prefix": "cost_prefix"}.get(k, k)
+    k = k.replace("<unnamed>::", "")
+    if k.startswith("k_sim_flow"):
+        return "sim_flow" + k.split("<")[1].rstrip(">").strip()
+    return {"k_refine": "refine", "k_refine_smem": "refine", "k_refine_list": "refine", "k_prune": "prune",
+            "k_prune_key": "prune", "k_prune_members": "prune", "k_sim_exact": "sim_exact",
+            "k_xsort_count": "sim_exact", "k_xsort_scan": "sim_exact", "k_xsort_scatter": "sim_exact",
+            "k_setup": "setup", "k_bottleneck": "bottleneck", "k_coarse_queue": "bottleneck", "k_rank": "rank",
+            "k_sim_prep": "sim_prep", "k_sim_classify": "sim_prep", "k_best": "best",
+            "k_cost_prefix": "cost_prefix", "k_dedup_insert": "dedup", "k_dedup_resolve": "dedup",
+            "k_dedup_copy_dp": "dedup_copy", "k_dedup_copy_refine": "dedup_copy", "k_coarse_copy": "dedup_copy",
+            "k_sim_share": "sim_share"}.get(k, k)
 
 
 def launches(path, tag):
@@ -110,7 +120,7 @@ def full(path, tag):
         if "dram__bytes_read.sum" in hdr:
             i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             rd, wr = to_bytes(r[i], units[i]), to_bytes(r[j], units[j])
-            traffic[name] = rd + wr
+            traffic[name] = max(traffic.get(name, 0.0), rd + wr)
         stalls = [(hdr[i], r[i]) for i in range(len(hdr))
                   if hdr[i].startswith("smsp__average_warps_issue_stalled_")
                   and hdr[i].endswith("_per_issue_active.ratio") and r[i] not in ("", "nan", "-nan")]
