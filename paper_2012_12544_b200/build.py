@@ -68,12 +68,31 @@ def build_product(force=False, verbose=False):
     return SO
 
 
+CLI = os.path.join(HERE, "bin", "bapipe")
+JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+
+
+def build_cli(force=False):
+    """The `bapipe` command-line front end (cli/bapipe.cpp), linked against
+    the product library; needs nlohmann/json.hpp (shipped with the image)."""
+    if not os.path.exists(os.path.join(JSON_DIR, "json.hpp")):
+        return None
+    src = os.path.join(HERE, "cli", "bapipe.cpp")
+    deps = [src, SO] + [os.path.join(ROOT, "include", "bapipe_b200", f) for f in ("explorer.hpp", "io.hpp")]
+    if not force and not _stale(CLI, deps):
+        return CLI
+    os.makedirs(os.path.dirname(CLI), exist_ok=True)
+    subprocess.run([_host_cxx(), "-std=c++17", "-O2", "-I" + os.path.join(ROOT, "include"), "-I" + JSON_DIR, "-o",
+                    CLI, src, "-L" + HERE, "-lbapipe_b200", "-Wl,-rpath,$ORIGIN/.."], check=True)
+    return CLI
+
+
 def build_oracles():
     """Test-only checkers: the C restatement always, oracle/_ref when the
     reference sources are present (dev container only)."""
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/include"):
-        targets += ["ref", "dropin"]
+        targets += ["ref", "dropin", "cli"]
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")] + targets, check=True)
     emu = os.path.join(ROOT, "tests", "emu")
     if os.path.isdir(emu):
@@ -85,5 +104,6 @@ def build_oracles():
 
 if __name__ == "__main__":
     build_product(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build_cli(force="--force" in sys.argv)
     build_oracles()
     print(SO)
