@@ -160,6 +160,73 @@ BPK_HDNI void estimate(const PS& p, const NetView& v, const ChainView& c, int ki
     }
 }
 
+// estimate() of a whole-layer plan that differs from the one whose estimate
+// is in s / o only in the adjacent stages i0 < i1 (a memory_fine_tune trial
+// move, partition.hpp:403-410).  The reference recomputes the whole estimate
+// (cost_models.hpp:124-166) for every trial; the per-stage values of the
+// other stages are the ones it computed before, with the same (absent)
+// errors, so only stages i0, i1, the cut between them and the aggregates are
+// recomputed here.  On a whole-layer plan F, B, W are integers, so the
+// per-link bandwidth demands a / Fm (or 2a / (Fm + Bm) for fbp-as) cannot
+// leave int64 once 2a and Fm + Bm fit: they are not formed during trials
+// (o.max_bw is left stale; the caller recomputes it for the final plan).
+BPK_HDNI void estimate_move(const WholePlan& p, const NetView& v, const ChainView& c, int kind, int64_t M,
+                            int64_t micro, const EstScratch& s, EstOut& o, int i0, int i1, Err& e) {
+    const int N = c.N;
+    const bool dbl = (kind == KIND_FBP || kind == KIND_SO);
+    // stage_costs (103-119) for the two stages, in the reference's order; the
+    // cut between them is stage i1's input (and stage 0's own activation unit
+    // is its output cut, plan.hpp:144-148)
+    for (int i = i0; i <= i1; ++i) {
+        p.FBW(i, s.F[i], s.B[i], s.W[i], e);
+        if (e.bad()) return;
+        if (i == i1 || i == 0) {
+            const int64_t act = (i >= 1) ? act_at(v, p.H(i - 1), e) : act_at(v, p.H(0), e);
+            if (e.bad()) return;
+            s.A[i] = act * micro;
+            if (i >= 1) {
+                s.SR[i] = link_sr(p, v, c, i - 1, micro, e);
+                if (e.bad()) return;
+            }
+        }
+    }
+    Rat Fm{0, 1}, Bm{0, 1};
+    int64_t SRm = 0;
+    bool balanced = true;
+    for (int i = 0; i < N; ++i) {
+        if (!rat_eq(s.F[i], s.F[0]) || !rat_eq(s.B[i], s.B[0])) balanced = false;
+        if (rat_gt(s.F[i], Fm)) Fm = s.F[i];
+        if (rat_gt(s.B[i], Bm)) Bm = s.B[i];
+        if (s.SR[i] > SRm) SRm = s.SR[i];
+    }
+    for (int i = 1; i < N; ++i)
+        if (s.SR[i] != s.SR[N > 1 ? 1 : 0]) balanced = false;
+    o.Fm = Fm;
+    o.Bm = Bm;
+    o.minibatch = minibatch_time(kind, M, N, Fm, Bm, R(SRm), e);
+    o.bubble = bubble_fraction(kind, M, N, Fm, Bm, R(SRm), e);
+    o.heuristic = (!balanced || M < N) ? 1 : 0;
+    if (e.bad()) return;
+    for (int i = i0; i <= i1; ++i) {
+        Rat fm = rat_mul(R(N - i), R(s.A[i]), e);
+        if (dbl) fm = rat_mul(R(2), fm, e);
+        Rat wm = rat_mul(R(2), s.W[i], e);
+        s.Mem[i] = rat_add(fm, wm, e);
+        if (e.bad()) return;
+    }
+    o.feasible = 1;
+    o.peak_mem = Rat{0, 1};
+    for (int i = 0; i < N; ++i) {
+        if (rat_gt(s.Mem[i], R(c.cap[i]))) o.feasible = 0;
+        if (rat_gt(s.Mem[i], o.peak_mem)) o.peak_mem = s.Mem[i];
+    }
+    // the bandwidth-demand operations that could overflow (see above)
+    if (kind == KIND_FBP) {
+        (void)rat_add(Fm, Bm, e);
+        for (int k = 0; k + 1 < N; ++k) (void)rat_mul(R(2), R(s.A[k + 1]), e);
+    }
+}
+
 // overloads() bookkeeping (partition.hpp:344-356) on the estimate in s.Mem:
 // ov = mem > cap ? mem - cap : 0; total += ov; worst = first max (381-383).
 // Only memory_fine_tune performs these Rat operations in the reference, so
@@ -282,7 +349,7 @@ BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, in
     if (e.bad()) return FT_OK;
     Rat total = o.total_over;
     int worst = o.worst;
-    int guard = 0;
+    int guard = 0, trials = 0;
     const int limit = 8 * (int)((int64_t)N * v.L + 4);
     const Rat zero{0, 1};
     while (rat_gt(total, zero)) {
@@ -309,7 +376,14 @@ BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, in
                 int32_t sw_lo = lo[worst], sw_hi = hi[worst], sn_lo = lo[nb], sn_hi = hi[nb];
                 if (cd[ci] < 0) { lo[worst] += 1; hi[nb] += 1; }
                 else { hi[worst] -= 1; lo[nb] -= 1; }
-                estimate(wp, v, c, kind, M, micro, s, o, nullptr, e);
+                // the trial changes stages i0 < i1 only: incremental estimate,
+                // with their scratch entries saved for the undo below
+                const int i0 = worst < nb ? worst : nb, i1 = i0 + 1;
+                const Rat kF[2] = {s.F[i0], s.F[i1]}, kB[2] = {s.B[i0], s.B[i1]}, kW[2] = {s.W[i0], s.W[i1]},
+                          kM[2] = {s.Mem[i0], s.Mem[i1]};
+                const int64_t kA[3] = {s.A[0], s.A[i1], s.SR[i1]};
+                estimate_move(wp, v, c, kind, M, micro, s, o, i0, i1, e);
+                ++trials;
                 if (!e.bad()) overloads_from_mem(c, s, o, e);
                 if (e.bad()) return FT_OK;
                 bool ok = rat_lt(o.total_over, total);
@@ -321,12 +395,11 @@ BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, in
                         Rat t = rat_add(s.F[n], s.B[n], e);
                         if (rat_gt(t, target)) target = t;
                     }
+                    // link_sr(k) of this plan is s.SR[k + 1] (the trial's
+                    // estimate formed it; the reference forms it again here)
                     bool bott = false;
-                    for (int k = 0; k + 1 < N; ++k) {
-                        int64_t ct = link_sr(wp, v, c, k, micro, e);
-                        if (e.bad()) return FT_OK;
-                        if (rat_gt(R(ct), target)) bott = true;
-                    }
+                    for (int k = 0; k + 1 < N; ++k)
+                        if (rat_gt(R(s.SR[k + 1]), target)) bott = true;
                     ok = !bott;
                 }
                 if (ok) {
@@ -336,10 +409,18 @@ BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, in
                     break;
                 }
                 lo[worst] = sw_lo; hi[worst] = sw_hi; lo[nb] = sn_lo; hi[nb] = sn_hi;
+                s.F[i0] = kF[0]; s.F[i1] = kF[1];
+                s.B[i0] = kB[0]; s.B[i1] = kB[1];
+                s.W[i0] = kW[0]; s.W[i1] = kW[1];
+                s.Mem[i0] = kM[0]; s.Mem[i1] = kM[1];
+                s.A[0] = kA[0]; s.A[i1] = kA[1]; s.SR[i1] = kA[2];
             }
         }
         if (!moved) return FT_REJ;
     }
+    // the accepted plan's full estimate (the bandwidth demands were not
+    // formed during the trials; same values, no new errors)
+    if (trials) estimate(wp, v, c, kind, M, micro, s, o, nullptr, e);
     return FT_OK;
 }
 

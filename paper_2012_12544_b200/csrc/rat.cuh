@@ -89,6 +89,26 @@ BPK_HD uint64_t umod64(uint64_t a, uint64_t b) {
     return a % b;
 }
 
+// x mod m for a 32-bit m without the 64-bit software remainder: a quotient
+// estimate from a double reciprocal (off by at most ~2^13), one exact
+// correction in double (|r| < 2^53), then integer fix-ups.  The result is
+// exact whatever the reciprocal's rounding, so host and device agree.
+BPK_HD uint32_t umod_u64_u32(uint64_t x, uint32_t m) {
+    if ((x >> 32) == 0) return (uint32_t)x % m;
+    if (m <= 1) return 0;
+#ifdef __CUDA_ARCH__
+    const double rm = __drcp_rn((double)m);
+#else
+    const double rm = 1.0 / (double)m;
+#endif
+    const uint64_t q = (uint64_t)((double)x * rm);
+    int64_t r = (int64_t)(x - q * (uint64_t)m);
+    r -= (int64_t)((double)r * rm) * (int64_t)m;
+    while (r < 0) r += m;
+    while (r >= (int64_t)m) r -= m;
+    return (uint32_t)r;
+}
+
 // out of line: inlined at its ~20 call sites it dominated the kernels' code
 // size (instruction-cache misses were the top stall in refine and prune)
 BPK_HDNI uint64_t gcd_u64(uint64_t u, uint64_t v) {
@@ -97,8 +117,8 @@ BPK_HDNI uint64_t gcd_u64(uint64_t u, uint64_t v) {
     if (v == 0) return u;
     if (u < v) { uint64_t t = u; u = v; v = t; }
     if ((v >> 32) == 0) {              // one Euclid step brings both below 2^32
-        uint64_t r = umod64(u, v);
-        return r == 0 ? v : gcd_u32((uint32_t)v, (uint32_t)r);
+        const uint32_t r = umod_u64_u32(u, (uint32_t)v);
+        return r == 0 ? v : gcd_u32((uint32_t)v, r);
     }
     int shift = bpk_ffs64((long long)(u | v)) - 1;
     u >>= (bpk_ffs64((long long)u) - 1);
@@ -208,25 +228,6 @@ BPK_HD uint64_t inv64_lift(uint32_t m, uint32_t x32) {
     return x * (2 - (uint64_t)m * x);
 }
 
-// x mod m for a 32-bit m without the 64-bit software remainder: a quotient
-// estimate from a double reciprocal (off by at most ~2^13), one exact
-// correction in double (|r| < 2^53), then integer fix-ups.  The result is
-// exact whatever the reciprocal's rounding, so host and device agree.
-BPK_HD uint32_t umod_u64_u32(uint64_t x, uint32_t m) {
-    if ((x >> 32) == 0) return (uint32_t)x % m;
-    if (m <= 1) return 0;
-#ifdef __CUDA_ARCH__
-    const double rm = __drcp_rn((double)m);
-#else
-    const double rm = 1.0 / (double)m;
-#endif
-    const uint64_t q = (uint64_t)((double)x * rm);
-    int64_t r = (int64_t)(x - q * (uint64_t)m);
-    r -= (int64_t)((double)r * rm) * (int64_t)m;
-    while (r < 0) r += m;
-    while (r >= (int64_t)m) r -= m;
-    return (uint32_t)r;
-}
 
 // a + s*b with s = +1 / -1 (operator+ / operator-), Knuth 4.5.1: with
 // g = gcd(a.d, b.d), t = a.n*(b.d/g) + b.n*(a.d/g) and g2 = gcd(t, g) the

@@ -81,6 +81,11 @@ int main(int argc, char** argv) {
                 printf("umod fail x=%llu m=%u\n", (unsigned long long)x, m);
                 return 1;
             }
+            const uint64_t gu = rnd() >> (rnd() % 64), gv = rnd() >> (rnd() % 64);
+            if (gcd_u64(gu, gv) != (uint64_t)ugcd(gu, gv)) {
+                printf("gcd fail %llu %llu\n", (unsigned long long)gu, (unsigned long long)gv);
+                return 1;
+            }
             uint32_t o = (uint32_t)rnd() | 1u;
             if (o * inv32_odd(o) != 1u || (uint64_t)o * inv64_lift(o, inv32_odd(o)) != 1ull) {
                 printf("inverse fail %u\n", o);
