@@ -176,6 +176,8 @@ def rooflines(stats, steps, clocks, problem, step_ms):
             e["achieved_gops"] = ops / (ms * 1e6)
             e["frac"] = e["achieved_gops"] / issue_peak
         kern[k] = e
+    crit = stats.pop("refine_critical_path", None)
+    kern.pop("refine_critical_path", None)
     dom = max(stats, key=lambda k: stats[k]["ms"])
     d = kern[dom]
     u = work_unit(dom)
@@ -186,6 +188,14 @@ def rooflines(stats, steps, clocks, problem, step_ms):
                      is not None else f"{dom}: no work count"),
             "peak_source": f"{SMS} SMs x {LANES} lanes x {f_max / 1e6:.0f} MHz (sm_max_mhz, {peak_kind} "
                            f"MEASURED_PEAKS.json); HBM {peaks.get('hbm_gbs')} GB/s"}
+    if dom == "refine" and crit and crit["work"] > 0:
+        # refine is a serial recurrence per query: its time is the longest
+        # query's walk, so the meaningful bound is per-step latency on that path
+        ms_launch = d["ms_per_step"]
+        roof["critical_path"] = {"boundary_steps": crit["work"], "us_per_step": 1e3 * ms_launch / crit["work"],
+                                 "cycles_per_step": ms_launch * 1e-3 * f_max / crit["work"],
+                                 "note": "one query's intra_layer_refine walk is serial (each boundary step "
+                                         "reads the stage times the previous step wrote)"}
     # sweep bound: t_roof = sum B_cost / BW + (X_dp * c_dp + X_sim * c_sim) / issue
     q = problem.queries
     U = np.array([problem.networks[i].L for i in q["network"]], dtype=np.float64)

@@ -492,6 +492,7 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
             c->stats["minmax_dp"].work = (double)work[WORK_DP_WHOLE];
             c->stats["minmax_dp_coarse"].work = (double)work[WORK_DP_COARSE];
             c->stats["refine"].work = (double)work[WORK_REFINE];
+            c->stats["refine_critical_path"].work = (double)work[WORK_REFINE_MAX];
             c->stats["prune"].work = (double)work[WORK_PRUNE];
             for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work = (double)work[WORK_SIM_EVENTS + k];
         }

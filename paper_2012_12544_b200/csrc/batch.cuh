@@ -64,9 +64,10 @@ enum { SIM_CLASSES = 11, SIM_EXACT = 8, SIM_FLOW = 9, SIM_FLOW_CLASSES = 2 };
 // the dataflow kernel: their serial walk would otherwise set the kernel time
 constexpr int64_t FLOW_MIN_EVENTS = 1024;
 // instrumentation slots of BatchDev::work (algorithmic work of one run)
-// refine: boundary steps evaluated; prune: candidate-stages estimated
-enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_REFINE = 2, WORK_PRUNE = 3, WORK_SIM_EVENTS = 4,
-       WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
+// refine: boundary steps evaluated (and the longest query's count: the serial
+// critical path); prune: candidate-stages estimated
+enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_REFINE = 2, WORK_PRUNE = 3, WORK_REFINE_MAX = 4,
+       WORK_SIM_EVENTS = 5, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
 enum { XBUCKETS = 32768, XSIM_WARPS_PER_SM = 32 };
 
 // Per-candidate device state (beyond the bp_candidate output record).

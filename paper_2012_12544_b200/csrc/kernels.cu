@@ -297,7 +297,9 @@ __global__ void k_refine(BatchDev B) {
     if (i >= B.nq) return;
     const int qi = B.qorder[i];
     refine_query(B, qi);
-    if (B.qs[qi].refined) atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
+    if (!B.qs[qi].refined) return;
+    atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
+    atomicMax(&B.work[WORK_REFINE_MAX], (unsigned long long)B.qs[qi].refine_evals);
 }
 
 // intra_layer_refine is a long serial walk per query (up to ~3000 boundary
@@ -333,6 +335,7 @@ __global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm) {
         const int qi = B.rlist[i];
         refine_query_at(B, qi, &sc);
         atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
+        atomicMax(&B.work[WORK_REFINE_MAX], (unsigned long long)B.qs[qi].refine_evals);
     }
 }
 
