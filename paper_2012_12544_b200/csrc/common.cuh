@@ -100,8 +100,11 @@ BPK_HD int64_t act_at(const NetView& v, int64_t j, Err& e) {
     return v.a[j - 1];
 }
 
+// fp + bp of layer j on type t, from the prefix sums (the refine kernel keeps
+// only those in shared memory)
 BPK_HD int64_t fpbp_at(const NetView& v, int64_t j, int32_t t) {
-    return v.fp[(int64_t)t * v.L + (j - 1)] + v.bp[(int64_t)t * v.L + (j - 1)];
+    const int64_t o = (int64_t)t * (v.L + 1) + j;
+    return (v.Pfp[o] - v.Pfp[o - 1]) + (v.Pbp[o] - v.Pbp[o - 1]);
 }
 
 BPK_HD int64_t pref(const int64_t* P, int64_t L, int32_t t, int64_t j) {

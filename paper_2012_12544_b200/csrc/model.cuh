@@ -513,6 +513,39 @@ BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, 
     return FS_MOVE;
 }
 
+// The reference's boundary step on exact Rats (partition.hpp:302-327), for
+// the steps refine_fast_step cannot bound; out of line so that the common
+// path's code stays small.  Returns FS_NOMOVE or FS_MOVE (errors go to e,
+// which the caller checks first).
+BPK_HDNI int refine_exact_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh,
+                               Rat& nl, Err& e) {
+    const Rat zero{0, 1}, step{1, 1024};
+    x = rat_div(rat_sub(t_hi, t_lo, e), rat_add(R(c_from), R(c_to), e), e);
+    if (rat_ge(x, avail)) x = rat_sub(avail, step, e);
+    if (e.bad() || !rat_gt(x, zero)) return FS_NOMOVE;
+    if (x.d > 1024) {                                       // quantize (257-265)
+        const Rat y = rat_mul(x, R(1024), e);
+        if (e.bad()) return FS_NOMOVE;
+        const Rat qlo = rat_nd(rat_floor(y), 1024, e);
+        const Rat qhi = rat_nd(rat_ceil(y), 1024, e);
+        if (rat_ge(qhi, avail)) {
+            x = qlo;
+        } else {
+            const Rat s_lo = rat_max(rat_sub(t_hi, rat_mul(qlo, R(c_from), e), e),
+                                     rat_add(t_lo, rat_mul(qlo, R(c_to), e), e));
+            const Rat s_hi = rat_max(rat_sub(t_hi, rat_mul(qhi, R(c_from), e), e),
+                                     rat_add(t_lo, rat_mul(qhi, R(c_to), e), e));
+            if (e.bad()) return FS_NOMOVE;
+            x = rat_le(s_lo, s_hi) ? qlo : qhi;
+        }
+    }
+    if (!rat_gt(x, zero) || rat_ge(x, avail)) return FS_NOMOVE;
+    nh = rat_sub(t_hi, rat_mul(x, R(c_from), e), e);
+    nl = rat_add(t_lo, rat_mul(x, R(c_to), e), e);
+    if (e.bad() || rat_ge(rat_max(nh, nl), t_hi)) return FS_NOMOVE;
+    return FS_MOVE;
+}
+
 // True when recomputing the stage time from the plan (stage_fp_time +
 // stage_bp_time, plan.hpp:90-113) cannot overflow: every partial sum is at
 // most t and its reduced denominator divides den(lead) * den(trail).
@@ -526,8 +559,6 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
     stats[0] = stats[1] = stats[2] = stats[3] = 0;   // iterations, evaluated steps, moves, exact steps
     if (N <= 1) return;
     for (int s = 0; s < N; ++s) dirty[s] = 1;
-    const Rat zero{0, 1};
-    const Rat step{1, 1024};
     auto T = [&](int s) -> Rat {
         if (dirty[s] & 1) {
             stage_times(v, c, s, lo, hi, lead, trail, tF[s], tB[s], e);
@@ -582,32 +613,9 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
                 if (fs == FS_NOMOVE) continue;
                 if (fs == FS_FALLBACK) {                   // the reference's Rat step, verbatim
                     ++stats[3];
-                    x = rat_div(rat_sub(t_hi, t_lo, e), rat_add(R(c_from), R(c_to), e), e);
-                    if (rat_ge(x, avail)) x = rat_sub(avail, step, e);
+                    const int xs = refine_exact_step(t_hi, t_lo, c_from, c_to, avail, x, nh, nl, e);
                     if (e.bad()) return;
-                    if (!rat_gt(x, zero)) continue;
-                    // quantize (257-265)
-                    if (x.d > 1024) {
-                        Rat y = rat_mul(x, R(1024), e);
-                        if (e.bad()) return;
-                        Rat qlo = rat_nd(rat_floor(y), 1024, e);
-                        Rat qhi = rat_nd(rat_ceil(y), 1024, e);
-                        if (rat_ge(qhi, avail)) {
-                            x = qlo;
-                        } else {
-                            Rat s_lo = rat_max(rat_sub(t_hi, rat_mul(qlo, R(c_from), e), e),
-                                               rat_add(t_lo, rat_mul(qlo, R(c_to), e), e));
-                            Rat s_hi = rat_max(rat_sub(t_hi, rat_mul(qhi, R(c_from), e), e),
-                                               rat_add(t_lo, rat_mul(qhi, R(c_to), e), e));
-                            if (e.bad()) return;
-                            x = rat_le(s_lo, s_hi) ? qlo : qhi;
-                        }
-                    }
-                    if (!rat_gt(x, zero) || rat_ge(x, avail)) continue;
-                    nh = rat_sub(t_hi, rat_mul(x, R(c_from), e), e);
-                    nl = rat_add(t_lo, rat_mul(x, R(c_to), e), e);
-                    if (e.bad()) return;
-                    if (rat_ge(rat_max(nh, nl), t_hi)) continue;
+                    if (xs == FS_NOMOVE) continue;
                 }
                 // apply_move (269-292)
                 int a = n0, b = n0 + 1;

@@ -139,11 +139,13 @@ BPK_HD bool refine_wanted(const BatchDev& B, int qi) {
     return Q.schema_ok && need && !qs.dp_shape && Q.N >= 2;
 }
 
-BPK_HDNI void refine_query_at(const BatchDev& B, int qi, const RefineScratch* sc) {
+// vo (nullable): the query's network view with its tables staged elsewhere
+// (shared memory in k_refine_smem)
+BPK_HDNI void refine_query_at(const BatchDev& B, int qi, const RefineScratch* sc, const NetView* vo = nullptr) {
     const QDesc Q = B.q[qi];
     QState& qs = B.qs[qi];
     if (!refine_wanted(B, qi)) return;
-    NetView v = net_view(B.P, Q.net);
+    NetView v = vo ? *vo : net_view(B.P, Q.net);
     ChainView c = chain_view(B.P, Q.cl, Q.N);
     const int64_t o = Q.qstage_off;
     int32_t* lo = sc ? sc->lo : B.qlo + o;

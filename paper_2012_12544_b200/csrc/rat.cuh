@@ -235,6 +235,8 @@ BPK_HD uint64_t inv64_lift(uint32_t m, uint32_t x32) {
 // Out of line on purpose: inlining every Rat operation into the refine and
 // simulator loops produced ~1 MB of SASS and the kernels stalled on
 // instruction fetch (ncu: "no_instruction" 17.5 cycles per issue).
+BPK_HDNI Rat rat_addsub_general(Rat a, Rat b, int s, Err& e);
+
 BPK_HDNI Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
     i128 bn = s > 0 ? (i128)b.n : -(i128)b.n;
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n + bn, 1, e);
@@ -270,6 +272,13 @@ BPK_HDNI Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
             return Rat{tt < 0 ? (int64_t)((uint64_t)0 - q) : (int64_t)q, (int64_t)den};
         }
     }
+    return rat_addsub_general(a, b, s, e);
+}
+
+// 64-bit denominators or a 128-bit t: kept out of the hot function so the
+// kernels' instruction stream stays small.
+BPK_HDNI Rat rat_addsub_general(Rat a, Rat b, int s, Err& e) {
+    i128 bn = s > 0 ? (i128)b.n : -(i128)b.n;
     uint64_t g = gcd_u64((uint64_t)a.d, (uint64_t)b.d);
     if (g == 1) return fit128((i128)a.n * b.d + bn * a.d, (i128)a.d * b.d, e);
     int64_t ad = (int64_t)udiv_exact64((uint64_t)a.d, g), bd = (int64_t)udiv_exact64((uint64_t)b.d, g);
