@@ -6,6 +6,9 @@
 // There is no CPU fallback: without a usable device, bp_create returns NULL.
 #include <cuda_runtime.h>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <new>
@@ -271,14 +274,19 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     const size_t nqs = (size_t)nq, nc = (size_t)hb.ncand, ns = (size_t)hb.nstage, nqst = (size_t)hb.nqstage,
                  nms = (size_t)hb.nmslot;
     Layout L;
-    // inputs (one H2D copy): QDesc, Mpool, DP items, dp_count
+    // inputs (one H2D copy): QDesc, Mpool, dp_count
     size_t o_q = L.take<QDesc>(nqs);
     size_t o_M = L.take<int64_t>(hb.Mpool.size());
-    size_t o_items = L.take<DPItem>(nqs + nms);
     size_t o_cnt = L.take<int32_t>(4);
+    size_t in_end = L.off;
+    // DP items and the scheduling orders (built on the device, k_sched_*)
+    size_t o_items = L.take<DPItem>(nqs + nms);
     size_t o_qord = L.take<int32_t>(nqs);
     size_t o_cperm = L.take<int32_t>(nc);
-    size_t in_end = L.off;
+    const size_t otemp_bytes = sched_temp_bytes(std::max(1, nq));
+    size_t o_okey = L.take<unsigned long long>(nqs), o_okey2 = L.take<unsigned long long>(nqs);
+    size_t o_oval = L.take<int32_t>(nqs), o_ocnt = L.take<int32_t>(nqs), o_ocoff = L.take<int32_t>(nqs),
+           o_owfl = L.take<int32_t>(nqs), o_owoff = L.take<int32_t>(nqs), o_otemp = L.take<char>(otemp_bytes);
     // outputs
     size_t o_res = L.take<bp_query_result>(nqs);
     size_t o_cand = L.take<bp_candidate>(nc);
@@ -316,11 +324,8 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     char* h = (char*)B->stage_in.p;
     std::memcpy(h + o_q, hb.q.data(), nqs * sizeof(QDesc));
     if (!hb.Mpool.empty()) std::memcpy(h + o_M, hb.Mpool.data(), hb.Mpool.size() * 8);
-    if (!hb.whole_items.empty()) std::memcpy(h + o_items, hb.whole_items.data(), hb.whole_items.size() * sizeof(DPItem));
-    int32_t cnt[4] = {(int32_t)hb.whole_items.size(), 0, 0, 0};
+    int32_t cnt[4] = {0, 0, 0, 0};   // [0] is set by k_sched_scatter, [1] by k_coarse_queue
     std::memcpy(h + o_cnt, cnt, sizeof(cnt));
-    if (nqs) std::memcpy(h + o_qord, hb.qorder.data(), nqs * 4);
-    if (nc) std::memcpy(h + o_cperm, hb.cperm.data(), nc * 4);
     B->in_off = 0;
     B->in_bytes = in_end;
     B->res_off = o_res;
@@ -383,6 +388,15 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.pmask = stab - 1;
     D.qorder = dptr<int32_t>(b, o_qord);
     D.cperm = dptr<int32_t>(b, o_cperm);
+    D.okey = dptr<unsigned long long>(b, o_okey);
+    D.okey2 = dptr<unsigned long long>(b, o_okey2);
+    D.oval = dptr<int32_t>(b, o_oval);
+    D.ocnt = dptr<int32_t>(b, o_ocnt);
+    D.ocoff = dptr<int32_t>(b, o_ocoff);
+    D.owfl = dptr<int32_t>(b, o_owfl);
+    D.owoff = dptr<int32_t>(b, o_owoff);
+    D.otemp = dptr<char>(b, o_otemp);
+    D.otemp_bytes = otemp_bytes;
     D.sim_list = dptr<int32_t>(b, o_slist);
     D.sim_count = dptr<int32_t>(b, o_scnt);
     D.details = details ? 1 : 0;
@@ -417,6 +431,8 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(c, e, "memset");
     const int T = c->max_T, maxN = std::max(1, hb.max_N);
     timed(c, "setup", st, [&] { launch_setup(D, st); });
+    // 3 own kernels (+ CUB's radix sort / scans, library code, not counted)
+    timed(c, "sched", st, [&] { launch_sched(D, st); }, 3);
     timed(c, "dedup", st, [&] { launch_dedup(D, st); }, 2);
     if (!hb.whole_items.empty()) {
         timed(c, "minmax_dp", st, [&] {
@@ -657,10 +673,20 @@ int bp_explore_batch(bp_ctx* c, const bp_query* q, int nq, bp_query_result* res,
         cudaStream_t st = (cudaStream_t)stream;
         if (!c->cached) c->cached = new bp_batch();
         bp_batch* B = c->cached;
+        static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        const auto t0 = now();
         int rc = prepare(c, B, q, nq, stages != nullptr, st);
+        const auto t1 = now();
         if (rc == BP_OK) rc = upload_inputs(c, B, st);
         if (rc == BP_OK) rc = run(c, B, st);
+        const auto t2 = now();
         if (rc == BP_OK) rc = fetch(c, B, res, cand, stages, st);
+        if (timing) {
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            fprintf(stderr, "bp_explore_batch: prepare %.2f ms, launch %.2f ms, wait+fetch %.2f ms\n", ms(t0, t1),
+                    ms(t1, t2), ms(t2, now()));
+        }
         return rc;
     } catch (const std::bad_alloc&) {
         return fail(c, BP_OUT_OF_MEMORY, "host allocation failed");

@@ -113,8 +113,15 @@ struct BatchDev {
     Rat* simbuf;              // exact simulator state, 9 Rats per stage slot
     int32_t* cq;              // candidate -> query
     int32_t* corder;          // ranking scratch, one slot per candidate
-    const int32_t* qorder;    // scheduling order of queries (host_prep.hpp)
-    const int32_t* cperm;     // scheduling order of candidates
+    // scheduling orders, built on the device each run (k_sched_*): queries by
+    // (stage count, layers, network, chain type signature) so that a warp's
+    // lanes run similar instruction streams; candidates follow their query
+    int32_t* qorder;          // [nq]
+    int32_t* cperm;           // [ncand]
+    unsigned long long *okey, *okey2;   // [nq] order sort keys (in / out)
+    int32_t *oval, *ocnt, *ocoff, *owfl, *owoff;   // [nq] sort values, counts, offsets
+    void* otemp;              // CUB temporary storage
+    size_t otemp_bytes;
     int32_t* sim_list;        // [SIM_CLASSES][ncand] candidate lists per simulator class
     int32_t* sim_count;       // [SIM_CLASSES]
     // exact-simulator scheduling: counting sort of its list by (N, log2 M)

@@ -154,13 +154,7 @@ inline bool build_clusters(const bp_cluster* cls, int n, HostCls& H, std::string
 struct HostBatch {
     std::vector<QDesc> q;
     std::vector<int64_t> Mpool;
-    std::vector<DPItem> whole_items;
-    // Scheduling orders (results do not depend on them): queries sorted by
-    // (stage count, layer count, network, chain type signature) so that a
-    // warp's lanes run similar instruction streams; candidates follow their
-    // query's position.
-    std::vector<int32_t> qorder;
-    std::vector<int32_t> cperm;
+    std::vector<DPItem> whole_items;   // in query order (the device sorts its own copy)
     int64_t ncand = 0, nstage = 0, nqstage = 0, nmslot = 0;
     int max_units = 0, max_N = 0, max_nbase = 0;
 };
@@ -236,36 +230,10 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
             HB.max_units = std::max(HB.max_units, nd.L);
         }
     }
-    // heaviest DP instances first (load balance across thread blocks)
-    std::stable_sort(HB.whole_items.begin(), HB.whole_items.end(), [&](const DPItem& x, const DPItem& y) {
-        int64_t lx = HN.desc[HB.q[x.q].net].L, ly = HN.desc[HB.q[y.q].net].L;
-        return lx * lx > ly * ly;
-    });
-    std::vector<uint64_t> sig(nq);
-    for (int i = 0; i < nq; ++i) {
-        const QDesc& Q = HB.q[i];
-        const ClDesc& cd = HC.desc[Q.cl];
-        uint64_t h = 1469598103934665603ULL;   // FNV-1a over the chain's type ids
-        for (int k = 0; k < Q.N; ++k) {
-            h ^= (uint64_t)(uint32_t)HC.ctype[cd.off_acc + k];
-            h *= 1099511628211ULL;
-        }
-        sig[i] = h;
-    }
-    HB.qorder.resize(nq);
-    for (int i = 0; i < nq; ++i) HB.qorder[i] = i;
-    std::stable_sort(HB.qorder.begin(), HB.qorder.end(), [&](int a, int b) {
-        const QDesc &x = HB.q[a], &y = HB.q[b];
-        if (x.N != y.N) return x.N > y.N;
-        int64_t lx = HN.desc[x.net].L, ly = HN.desc[y.net].L;
-        if (lx != ly) return lx > ly;
-        if (x.net != y.net) return x.net < y.net;
-        return sig[a] < sig[b];
-    });
-    HB.cperm.clear();
-    HB.cperm.reserve((size_t)HB.ncand);
-    for (int qi : HB.qorder)
-        for (int64_t c = 0; c < 2 * (int64_t)HB.q[qi].nbase; ++c) HB.cperm.push_back((int32_t)(HB.q[qi].cand_off + c));
+    // The scheduling orders (queries by stage count, layers, network and
+    // chain type signature; candidates following their query; whole-layer DP
+    // items heaviest first) are built on the device (kernels.cu, k_sched_*):
+    // results do not depend on them.
     return true;
 }
 

@@ -14,6 +14,8 @@
 //   k_sim          K4  schedule simulation, thread per candidate
 //   k_rank         K5  ranking / query outcome, thread per query
 //   k_best             argmin of the per-query bests (multi-GPU exchange record)
+#include <cub/cub.cuh>
+
 #include "kernels.h"
 #include "phases.cuh"
 
@@ -570,6 +572,63 @@ void launch_cost_prefix(const NetDesc* nets, int n_nets, const int64_t* fp, cons
 
 void launch_setup(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_setup<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+}
+
+// ---- scheduling orders on the device: a radix sort of one packed key per
+// query, then the candidate permutation and the whole-layer DP item list by
+// exclusive scans over the sorted queries.  Only work placement depends on
+// them, never a result.
+__global__ void k_sched_keys(BatchDev B) {
+    const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    const QDesc Q = B.q[qi];
+    const ChainView c = chain_view(B.P, Q.cl, Q.N);
+    uint64_t h = 1469598103934665603ULL;   // FNV-1a over the chain's type ids
+    for (int k = 0; k < Q.N; ++k) h = (h ^ (uint64_t)(uint32_t)c.type[k]) * 1099511628211ULL;
+    const uint64_t N = Q.N < 255 ? (uint64_t)Q.N : 255, L = B.P.nets[Q.net].L;
+    const uint64_t Lk = L < 65535 ? L : 65535;
+    // stage count desc, layers desc, network, signature
+    B.okey[qi] = ((255 - N) << 56) | ((65535 - Lk) << 40) | ((uint64_t)(Q.net & 0xFF) << 32) | (h >> 32);
+    B.oval[qi] = qi;
+}
+
+__global__ void k_sched_counts(BatchDev B) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= B.nq) return;
+    const QDesc Q = B.q[B.qorder[r]];
+    B.ocnt[r] = 2 * Q.nbase;
+    B.owfl[r] = (Q.schema_ok && Q.N >= 2) ? 1 : 0;
+}
+
+__global__ void k_sched_scatter(BatchDev B) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= B.nq) return;
+    const int qi = B.qorder[r];
+    const int64_t co = B.q[qi].cand_off;
+    for (int k = 0; k < B.ocnt[r]; ++k) B.cperm[B.ocoff[r] + k] = (int32_t)(co + k);
+    if (B.owfl[r]) B.dp_items[B.owoff[r]] = DPItem{qi, -1, -1};
+    if (r == B.nq - 1) B.dp_count[0] = B.owoff[r] + B.owfl[r];
+}
+
+size_t sched_temp_bytes(int nq) {
+    size_t a = 0, b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, a, (const unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                    (const int32_t*)nullptr, (int32_t*)nullptr, nq);
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (const int32_t*)nullptr, (int32_t*)nullptr, nq);
+    return a > b ? a : b;
+}
+
+void launch_sched(const BatchDev& B, cudaStream_t st) {
+    if (!B.nq) return;
+    k_sched_keys<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    size_t tb = B.otemp_bytes;
+    cub::DeviceRadixSort::SortPairs(B.otemp, tb, B.okey, B.okey2, B.oval, B.qorder, B.nq, 0, 64, st);
+    k_sched_counts<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    tb = B.otemp_bytes;
+    cub::DeviceScan::ExclusiveSum(B.otemp, tb, B.ocnt, B.ocoff, B.nq, st);
+    tb = B.otemp_bytes;
+    cub::DeviceScan::ExclusiveSum(B.otemp, tb, B.owfl, B.owoff, B.nq, st);
+    k_sched_scatter<<<blocks(B.nq, 128), 128, 0, st>>>(B);
 }
 void launch_dedup(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.dkey, 0, ((size_t)B.dmask + 1) * sizeof(unsigned long long), st);

@@ -10,6 +10,8 @@ namespace bpk {
 void launch_cost_prefix(const NetDesc* nets, int n_nets, const int64_t* fp, const int64_t* bp, const int64_t* w,
                         int64_t* Pfp, int64_t* Pbp, int64_t* Pc, int64_t* Pw, cudaStream_t st, int max_T);
 void launch_setup(const BatchDev& B, cudaStream_t st);
+void launch_sched(const BatchDev& B, cudaStream_t st);
+size_t sched_temp_bytes(int nq);
 void launch_partition(const BatchDev& B, int which, int grid, int max_units, int max_N, int T_slots,
                       cudaStream_t st);
 size_t partition_smem_bytes(int max_units, int max_N, int T_slots);
