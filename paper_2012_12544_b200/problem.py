@@ -158,7 +158,25 @@ class Problem:
         self.n_candidates = ncand
 
     # -- ctypes views ----------------------------------------------------------
+    def _cached(self, name, arrays, build):
+        """ctypes descriptor arrays hold raw pointers into the numpy arrays:
+        rebuild them only when an array object was replaced (e.g. by pin())."""
+        c = getattr(self, name, None)
+        if c is not None and len(c[0]) == len(arrays) and all(x is y for x, y in zip(c[0], arrays)):
+            return c[1]
+        out = build()
+        setattr(self, name, (arrays, out))
+        return out
+
     def c_networks(self):
+        arrays = [x for n in self.networks for x in (n.fp, n.bp, n.w, n.a)]
+        return self._cached("_c_nets", arrays, self._build_c_networks)
+
+    def c_clusters(self):
+        arrays = [x for c in self.clusters for x in (c.types, c.cap, c.bw, c.min_micro)]
+        return self._cached("_c_cls", arrays, self._build_c_clusters)
+
+    def _build_c_networks(self):
         arr = (abi.bp_network * len(self.networks))()
         for i, n in enumerate(self.networks):
             arr[i].n_layers = n.L
@@ -169,7 +187,7 @@ class Problem:
             arr[i].out_act_bytes = n.a.ctypes.data_as(abi.P64)
         return arr
 
-    def c_clusters(self):
+    def _build_c_clusters(self):
         arr = (abi.bp_cluster * len(self.clusters))()
         for i, c in enumerate(self.clusters):
             arr[i].n_accels = c.N
