@@ -431,9 +431,10 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_fail(c, e, "memset");
     const int T = c->max_T, maxN = std::max(1, hb.max_N);
     timed(c, "setup", st, [&] { launch_setup(D, st); });
-    // 3 own kernels (+ CUB's radix sort / scans, library code, not counted)
-    timed(c, "sched", st, [&] { launch_sched(D, st); }, 3);
     timed(c, "dedup", st, [&] { launch_dedup(D, st); }, 2);
+    // 3 own kernels (+ CUB's radix sort / scans, library code, not counted);
+    // after dedup: the DP item list holds class representatives only
+    timed(c, "sched", st, [&] { launch_sched(D, st); }, 3);
     if (!hb.whole_items.empty()) {
         timed(c, "minmax_dp", st, [&] {
             launch_partition(D, 0, std::min<int>(B->dp_grid, (int)hb.whole_items.size()), B->dp_max_units, maxN, T,

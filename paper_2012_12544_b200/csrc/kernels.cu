@@ -587,8 +587,9 @@ __global__ void k_sched_keys(BatchDev B) {
     for (int k = 0; k < Q.N; ++k) h = (h ^ (uint64_t)(uint32_t)c.type[k]) * 1099511628211ULL;
     const uint64_t N = Q.N < 255 ? (uint64_t)Q.N : 255, L = B.P.nets[Q.net].L;
     const uint64_t Lk = L < 65535 ? L : 65535;
-    // stage count desc, layers desc, network, signature
-    B.okey[qi] = ((255 - N) << 56) | ((65535 - Lk) << 40) | ((uint64_t)(Q.net & 0xFF) << 32) | (h >> 32);
+    // layers desc (the whole-layer DP's cost grows as L^2: heaviest blocks
+    // first), stage count desc, network, signature
+    B.okey[qi] = ((65535 - Lk) << 48) | ((255 - N) << 40) | ((uint64_t)(Q.net & 0xFF) << 32) | (h >> 32);
     B.oval[qi] = qi;
 }
 
@@ -597,7 +598,8 @@ __global__ void k_sched_counts(BatchDev B) {
     if (r >= B.nq) return;
     const QDesc Q = B.q[B.qorder[r]];
     B.ocnt[r] = 2 * Q.nbase;
-    B.owfl[r] = (Q.schema_ok && Q.N >= 2) ? 1 : 0;
+    // whole-layer DP items: class representatives only (k_dedup_resolve ran)
+    B.owfl[r] = (Q.schema_ok && Q.N >= 2 && B.qrep[B.qorder[r]] == B.qorder[r]) ? 1 : 0;
 }
 
 __global__ void k_sched_scatter(BatchDev B) {
