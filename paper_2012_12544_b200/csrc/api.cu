@@ -450,6 +450,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
         cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
     }
+    launch_prune_reset(D, st);
     cudaEventRecord(c->fork, st);
     cudaStreamWaitEvent(c->side, c->fork, 0);
     if (hb.nmslot > 0) {
@@ -461,8 +462,9 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "refine", st, [&] { launch_refine(D, c->sm_count, st); }, 2);
     timed(c, "dedup_copy", st, [&] { launch_dedup_copy_refine(D, st); });
     cudaStreamWaitEvent(st, c->join, 0);
-    // (pruning the coarse-plan candidates on the side stream during refine was
-    // measured slower: it takes issue slots from refine's single-lane warps)
+    // (pruning the coarse-path candidates on the side stream while refine runs,
+    // launch_prune(D, 0, side), was measured no faster overall: refine's
+    // single-lane walks slow down by as much as the overlap saves)
     timed(c, "prune", st, [&] { launch_prune(D, -1, st); }, 3);
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",

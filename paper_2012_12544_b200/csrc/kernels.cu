@@ -411,9 +411,18 @@ __device__ int64_t est_rep(const BatchDev& B, uint64_t h) {
     return (int64_t)((1u << 22) - 1) - (int64_t)(B.pbest[slot] & ((1ull << 22) - 1));
 }
 
-__global__ void k_prune_key(BatchDev B) {
+// 1: the candidate's plan is the refined plan (it must wait for refine); 0:
+// N = 1, InfeasibleShape or a comm-bottleneck M slot (coarse plan)
+__device__ __forceinline__ int prune_path(const BatchDev& B, int64_t ci) {
+    const int qi = B.cq[ci];
+    const QDesc Q = B.q[qi];
+    if (Q.N < 2 || B.qs[qi].dp_shape) return 0;
+    return B.ms[Q.mslot_off + (ci - Q.cand_off) % Q.nbase].bott ? 0 : 1;
+}
+
+__global__ void k_prune_key(BatchDev B, int pass) {
     const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (ci >= B.ncand) return;
+    if (ci >= B.ncand || (pass >= 0 && prune_path(B, ci) != pass)) return;
     uint64_t h;
     int32_t coarse;
     const bool ok = est_key_of(B, ci, h, coarse);
@@ -441,7 +450,7 @@ __global__ void k_prune(BatchDev B, int pass) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B.ncand) return;
     const int64_t ci = B.cperm[i];
-    if (B.cand[ci].status != C_PENDING) return;
+    if (B.cand[ci].status != C_PENDING || (pass >= 0 && prune_path(B, ci) != pass)) return;
     if (B.cs[ci].pshare) {
         uint64_t h;
         int32_t coarse;
@@ -451,11 +460,11 @@ __global__ void k_prune(BatchDev B, int pass) {
     count_prune(B, ci);
 }
 
-__global__ void k_prune_members(BatchDev B) {
+__global__ void k_prune_members(BatchDev B, int pass) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B.ncand) return;
     const int64_t ci = B.cperm[i];
-    if (!B.cs[ci].pshare) return;
+    if (!B.cs[ci].pshare || (pass >= 0 && prune_path(B, ci) != pass)) return;
     uint64_t h;
     int32_t coarse;
     // representatives were pruned by k_prune: their status is no longer pending
@@ -684,13 +693,18 @@ void launch_refine(const BatchDev& B, int sms, cudaStream_t st) {
     k_refine_list<<<blocks(B.nq, 128), 128, 0, st>>>(B);
     k_refine_smem<<<sms * 32, 32, bytes, st>>>(B, B.max_N);
 }
-void launch_prune(const BatchDev& B, int pass, cudaStream_t st) {
-    if (!B.ncand) return;
+void launch_prune_reset(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.pkey, 0, ((size_t)B.pmask + 1) * sizeof(unsigned long long), st);
     cudaMemsetAsync(B.pbest, 0, ((size_t)B.pmask + 1) * sizeof(unsigned long long), st);
-    k_prune_key<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
+}
+
+// pass -1: all candidates (after launch_prune_reset); 0 / 1: the coarse-path /
+// refined-path candidates only (both after one launch_prune_reset)
+void launch_prune(const BatchDev& B, int pass, cudaStream_t st) {
+    if (!B.ncand) return;
+    k_prune_key<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
     k_prune<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
-    k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
+    k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
 }
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);

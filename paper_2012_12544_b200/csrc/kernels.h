@@ -22,6 +22,7 @@ void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
 void launch_refine(const BatchDev& B, int sms, cudaStream_t st);
 void launch_prune(const BatchDev& B, int pass, cudaStream_t st);
+void launch_prune_reset(const BatchDev& B, cudaStream_t st);
 void launch_sim_prep(const BatchDev& B, cudaStream_t st);
 void launch_sim_share(const BatchDev& B, cudaStream_t st);
 void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st);
