@@ -26,7 +26,11 @@ namespace bpk {
 
 namespace {
 
-constexpr int FLOW_Q = 8;   // FIFO slots per link and direction
+// FIFO slots per link and direction.  A producer runs at most a few ops ahead
+// of its consumer (their warm-up depths differ by 1 or 2), and a full FIFO
+// only makes it wait a round; 4 slots halve the shared memory of 8 and let
+// twice as many candidates share an SM.
+constexpr int FLOW_Q = 4;
 
 template <int NT>
 struct FlowSmem {
@@ -169,8 +173,8 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
 }  // namespace
 
 void launch_sim_flow(const BatchDev& B, int k, int sms, cudaStream_t st) {
-    if (k == 0) k_sim_flow<32><<<sms * 24, 32, 0, st>>>(B, SIM_FLOW);
-    else k_sim_flow<64><<<sms * 12, 64, 0, st>>>(B, SIM_FLOW + 1);
+    if (k == 0) k_sim_flow<32><<<sms * 32, 32, 0, st>>>(B, SIM_FLOW);
+    else k_sim_flow<64><<<sms * 24, 64, 0, st>>>(B, SIM_FLOW + 1);
 }
 
 }  // namespace bpk
