@@ -298,7 +298,8 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
            o_qW = L.take<Rat>(nqst), o_qT = L.take<Rat>(nqst);
     size_t o_qd = L.take<uint8_t>(nqst);
     size_t o_clo = L.take<int32_t>(ns), o_chi = L.take<int32_t>(ns);
-    size_t o_sF = L.take<Rat>(ns), o_sB = L.take<Rat>(ns), o_sW = L.take<Rat>(ns), o_sM = L.take<Rat>(ns);
+    size_t o_sF = L.take<Rat>(ns), o_sB = L.take<Rat>(ns), o_sW = L.take<Rat>(ns), o_sM = L.take<Rat>(ns),
+           o_sM0 = L.take<Rat>(ns);
     size_t o_sA = L.take<int64_t>(ns), o_sSR = L.take<int64_t>(ns);
     size_t o_sim = L.take<char>(sim_exact_state_bytes(c->sm_count, std::max(1, hb.max_N)));
     size_t o_xkey = L.take<int32_t>(nc), o_xsorted = L.take<int32_t>(nc), o_xhist = L.take<int32_t>(XBUCKETS + 1);
@@ -312,6 +313,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     while (stab < 2 * std::max<int64_t>(1, hb.ncand)) stab <<= 1;
     size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
     size_t o_rlist = L.take<int32_t>(nqs), o_rcount = L.take<int32_t>(1);
+    size_t o_plist = L.take<int32_t>(nc), o_pctr = L.take<int32_t>(2);
     size_t o_pkey = L.take<unsigned long long>((size_t)stab), o_pbest = L.take<unsigned long long>((size_t)stab);
     int32_t ctab = 1;
     while (ctab < 2 * std::max<int64_t>(1, (int64_t)nms)) ctab <<= 1;
@@ -359,6 +361,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.sB = dptr<Rat>(b, o_sB);
     D.sW = dptr<Rat>(b, o_sW);
     D.sMem = dptr<Rat>(b, o_sM);
+    D.sMem0 = dptr<Rat>(b, o_sM0);
     D.sA = dptr<int64_t>(b, o_sA);
     D.sSR = dptr<int64_t>(b, o_sSR);
     D.simbuf = dptr<Rat>(b, o_sim);
@@ -383,6 +386,8 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.cmask = ctab - 1;
     D.rlist = dptr<int32_t>(b, o_rlist);
     D.rcount = dptr<int32_t>(b, o_rcount);
+    D.plist = dptr<int32_t>(b, o_plist);
+    D.pctr = dptr<int32_t>(b, o_pctr);
     D.pkey = dptr<unsigned long long>(b, o_pkey);
     D.pbest = dptr<unsigned long long>(b, o_pbest);
     D.pmask = stab - 1;
@@ -465,7 +470,10 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     // (pruning the coarse-path candidates on the side stream while refine runs,
     // launch_prune(D, 0, side), was measured no faster overall: refine's
     // single-lane walks slow down by as much as the overlap saves)
-    timed(c, "prune", st, [&] { launch_prune(D, -1, st); }, 3);
+    timed(c, "prune_list", st, [&] { launch_prune(D, -1, st, 1); }, 2);
+    timed(c, "prune", st, [&] { launch_prune(D, -1, st, 2); });
+    timed(c, "prune_members", st, [&] { launch_prune(D, -1, st, 4); });
+    timed(c, "prune_members_full", st, [&] { launch_prune(D, -1, st, 8); });
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
@@ -513,6 +521,8 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
             c->stats["refine"].work = (double)work[WORK_REFINE];
             c->stats["refine_critical_path"].work = (double)work[WORK_REFINE_MAX];
             c->stats["prune"].work = (double)work[WORK_PRUNE];
+            c->stats["prune_trials"].work = (double)work[WORK_PRUNE_TRIALS];
+            c->stats["prune_critical_path"].work = (double)work[WORK_PRUNE_MAX];
             for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work = (double)work[WORK_SIM_EVENTS + k];
         }
         collect(c);

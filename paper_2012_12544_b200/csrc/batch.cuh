@@ -67,7 +67,7 @@ constexpr int64_t FLOW_MIN_EVENTS = 1024;
 // refine: boundary steps evaluated (and the longest query's count: the serial
 // critical path); prune: candidate-stages estimated
 enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_REFINE = 2, WORK_PRUNE = 3, WORK_REFINE_MAX = 4,
-       WORK_SIM_EVENTS = 5, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
+       WORK_PRUNE_TRIALS = 5, WORK_PRUNE_MAX = 6, WORK_SIM_EVENTS = 7, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
 enum { XBUCKETS = 32768, XSIM_WARPS_PER_SM = 32 };
 
 // Per-candidate device state (beyond the bp_candidate output record).
@@ -79,6 +79,9 @@ struct CState {
     int32_t sim_rep;       // candidate whose identical simulation this one shares, -1 = none
     int32_t pshare;        // prune: first estimate may be shared (see k_prune_key)
     int32_t est_first;     // prune: 1 = first estimate feasible, 2 = it raised (shareable outcomes)
+    int32_t ft_trials;     // prune: memory_fine_tune trial moves (instrumentation)
+    int32_t mem0_from;     // prune member: representative whose first-estimate memory it starts from, -1 = none
+    int32_t mem0_buf;      // 0: that memory is in sMem (estimate was feasible), 1: in sMem0
 };
 
 // DP work item: a (query, a_th) pair; a_th < 0 = whole-layer partition.
@@ -109,6 +112,7 @@ struct BatchDev {
     int32_t *clo, *chi;
     // per-candidate estimate scratch (stage_off + local*N), 6 arrays
     Rat *sF, *sB, *sW, *sMem;
+    Rat* sMem0;               // first-estimate memory of infeasible prune-sharing candidates (null: none)
     int64_t *sA, *sSR;
     Rat* simbuf;              // exact simulator state, 9 Rats per stage slot
     int32_t* cq;              // candidate -> query
@@ -145,6 +149,8 @@ struct BatchDev {
     int32_t dedup;            // BP_OPT_DEDUP: share identical subproblems
     int32_t* rlist;           // [nq] queries to refine this run (compacted)
     int32_t* rcount;          // [1]
+    int32_t* plist;           // [ncand] candidates to prune this run (compacted)
+    int32_t* pctr;            // [2] list length, next chunk
     unsigned long long* pkey; // [pmask+1] estimate-input hashes (prune dedup)
     unsigned long long* pbest;// [pmask+1] max (capacity score, -index) per hash
     int32_t pmask;

@@ -428,6 +428,7 @@ __global__ void k_prune_key(BatchDev B, int pass) {
     const bool ok = est_key_of(B, ci, h, coarse);
     B.cs[ci].pshare = ok ? 1 : 0;
     B.cs[ci].est_first = 0;
+    B.cs[ci].mem0_from = -1;
     if (!ok) return;
     const uint64_t sc = est_score(B, ci);
     for (uint32_t slot = est_slot(B, h);; slot = (slot + 1) & (uint32_t)B.pmask) {
@@ -441,12 +442,21 @@ __global__ void k_prune_key(BatchDev B, int pass) {
 
 __device__ __forceinline__ void count_prune(const BatchDev& B, int64_t ci) {
     atomicAdd(&B.work[WORK_PRUNE], (unsigned long long)B.cand[ci].n_stages);
+    const unsigned long long t = (unsigned long long)B.cs[ci].ft_trials;
+    if (t) {
+        atomicAdd(&B.work[WORK_PRUNE_TRIALS], t);
+        atomicMax(&B.work[WORK_PRUNE_MAX], t * B.cand[ci].n_stages);
+    }
 }
 
 // representatives and unshareable candidates
 // (capping registers at 128 for 4 blocks per SM was measured slower: 27 vs
 // 22 ms on the C5 sweep)
-__global__ void k_prune(BatchDev B, int pass) {
+// Most candidates need no prune here (rejected earlier, or members deferred
+// to k_prune_members): the rest are compacted in scheduling order, and
+// persistent warps take chunks of 32 off a counter, so the few long ones do
+// not quantise the kernel into waves of mostly idle blocks.
+__global__ void k_prune_list(BatchDev B, int pass) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B.ncand) return;
     const int64_t ci = B.cperm[i];
@@ -456,8 +466,23 @@ __global__ void k_prune(BatchDev B, int pass) {
         int32_t coarse;
         if (est_key_of(B, ci, h, coarse) && est_rep(B, h) != ci) return;   // deferred to k_prune_members
     }
-    prune_candidate(B, ci, pass);
-    count_prune(B, ci);
+    B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;
+}
+
+__global__ void k_prune(BatchDev B, int pass) {
+    const int lane = threadIdx.x & 31;
+    const int count = B.pctr[0];
+    for (;;) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&B.pctr[1], 32);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= count) break;
+        if (base + lane < count) {
+            const int64_t ci = B.plist[base + lane];
+            prune_candidate(B, ci, pass);
+            count_prune(B, ci);
+        }
+    }
 }
 
 __global__ void k_prune_members(BatchDev B, int pass) {
@@ -480,22 +505,26 @@ __global__ void k_prune_members(BatchDev B, int pass) {
         rc = msr.bott ? (msr.crep >= 0 ? msr.crep : (int32_t)(Qr.mslot_off + mr)) : -1;
     }
     const int ef = B.cs[r].est_first;
-    if (ef != 0 && same_est(B, ci, r, coarse, rc)) {
+    if (same_est(B, ci, r, coarse, rc)) {
         bp_candidate& cd = B.cand[ci];
         const bp_candidate& rd = B.cand[r];
         if (ef == 2) {   // the estimate itself raised
             cd.status = rd.status;
             return;
         }
-        // copy the estimate and test this candidate's own capacities
+        // test this candidate's own capacities on the shared estimate's memory
         const QDesc Q = B.q[B.cq[ci]], Qr = B.q[B.cq[r]];
         const int N = Q.N;
         const int64_t so = Q.stage_off + (ci - Q.cand_off) * N, sr = Qr.stage_off + (r - Qr.cand_off) * N;
         const ChainView c = chain_view(B.P, Q.cl, N);
+        const Rat* mem = ef == 1 ? B.sMem + sr : B.sMem0 + sr;
         bool feasible = true;
         for (int s = 0; s < N; ++s)
-            if (rat_gt(B.sMem[sr + s], R(c.cap[s]))) feasible = false;
-        if (feasible) {
+            if (rat_gt(mem[s], R(c.cap[s]))) feasible = false;
+        if (!feasible) {   // memory fine-tune from the shared estimate
+            B.cs[ci].mem0_from = (int32_t)r;
+            B.cs[ci].mem0_buf = ef == 1 ? 0 : 1;
+        } else if (ef == 1) {   // copy the estimate
             for (int s = 0; s < N; ++s) {
                 B.sF[so + s] = B.sF[sr + s];
                 B.sB[so + s] = B.sB[sr + s];
@@ -517,8 +546,7 @@ __global__ void k_prune_members(BatchDev B, int pass) {
             return;
         }
     }
-    prune_candidate(B, ci);
-    count_prune(B, ci);
+    B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;   // pruned by the second k_prune
 }
 
 __global__ void k_rank(BatchDev B) {
@@ -700,11 +728,27 @@ void launch_prune_reset(const BatchDev& B, cudaStream_t st) {
 
 // pass -1: all candidates (after launch_prune_reset); 0 / 1: the coarse-path /
 // refined-path candidates only (both after one launch_prune_reset)
-void launch_prune(const BatchDev& B, int pass, cudaStream_t st) {
+void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part) {
     if (!B.ncand) return;
-    k_prune_key<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
-    k_prune<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
-    k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
+    static int grid = 0;
+    if (!grid) {   // persistent: fill every SM to its register-limited occupancy
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune, 32, 0);
+        grid = sms * (per_sm > 0 ? per_sm : 1);
+    }
+    if (part & 1) {
+        k_prune_key<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
+        cudaMemsetAsync(B.pctr, 0, 2 * sizeof(int32_t), st);
+        k_prune_list<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
+    }
+    if (part & 2) k_prune<<<grid, 32, 0, st>>>(B, pass);
+    if (part & 4) {
+        cudaMemsetAsync(B.pctr, 0, 2 * sizeof(int32_t), st);
+        k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
+    }
+    if (part & 8) k_prune<<<grid, 32, 0, st>>>(B, -1);
 }
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);

@@ -21,7 +21,9 @@ void launch_coarse_copy(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
 void launch_refine(const BatchDev& B, int sms, cudaStream_t st);
-void launch_prune(const BatchDev& B, int pass, cudaStream_t st);
+// part: bit 0 = keys + work list, bit 1 = representatives, bit 2 = members (copy
+// the shared estimate, or list), bit 3 = the listed members
+void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part = 15);
 void launch_prune_reset(const BatchDev& B, cudaStream_t st);
 void launch_sim_prep(const BatchDev& B, cudaStream_t st);
 void launch_sim_share(const BatchDev& B, cudaStream_t st);

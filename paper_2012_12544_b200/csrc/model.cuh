@@ -52,6 +52,7 @@ struct EstOut {
     int worst;          // first index of the maximal overload
     Rat peak_mem;       // max_i(features_i + weights_i) (explorer.hpp:405-408)
     Rat max_bw;         // max bandwidth demand (explorer.hpp:409-410)
+    int trials = 0;     // memory_fine_tune trial moves (instrumentation)
 };
 
 // Optional per-stage outputs (features, weights, bw demand), may be null.
@@ -329,6 +330,118 @@ BPK_HDNI int validate_frac(const int32_t* lo, const int32_t* hi, const Rat* lead
 // FT_NOCONV; errors go to e.
 enum { FT_OK = 0, FT_REJ = 3, FT_NOCONV = 4 };
 
+// Once memory_fine_tune has collapsed the plan to whole layers, every Rat its
+// trial estimates form is an integer (sums of layer costs, products with
+// integers, quotients that are only compared).  ft_int_ok bounds all of them
+// for this candidate from the network totals (costs, weights and activations
+// are >= 0, fp/bp >= 1: profiles.hpp:83-98), so that none can leave int64:
+//   features + weights of a stage  <= 2 N amax micro + 2 W_total
+//   total overload                 <= N * that
+//   minibatch_time, bubble_fraction terms <= (M + N)(F_tot + B_tot) + 4 (M + N) amax micro
+// (bandwidth demands a / Fm, 2a / (Fm + Bm) are quotients of such integers,
+// Fm >= 1).  Under the bound the reference's trials cannot raise, so they can
+// be decided with int64 arithmetic (fine_tune_int).
+BPK_HD bool ft_int_ok(const NetView& v, const ChainView& c, int64_t M, int64_t micro) {
+    const int N = c.N;
+    if (micro < 0 || M < 1 || v.L < 1) return false;
+    int64_t amax = v.a[v.L - 1];
+    if (v.L >= 2 && v.asort[v.L - 2] > amax) amax = v.asort[v.L - 2];   // asort: first L-1, ascending
+    int64_t ft = 0, bt = 0;
+    for (int s = 0; s < N; ++s) {
+        const int64_t o = (int64_t)c.type[s] * (v.L + 1) + v.L;
+        if (v.Pfp[o] > ft) ft = v.Pfp[o];
+        if (v.Pbp[o] > bt) bt = v.Pbp[o];
+    }
+    const i128 lim = (i128)1 << 61;
+    const i128 A = (i128)amax * micro;
+    if (amax < 0 || A >= lim) return false;
+    const i128 mem = 2 * (i128)N * A + 2 * (i128)v.Pw[v.L];
+    if ((i128)N * mem >= lim) return false;
+    return (i128)(M + N) * ((i128)ft + bt) + 4 * (i128)(M + N) * A < lim;
+}
+
+// memory_fine_tune's trial loop (partition.hpp:375-433) under ft_int_ok: the
+// same moves, in the same order, accepted on the same comparisons, but only
+// the values a decision reads are formed -- stage i0/i1 costs, the overloads,
+// and on a non-relaxed improvement max(F + B) against the link times.  The
+// accepted plan's full estimate is then recomputed exactly.
+BPK_HDNI int fine_tune_int(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, int32_t* lo,
+                           int32_t* hi, const EstScratch& s, EstOut& o, Err& e, int64_t total, int worst,
+                           int limit) {
+    const int N = c.N;
+    const int64_t fmul = (kind == KIND_FBP || kind == KIND_SO) ? 2 : 1;
+    WholePlan wp{&v, &c, lo, hi};
+    int guard = 0, trials = 0;
+    while (total > 0) {
+        if (++guard > limit) { o.trials = trials; return FT_NOCONV; }
+        int cn[2], cd[2], nc = 0;
+        if (worst > 0) { cn[nc] = worst - 1; cd[nc] = -1; ++nc; }
+        if (worst < N - 1) { cn[nc] = worst + 1; cd[nc] = +1; ++nc; }
+        if (nc == 2 && c.cap[worst + 1] - s.Mem[worst + 1].n > c.cap[worst - 1] - s.Mem[worst - 1].n) {
+            int t = cn[0]; cn[0] = cn[1]; cn[1] = t;
+            t = cd[0]; cd[0] = cd[1]; cd[1] = t;
+        }
+        bool moved = false;
+        for (int relax = 0; relax < 2 && !moved; ++relax) {
+            for (int ci = 0; ci < nc; ++ci) {
+                if (lo[worst] == hi[worst]) continue;
+                const int nb = cn[ci];
+                const int32_t sw_lo = lo[worst], sw_hi = hi[worst], sn_lo = lo[nb], sn_hi = hi[nb];
+                if (cd[ci] < 0) { lo[worst] += 1; hi[nb] += 1; }
+                else { hi[worst] -= 1; lo[nb] -= 1; }
+                const int i0 = worst < nb ? worst : nb, i1 = i0 + 1;
+                const Rat kF[2] = {s.F[i0], s.F[i1]}, kB[2] = {s.B[i0], s.B[i1]}, kW[2] = {s.W[i0], s.W[i1]},
+                          kM[2] = {s.Mem[i0], s.Mem[i1]};
+                const int64_t kA[3] = {s.A[0], s.A[i1], s.SR[i1]};
+                for (int i = i0; i <= i1; ++i) {           // stage_costs (cost_models.hpp:103-119)
+                    wp.FBW(i, s.F[i], s.B[i], s.W[i], e);
+                    if (i == i1 || i == 0) {
+                        const int64_t act = (i >= 1) ? act_at(v, wp.H(i - 1), e) : act_at(v, wp.H(0), e);
+                        s.A[i] = act * micro;
+                        if (i >= 1) s.SR[i] = link_sr(wp, v, c, i - 1, micro, e);
+                    }
+                    if (e.bad()) return FT_OK;
+                    s.Mem[i] = R((int64_t)(N - i) * s.A[i] * fmul + 2 * s.W[i].n);
+                }
+                ++trials;
+                int64_t tot = 0, wo = 0;
+                int wi = 0;
+                for (int i = 0; i < N; ++i) {                  // overloads (partition.hpp:344-356, 381-383)
+                    const int64_t ov = s.Mem[i].n > c.cap[i] ? s.Mem[i].n - c.cap[i] : 0;
+                    tot += ov;
+                    if (i == 0 || ov > wo) { wo = ov; wi = i; }
+                }
+                bool ok = tot < total;
+                if (ok && !relax) {
+                    int64_t target = 0;                         // max_stage_compute_time
+                    for (int n = 0; n < N; ++n) {
+                        const int64_t t = s.F[n].n + s.B[n].n;
+                        if (t > target) target = t;
+                    }
+                    for (int k = 0; k + 1 < N; ++k)             // detect_comm_bottleneck
+                        if (s.SR[k + 1] > target) ok = false;
+                }
+                if (ok) {
+                    total = tot;
+                    worst = wi;
+                    moved = true;
+                    break;
+                }
+                lo[worst] = sw_lo; hi[worst] = sw_hi; lo[nb] = sn_lo; hi[nb] = sn_hi;
+                s.F[i0] = kF[0]; s.F[i1] = kF[1];
+                s.B[i0] = kB[0]; s.B[i1] = kB[1];
+                s.W[i0] = kW[0]; s.W[i1] = kW[1];
+                s.Mem[i0] = kM[0]; s.Mem[i1] = kM[1];
+                s.A[0] = kA[0]; s.A[i1] = kA[1]; s.SR[i1] = kA[2];
+            }
+        }
+        if (!moved) { o.trials = trials; return FT_REJ; }
+    }
+    o.trials = trials;
+    if (trials) estimate(wp, v, c, kind, M, micro, s, o, nullptr, e);
+    return FT_OK;
+}
+
 BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
                                 int32_t* lo, int32_t* hi, const Rat* frac_lead, const Rat* frac_trail,
                                 const EstScratch& s, EstOut& o, Err& e) {
@@ -351,9 +464,11 @@ BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, in
     int worst = o.worst;
     int guard = 0, trials = 0;
     const int limit = 8 * (int)((int64_t)N * v.L + 4);
+    if (total.d == 1 && ft_int_ok(v, c, M, micro))
+        return fine_tune_int(v, c, kind, M, micro, lo, hi, s, o, e, total.n, worst, limit);
     const Rat zero{0, 1};
     while (rat_gt(total, zero)) {
-        if (++guard > limit) return FT_NOCONV;
+        if (++guard > limit) { o.trials = trials; return FT_NOCONV; }
         int cn[2], cd[2], nc = 0;
         if (worst > 0) { cn[nc] = worst - 1; cd[nc] = -1; ++nc; }
         if (worst < N - 1) { cn[nc] = worst + 1; cd[nc] = +1; ++nc; }
@@ -416,10 +531,11 @@ BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, in
                 s.A[0] = kA[0]; s.A[i1] = kA[1]; s.SR[i1] = kA[2];
             }
         }
-        if (!moved) return FT_REJ;
+        if (!moved) { o.trials = trials; return FT_REJ; }
     }
     // the accepted plan's full estimate (the bandwidth demands were not
     // formed during the trials; same values, no new errors)
+    o.trials = trials;
     if (trials) estimate(wp, v, c, kind, M, micro, s, o, nullptr, e);
     return FT_OK;
 }

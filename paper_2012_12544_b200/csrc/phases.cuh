@@ -252,6 +252,26 @@ BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci, int pass = -1) {
     EstOut o;
     int plan_kind = PLAN_WHOLE;
     int ft = FT_OK;
+    // A prune-sharing member whose representative's first estimate (same
+    // inputs, hence same values and no error) is infeasible for it starts
+    // from that estimate's memory (k_prune_members); memory_fine_tune reads
+    // nothing else of it.  Representatives keep theirs for the members.
+    const Rat* mem0 = nullptr;
+    if (cs.pshare && cs.mem0_from >= 0) {
+        const QDesc Qr = B.q[B.cq[cs.mem0_from]];
+        mem0 = (cs.mem0_buf ? B.sMem0 : B.sMem) + Qr.stage_off + (cs.mem0_from - Qr.cand_off) * N;
+    }
+    auto first_estimate = [&](const auto& plan) {
+        if (mem0) {
+            for (int s = 0; s < N; ++s) S.Mem[s] = mem0[s];
+            o.feasible = 0;
+        } else {
+            estimate(plan, v, c, kind, M, micro, S, o, nullptr, e);
+            if (cs.pshare && B.sMem0 && !e.bad() && !o.feasible)
+                for (int s = 0; s < N; ++s) B.sMem0[slot + s] = S.Mem[s];
+        }
+        cs.est_first = e.bad() ? 2 : o.feasible ? 1 : 0;
+    };
     if (N == 1) {                                                  // 447-451
         lo[0] = 1;
         hi[0] = (int32_t)v.L;
@@ -267,16 +287,12 @@ BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci, int pass = -1) {
         if (ms.bott) {                                             // 456-467
             if (ms.err) { cd.status = status_of_err(ms.err); return; }
             if (ms.K < N) { cd.status = BP_C_REJ_COARSEN; cd.detail = ms.K; return; }
-            WholePlan wp{&v, &c, lo, hi};
-            estimate(wp, v, c, kind, M, micro, S, o, nullptr, e);
-            cs.est_first = e.bad() ? 2 : o.feasible ? 1 : 0;
+            first_estimate(WholePlan{&v, &c, lo, hi});
             if (!e.bad()) ft = memory_fine_tune(v, c, kind, M, micro, lo, hi, nullptr, nullptr, S, o, e);
         } else {                                                   // 469-473
             if (qs.refine_err) { cd.status = status_of_err(qs.refine_err); return; }
             const int64_t qo = Q.qstage_off;
-            CachedPlan cp{B.qhi + qo, B.qF + qo, B.qB + qo, B.qW + qo};
-            estimate(cp, v, c, kind, M, micro, S, o, nullptr, e);
-            cs.est_first = e.bad() ? 2 : o.feasible ? 1 : 0;
+            first_estimate(CachedPlan{B.qhi + qo, B.qF + qo, B.qB + qo, B.qW + qo});
             if (!e.bad() && !o.feasible) {
                 for (int s = 0; s < N; ++s) { lo[s] = B.qlo[qo + s]; hi[s] = B.qhi[qo + s]; }
                 ft = memory_fine_tune(v, c, kind, M, micro, lo, hi, B.qlead + qo, B.qtrail + qo, S, o, e);
@@ -285,6 +301,7 @@ BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci, int pass = -1) {
             }
         }
     }
+    cs.ft_trials = o.trials;
     if (e.bad()) { fail(cd, e); return; }
     if (ft == FT_REJ) { cd.status = BP_C_REJ_FINETUNE; return; }
     if (ft == FT_NOCONV) { cd.status = BP_C_REJ_FINETUNE_NOCONV; return; }
