@@ -312,7 +312,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     int32_t stab = 1;
     while (stab < 2 * std::max<int64_t>(1, hb.ncand)) stab <<= 1;
     size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
-    size_t o_rlist = L.take<int32_t>(nqs), o_rcount = L.take<int32_t>(1);
+    size_t o_rlist = L.take<int32_t>(nqs), o_rcount = L.take<int32_t>(2);
     size_t o_plist = L.take<int32_t>(nc), o_pctr = L.take<int32_t>(2);
     size_t o_pkey = L.take<unsigned long long>((size_t)stab), o_pbest = L.take<unsigned long long>((size_t)stab);
     int32_t ctab = 1;
@@ -521,6 +521,8 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
             c->stats["refine"].work = (double)work[WORK_REFINE];
             c->stats["refine_critical_path"].work = (double)work[WORK_REFINE_MAX];
             c->stats["prune"].work = (double)work[WORK_PRUNE];
+            c->stats["refine_moves"].work = (double)work[WORK_REFINE_MOVES];
+            c->stats["refine_exact_steps"].work = (double)work[WORK_REFINE_EXACT];
             c->stats["prune_trials"].work = (double)work[WORK_PRUNE_TRIALS];
             c->stats["prune_critical_path"].work = (double)work[WORK_PRUNE_MAX];
             for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work = (double)work[WORK_SIM_EVENTS + k];

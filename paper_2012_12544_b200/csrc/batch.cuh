@@ -67,7 +67,8 @@ constexpr int64_t FLOW_MIN_EVENTS = 1024;
 // refine: boundary steps evaluated (and the longest query's count: the serial
 // critical path); prune: candidate-stages estimated
 enum { WORK_DP_WHOLE = 0, WORK_DP_COARSE = 1, WORK_REFINE = 2, WORK_PRUNE = 3, WORK_REFINE_MAX = 4,
-       WORK_PRUNE_TRIALS = 5, WORK_PRUNE_MAX = 6, WORK_SIM_EVENTS = 7, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
+       WORK_PRUNE_TRIALS = 5, WORK_PRUNE_MAX = 6, WORK_REFINE_MOVES = 7, WORK_REFINE_EXACT = 8,
+       WORK_SIM_EVENTS = 9, WORK_SLOTS = WORK_SIM_EVENTS + SIM_CLASSES };
 enum { XBUCKETS = 32768, XSIM_WARPS_PER_SM = 32 };
 
 // Per-candidate device state (beyond the bp_candidate output record).
@@ -148,7 +149,7 @@ struct BatchDev {
     int32_t cmask;
     int32_t dedup;            // BP_OPT_DEDUP: share identical subproblems
     int32_t* rlist;           // [nq] queries to refine this run (compacted)
-    int32_t* rcount;          // [1]
+    int32_t* rcount;          // [2] list length, next entry
     int32_t* plist;           // [ncand] candidates to prune this run (compacted)
     int32_t* pctr;            // [2] list length, next chunk
     unsigned long long* pkey; // [pmask+1] estimate-input hashes (prune dedup)

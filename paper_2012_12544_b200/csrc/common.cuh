@@ -129,8 +129,7 @@ BPK_HD bool kind_async(int kind) { return kind == KIND_AS || kind == KIND_FBP; }
 // whether any of them overflows; its reduced denominator is that of
 // lead * v_lo (adding integers keeps the denominator).
 //   P: prefix sums of v over layers (P[j] = v_1 + ... + v_j).
-BPK_HDNI Rat stage_sum_frac(int64_t lo, int64_t hi, Rat lead, Rat trail,
-                                              const int64_t* P, Err& e) {
+BPK_HD Rat stage_sum_frac_body(int64_t lo, int64_t hi, Rat lead, Rat trail, const int64_t* P, Err& e) {
     if (lo > hi) return Rat{0, 1};
     if (lo == hi) {
         Rat own = rat_sub(rat_add(lead, trail, e), R(1), e);
@@ -145,6 +144,17 @@ BPK_HDNI Rat stage_sum_frac(int64_t lo, int64_t hi, Rat lead, Rat trail,
     }
     Rat th = rat_mul(trail, R(P[hi] - P[hi - 1]), e);
     return rat_add(t, th, e);
+}
+// out of line, error by value (see RatE in rat.cuh)
+BPK_HDNI RatE stage_sum_frac_v(int64_t lo, int64_t hi, Rat lead, Rat trail, const int64_t* P) {
+    Err e{ERR_NONE};
+    const Rat r = stage_sum_frac_body(lo, hi, lead, trail, P, e);
+    return RatE{r, e.code};
+}
+BPK_HD Rat stage_sum_frac(int64_t lo, int64_t hi, Rat lead, Rat trail, const int64_t* P, Err& e) {
+    const RatE x = stage_sum_frac_v(lo, hi, lead, trail, P);
+    if (x.err) e.set(x.err);
+    return x.r;
 }
 
 // Whole-layer stage (fractions 1): plain prefix difference.  Partial sums are

@@ -332,12 +332,16 @@ __global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm) {
     sc.lo = reinterpret_cast<int32_t*>(sc.tT + nm);
     sc.hi = sc.lo + nm;
     sc.dirty = reinterpret_cast<uint8_t*>(sc.hi + nm);
-    const int count = *B.rcount;
-    for (int i = blockIdx.x; i < count; i += gridDim.x) {
+    const int count = B.rcount[0];
+    // dynamic: the list is heaviest-first (scheduling order), so a warp that
+    // finishes early takes the next query instead of a fixed stride's
+    for (int i = atomicAdd(&B.rcount[1], 1); i < count; i = atomicAdd(&B.rcount[1], 1)) {
         const int qi = B.rlist[i];
         refine_query_at(B, qi, &sc);
         atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
         atomicMax(&B.work[WORK_REFINE_MAX], (unsigned long long)B.qs[qi].refine_evals);
+        atomicAdd(&B.work[WORK_REFINE_MOVES], (unsigned long long)B.qs[qi].refine_moves);
+        atomicAdd(&B.work[WORK_REFINE_EXACT], (unsigned long long)B.qs[qi].refine_exact);
     }
 }
 
@@ -717,7 +721,7 @@ void launch_refine(const BatchDev& B, int sms, cudaStream_t st) {
         cudaFuncSetAttribute(k_refine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         attr = bytes;
     }
-    cudaMemsetAsync(B.rcount, 0, sizeof(int32_t), st);
+    cudaMemsetAsync(B.rcount, 0, 2 * sizeof(int32_t), st);
     k_refine_list<<<blocks(B.nq, 128), 128, 0, st>>>(B);
     k_refine_smem<<<sms * 32, 32, bytes, st>>>(B, B.max_N);
 }

@@ -12,6 +12,11 @@
 
 namespace bpk {
 
+struct IntE {
+    int r;
+    uint32_t err;
+};
+
 // ---------------------------------------------------------------------------
 // Plan sources for estimate(): per-stage F, B, W and the stage's hi.
 struct WholePlan {          // fractions all 1 (DP / coarse / fine-tuned plans)
@@ -103,7 +108,7 @@ BPK_HD int64_t link_sr(const PS& p, const NetView& v, const ChainView& c, int k0
 
 // estimate(kind, plan, net, cluster, M, micro), cost_models.hpp:124-166.
 template <class PS>
-BPK_HDNI void estimate(const PS& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
+BPK_HD void estimate_body(const PS& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
                          const EstScratch& s, EstOut& o, const EstStageOut* so, Err& e) {
     const int N = c.N;
     // stage_costs (103-119), stage order F, B, w, a, SR
@@ -161,6 +166,16 @@ BPK_HDNI void estimate(const PS& p, const NetView& v, const ChainView& c, int ki
     }
 }
 
+// out of line; the error latch travels by value (see RatE in rat.cuh)
+template <class PS>
+BPK_HDNI uint32_t estimate_v(const PS& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, const EstScratch& s, EstOut& o, const EstStageOut* so, uint32_t ecode) {
+    Err e{ecode};
+    estimate_body(p, v, c, kind, M, micro, s, o, so, e);
+    return e.code;
+}
+template <class PS>
+BPK_HD void estimate(const PS& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, const EstScratch& s, EstOut& o, const EstStageOut* so, Err& e) { e.code = estimate_v(p, v, c, kind, M, micro, s, o, so, e.code); }
+
 // estimate() of a whole-layer plan that differs from the one whose estimate
 // is in s / o only in the adjacent stages i0 < i1 (a memory_fine_tune trial
 // move, partition.hpp:403-410).  The reference recomputes the whole estimate
@@ -171,7 +186,7 @@ BPK_HDNI void estimate(const PS& p, const NetView& v, const ChainView& c, int ki
 // per-link bandwidth demands a / Fm (or 2a / (Fm + Bm) for fbp-as) cannot
 // leave int64 once 2a and Fm + Bm fit: they are not formed during trials
 // (o.max_bw is left stale; the caller recomputes it for the final plan).
-BPK_HDNI void estimate_move(const WholePlan& p, const NetView& v, const ChainView& c, int kind, int64_t M,
+BPK_HD void estimate_move_body(const WholePlan& p, const NetView& v, const ChainView& c, int kind, int64_t M,
                             int64_t micro, const EstScratch& s, EstOut& o, int i0, int i1, Err& e) {
     const int N = c.N;
     const bool dbl = (kind == KIND_FBP || kind == KIND_SO);
@@ -227,6 +242,14 @@ BPK_HDNI void estimate_move(const WholePlan& p, const NetView& v, const ChainVie
         for (int k = 0; k + 1 < N; ++k) (void)rat_mul(R(2), R(s.A[k + 1]), e);
     }
 }
+
+// out of line; the error latch travels by value (see RatE in rat.cuh)
+BPK_HDNI uint32_t estimate_move_v(const WholePlan& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, const EstScratch& s, EstOut& o, int i0, int i1, uint32_t ecode) {
+    Err e{ecode};
+    estimate_move_body(p, v, c, kind, M, micro, s, o, i0, i1, e);
+    return e.code;
+}
+BPK_HD void estimate_move(const WholePlan& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, const EstScratch& s, EstOut& o, int i0, int i1, Err& e) { e.code = estimate_move_v(p, v, c, kind, M, micro, s, o, i0, i1, e.code); }
 
 // overloads() bookkeeping (partition.hpp:344-356) on the estimate in s.Mem:
 // ov = mem > cap ? mem - cap : 0; total += ov; worst = first max (381-383).
@@ -365,7 +388,7 @@ BPK_HD bool ft_int_ok(const NetView& v, const ChainView& c, int64_t M, int64_t m
 // the values a decision reads are formed -- stage i0/i1 costs, the overloads,
 // and on a non-relaxed improvement max(F + B) against the link times.  The
 // accepted plan's full estimate is then recomputed exactly.
-BPK_HDNI int fine_tune_int(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, int32_t* lo,
+BPK_HD int fine_tune_int(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, int32_t* lo,
                            int32_t* hi, const EstScratch& s, EstOut& o, Err& e, int64_t total, int worst,
                            int limit) {
     const int N = c.N;
@@ -442,9 +465,9 @@ BPK_HDNI int fine_tune_int(const NetView& v, const ChainView& c, int kind, int64
     return FT_OK;
 }
 
-BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
-                                int32_t* lo, int32_t* hi, const Rat* frac_lead, const Rat* frac_trail,
-                                const EstScratch& s, EstOut& o, Err& e) {
+BPK_HD int memory_fine_tune_body(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
+                                 int32_t* lo, int32_t* hi, const Rat* frac_lead, const Rat* frac_trail,
+                                 const EstScratch& s, EstOut& o, Err& e) {
     const int N = c.N;
     overloads_from_mem(c, s, o, e);                        // first overloads() (357)
     if (e.bad()) return FT_OK;
@@ -540,6 +563,22 @@ BPK_HDNI int memory_fine_tune(const NetView& v, const ChainView& c, int kind, in
     return FT_OK;
 }
 
+// out of line; the error latch travels by value (see RatE in rat.cuh)
+BPK_HDNI IntE memory_fine_tune_v(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, int32_t* lo,
+                                 int32_t* hi, const Rat* frac_lead, const Rat* frac_trail, const EstScratch& s,
+                                 EstOut& o, uint32_t ecode) {
+    Err e{ecode};
+    const int r = memory_fine_tune_body(v, c, kind, M, micro, lo, hi, frac_lead, frac_trail, s, o, e);
+    return IntE{r, e.code};
+}
+BPK_HD int memory_fine_tune(const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro, int32_t* lo,
+                            int32_t* hi, const Rat* frac_lead, const Rat* frac_trail, const EstScratch& s, EstOut& o,
+                            Err& e) {
+    const IntE x = memory_fine_tune_v(v, c, kind, M, micro, lo, hi, frac_lead, frac_trail, s, o, e.code);
+    e.code = x.err;
+    return x.r;
+}
+
 // ---------------------------------------------------------------------------
 // intra_layer_refine (partition.hpp:248-333) on one query's plan.
 // lo/hi/lead/trail: the plan (in/out).  tF/tB/tT: per-stage fp, bp and
@@ -573,7 +612,8 @@ BPK_HD Rat reduce_pos(i128 n, i128 d) {       // n >= 0, d > 0, both < 2^62
 // Every product below is formed from two int64 factors already checked
 // against 2^62 (64x64 -> 128-bit multiplies only: a 128x128 product is ~60
 // instructions and this step runs millions of times).
-BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh, Rat& nl) {
+BPK_HD int refine_fast_step_body(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh,
+                                 Rat& nl) {
     const i128 B62 = (i128)1 << 62;
     if (t_hi.n < 0 || t_lo.n < 0 || avail.n <= 0) return FS_FALLBACK;
     const uint64_t g = gcd_u64((uint64_t)t_hi.d, (uint64_t)t_lo.d);
@@ -599,7 +639,13 @@ BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, 
     if (x.d > 1024) {                                     // quantize (257-265)
         if ((i128)x.n * 1024 >= B62) return FS_FALLBACK;
         const int64_t num = x.n * 1024;
-        const int64_t k = num / x.d, kc = k + (num % x.d != 0 ? 1 : 0);
+        // k = floor(num / x.d) < 1024 (0 < x < avail <= 1): a double
+        // estimate, corrected exactly, instead of a 64-bit software divide
+        const uint64_t un = (uint64_t)num, ud = (uint64_t)x.d;
+        uint64_t uk = (uint64_t)((double)un / (double)ud);
+        while (uk * ud > un) --uk;
+        while ((uk + 1) * ud <= un) ++uk;
+        const int64_t k = (int64_t)uk, kc = k + (uk * ud != un ? 1 : 0);
         Err le{ERR_NONE};
         const Rat qlo = rat_nd(k, 1024, le), qhi = rat_nd(kc, 1024, le);
         if (rat_ge(qhi, avail)) {
@@ -629,12 +675,24 @@ BPK_HDNI int refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, 
     return FS_MOVE;
 }
 
+// out of line, results by value (see RatE in rat.cuh)
+struct StepOut {
+    int fs;
+    uint32_t err;
+    Rat x, nh, nl;
+};
+BPK_HDNI StepOut refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail) {
+    StepOut o{};
+    o.fs = refine_fast_step_body(t_hi, t_lo, c_from, c_to, avail, o.x, o.nh, o.nl);
+    return o;
+}
+
 // The reference's boundary step on exact Rats (partition.hpp:302-327), for
 // the steps refine_fast_step cannot bound; out of line so that the common
 // path's code stays small.  Returns FS_NOMOVE or FS_MOVE (errors go to e,
 // which the caller checks first).
-BPK_HDNI int refine_exact_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh,
-                               Rat& nl, Err& e) {
+BPK_HD int refine_exact_step_body(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh,
+                                  Rat& nl, Err& e) {
     const Rat zero{0, 1}, step{1, 1024};
     x = rat_div(rat_sub(t_hi, t_lo, e), rat_add(R(c_from), R(c_to), e), e);
     if (rat_ge(x, avail)) x = rat_sub(avail, step, e);
@@ -661,6 +719,13 @@ BPK_HDNI int refine_exact_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to,
     if (e.bad() || rat_ge(rat_max(nh, nl), t_hi)) return FS_NOMOVE;
     return FS_MOVE;
 }
+BPK_HDNI StepOut refine_exact_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail) {
+    StepOut o{};
+    Err e{ERR_NONE};
+    o.fs = refine_exact_step_body(t_hi, t_lo, c_from, c_to, avail, o.x, o.nh, o.nl, e);
+    o.err = e.code;
+    return o;
+}
 
 // True when recomputing the stage time from the plan (stage_fp_time +
 // stage_bp_time, plan.hpp:90-113) cannot overflow: every partial sum is at
@@ -669,8 +734,8 @@ BPK_HD bool stage_time_safe(Rat t, Rat lead, Rat trail) {
     return (i128)t.n * lead.d * trail.d < ((i128)1 << 62) * t.d;
 }
 
-BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail,
-                       Rat* tF, Rat* tB, Rat* tT, uint8_t* dirty, int64_t* stats, Err& e) {
+BPK_HD void refine_body(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail,
+                        Rat* tF, Rat* tB, Rat* tT, uint8_t* dirty, int64_t* stats, Err& e) {
     const int N = c.N;
     stats[0] = stats[1] = stats[2] = stats[3] = 0;   // iterations, evaluated steps, moves, exact steps
     if (N <= 1) return;
@@ -724,15 +789,15 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
                 else if (j == lo[from]) avail = lead[from];
                 else avail = trail[from];
                 if (e.bad()) return;
-                Rat x, nh, nl;
-                const int fs = refine_fast_step(t_hi, t_lo, c_from, c_to, avail, x, nh, nl);
-                if (fs == FS_NOMOVE) continue;
-                if (fs == FS_FALLBACK) {                   // the reference's Rat step, verbatim
+                StepOut st = refine_fast_step(t_hi, t_lo, c_from, c_to, avail);
+                if (st.fs == FS_NOMOVE) continue;
+                if (st.fs == FS_FALLBACK) {                // the reference's Rat step, verbatim
                     ++stats[3];
-                    const int xs = refine_exact_step(t_hi, t_lo, c_from, c_to, avail, x, nh, nl, e);
-                    if (e.bad()) return;
-                    if (xs == FS_NOMOVE) continue;
+                    st = refine_exact_step(t_hi, t_lo, c_from, c_to, avail);
+                    if (st.err) { e.set(st.err); return; }
+                    if (st.fs == FS_NOMOVE) continue;
                 }
+                const Rat x = st.x, nh = st.nh, nl = st.nl;
                 // apply_move (269-292)
                 int a = n0, b = n0 + 1;
                 if (dir > 0) {
@@ -768,6 +833,18 @@ BPK_HDNI void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t*
             }
         }
     }
+}
+
+// out of line with the error latch in a register (see RatE in rat.cuh)
+BPK_HDNI uint32_t refine_v(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail,
+                           Rat* tF, Rat* tB, Rat* tT, uint8_t* dirty, int64_t* stats, uint32_t ecode) {
+    Err e{ecode};
+    refine_body(v, c, lo, hi, lead, trail, tF, tB, tT, dirty, stats, e);
+    return e.code;
+}
+BPK_HD void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail, Rat* tF,
+                   Rat* tB, Rat* tT, uint8_t* dirty, int64_t* stats, Err& e) {
+    e.code = refine_v(v, c, lo, hi, lead, trail, tF, tB, tT, dirty, stats, e.code);
 }
 
 }  // namespace bpk

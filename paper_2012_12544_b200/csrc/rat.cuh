@@ -39,6 +39,14 @@ inline int bpk_ffs64(long long x) { return __builtin_ffsll(x); }
 
 namespace bpk {
 
+// host-only operation counters for the test emulator (tests/emu, BPK_OPSTATS)
+#if defined(BPK_OPSTATS) && !defined(__CUDA_ARCH__)
+extern unsigned long long bpk_opstats[16];
+#define BPK_COUNT(i) (++bpk_opstats[i])
+#else
+#define BPK_COUNT(i) ((void)0)
+#endif
+
 typedef __int128 i128;
 typedef unsigned __int128 u128;
 
@@ -65,6 +73,16 @@ struct Rat {
 
 BPK_HD Rat R(int64_t v) { return Rat{v, 1}; }
 
+// Out-of-line Rat operations return their error by value: an Err passed by
+// reference to a non-inlined function has to live in local memory, and every
+// error test in the caller's loops then became a local-memory load.  NAME_body
+// is the operation, inlined into the out-of-line NAME_v (where its Err is a
+// register); NAME is the inline wrapper applying the first-error-wins latch.
+struct RatE {
+    Rat r;
+    uint32_t err;
+};
+
 // ---- integer helpers ----------------------------------------------------
 // GPUs have no native 64-bit divide; the helpers below keep the common cases
 // (operands below 2^32, exact quotients) off the generic software routines.
@@ -73,9 +91,16 @@ BPK_HD int ctz32(uint32_t x) { return bpk_ffs64((long long)x) - 1; }
 BPK_HD uint32_t gcd_u32(uint32_t u, uint32_t v) {
     if (u == 0) return v;
     if (v == 0) return u;
+    // a power of two on either side (the 1/1024-quantized fractions of
+    // refine make these common): the gcd is the lowest set bit of u | v
+    const uint32_t o = u | v;
+    BPK_COUNT(0);
+    if ((u & (u - 1)) == 0 || (v & (v - 1)) == 0) return o & (0u - o);
+    BPK_COUNT(1);
     int shift = ctz32(u | v);
     u >>= ctz32(u);
     do {
+        BPK_COUNT(2);
         v >>= ctz32(v);
         uint32_t lo = u < v ? u : v, hi = u < v ? v : u;
         u = lo;
@@ -94,8 +119,8 @@ BPK_HD uint64_t umod64(uint64_t a, uint64_t b) {
 // correction in double (|r| < 2^53), then integer fix-ups.  The result is
 // exact whatever the reciprocal's rounding, so host and device agree.
 BPK_HD uint32_t umod_u64_u32(uint64_t x, uint32_t m) {
+    if ((m & (m - 1)) == 0) return m == 0 ? 0 : (uint32_t)x & (m - 1);
     if ((x >> 32) == 0) return (uint32_t)x % m;
-    if (m <= 1) return 0;
 #ifdef __CUDA_ARCH__
     const double rm = __drcp_rn((double)m);
 #else
@@ -115,14 +140,20 @@ BPK_HDNI uint64_t gcd_u64(uint64_t u, uint64_t v) {
     if (((u | v) >> 32) == 0) return gcd_u32((uint32_t)u, (uint32_t)v);
     if (u == 0) return v;
     if (v == 0) return u;
+    const uint64_t o = u | v;
+    BPK_COUNT(3);
+    if ((u & (u - 1)) == 0 || (v & (v - 1)) == 0) return o & (0ull - o);   // see gcd_u32
     if (u < v) { uint64_t t = u; u = v; v = t; }
+    BPK_COUNT(4);
     if ((v >> 32) == 0) {              // one Euclid step brings both below 2^32
         const uint32_t r = umod_u64_u32(u, (uint32_t)v);
         return r == 0 ? v : gcd_u32((uint32_t)v, r);
     }
+    BPK_COUNT(5);
     int shift = bpk_ffs64((long long)(u | v)) - 1;
     u >>= (bpk_ffs64((long long)u) - 1);
     do {
+        BPK_COUNT(6);
         v >>= (bpk_ffs64((long long)v) - 1);
         uint64_t lo = u < v ? u : v, hi = u < v ? v : u;
         u = lo;
@@ -136,6 +167,7 @@ BPK_HDNI uint64_t gcd_u64(uint64_t u, uint64_t v) {
 BPK_HD uint64_t udiv_exact64(uint64_t a, uint64_t g) {
     if (g == 1) return a;
     if (((a | g) >> 32) == 0) return (uint32_t)a / (uint32_t)g;
+    BPK_COUNT(7);
     int tz = bpk_ffs64((long long)g) - 1;
     a >>= tz;
     g >>= tz;
@@ -158,6 +190,7 @@ BPK_HD int ctz128(u128 x) {
 }
 
 BPK_HDNI u128 gcd_u128(u128 u, u128 v) {
+    BPK_COUNT(9);
     if (u == 0) return v;
     if (v == 0) return u;
     if ((u >> 64) == 0 && (v >> 64) == 0) return gcd_u64((uint64_t)u, (uint64_t)v);
@@ -178,7 +211,7 @@ BPK_HDNI u128 gcd_u128(u128 u, u128 v) {
 BPK_HD u128 uabs128(i128 x) { return x < 0 ? (u128)(-x) : (u128)x; }
 
 // from128 (rational.hpp:83-95): reduce an exact 128-bit fraction, check fit.
-BPK_HDNI Rat from128(i128 n, i128 d, Err& e) {
+BPK_HD Rat from128_body(i128 n, i128 d, Err& e) {
     if (d == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
     if (d < 0) { n = -n; d = -d; }
     u128 g = gcd_u128(uabs128(n), (u128)d);
@@ -188,6 +221,17 @@ BPK_HDNI Rat from128(i128 n, i128 d, Err& e) {
         return Rat{0, 1};
     }
     return Rat{(int64_t)n, (int64_t)d};
+}
+
+BPK_HDNI RatE from128_v(i128 n, i128 d) {
+    Err e{ERR_NONE};
+    const Rat r = from128_body(n, d, e);
+    return RatE{r, e.code};
+}
+BPK_HD Rat from128(i128 n, i128 d, Err& e) {
+    const RatE x = from128_v(n, d);
+    if (x.err) e.set(x.err);
+    return x.r;
 }
 
 // A 128-bit value already known to be reduced: only the range check.
@@ -204,12 +248,23 @@ BPK_HD uint64_t uabs64(int64_t x) {
 }
 
 // Rat(n, d) constructor -> normalize() (rational.hpp:18, 100-106).
-BPK_HDNI Rat rat_nd(int64_t n, int64_t d, Err& e) {
+BPK_HD Rat rat_nd_body(int64_t n, int64_t d, Err& e) {
     if (d == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
     if (d < 0) { n = -n; d = -d; }
     uint64_t g = gcd_u64(uabs64(n), (uint64_t)d);
     if (g > 1) { n = sdiv_exact64(n, g); d = (int64_t)udiv_exact64((uint64_t)d, g); }
     return Rat{n, d};
+}
+
+BPK_HDNI RatE rat_nd_v(int64_t n, int64_t d) {
+    Err e{ERR_NONE};
+    const Rat r = rat_nd_body(n, d, e);
+    return RatE{r, e.code};
+}
+BPK_HD Rat rat_nd(int64_t n, int64_t d, Err& e) {
+    const RatE x = rat_nd_v(n, d);
+    if (x.err) e.set(x.err);
+    return x.r;
 }
 
 BPK_HD bool fits64(i128 x) { return x <= (i128)INT64_MAX && x >= (i128)INT64_MIN; }
@@ -235,9 +290,11 @@ BPK_HD uint64_t inv64_lift(uint32_t m, uint32_t x32) {
 // Out of line on purpose: inlining every Rat operation into the refine and
 // simulator loops produced ~1 MB of SASS and the kernels stalled on
 // instruction fetch (ncu: "no_instruction" 17.5 cycles per issue).
-BPK_HDNI Rat rat_addsub_general(Rat a, Rat b, int s, Err& e);
 
-BPK_HDNI Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
+BPK_HD Rat rat_addsub_general(Rat a, Rat b, int s, Err& e);
+
+BPK_HD Rat rat_addsub_body(Rat a, Rat b, int s, Err& e) {
+    BPK_COUNT(11);
     i128 bn = s > 0 ? (i128)b.n : -(i128)b.n;
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n + bn, 1, e);
     if (a.d == 1) return fit128((i128)a.n * b.d + bn, b.d, e);        // gcd(num, b.d) = 1
@@ -277,7 +334,8 @@ BPK_HDNI Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
 
 // 64-bit denominators or a 128-bit t: kept out of the hot function so the
 // kernels' instruction stream stays small.
-BPK_HDNI Rat rat_addsub_general(Rat a, Rat b, int s, Err& e) {
+BPK_HD Rat rat_addsub_general_body(Rat a, Rat b, int s, Err& e) {
+    BPK_COUNT(8);
     i128 bn = s > 0 ? (i128)b.n : -(i128)b.n;
     uint64_t g = gcd_u64((uint64_t)a.d, (uint64_t)b.d);
     if (g == 1) return fit128((i128)a.n * b.d + bn * a.d, (i128)a.d * b.d, e);
@@ -292,6 +350,28 @@ BPK_HDNI Rat rat_addsub_general(Rat a, Rat b, int s, Err& e) {
     return fit128(num, den, e);
 }
 
+BPK_HDNI RatE rat_addsub_general_v(Rat a, Rat b, int s) {
+    Err e{ERR_NONE};
+    const Rat r = rat_addsub_general_body(a, b, s, e);
+    return RatE{r, e.code};
+}
+BPK_HD Rat rat_addsub_general(Rat a, Rat b, int s, Err& e) {
+    const RatE x = rat_addsub_general_v(a, b, s);
+    if (x.err) e.set(x.err);
+    return x.r;
+}
+
+BPK_HDNI RatE rat_addsub_v(Rat a, Rat b, int s) {
+    Err e{ERR_NONE};
+    const Rat r = rat_addsub_body(a, b, s, e);
+    return RatE{r, e.code};
+}
+BPK_HD Rat rat_addsub(Rat a, Rat b, int s, Err& e) {
+    const RatE x = rat_addsub_v(a, b, s);
+    if (x.err) e.set(x.err);
+    return x.r;
+}
+
 BPK_HD Rat rat_add(Rat a, Rat b, Err& e) {
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n + b.n, 1, e);
     return rat_addsub(a, b, +1, e);
@@ -302,7 +382,8 @@ BPK_HD Rat rat_sub(Rat a, Rat b, Err& e) {
 }
 
 // operator* (rational.hpp:33-35).
-BPK_HDNI Rat rat_mul_nl(Rat a, Rat b, Err& e) {
+BPK_HD Rat rat_mul_nl_body(Rat a, Rat b, Err& e) {
+    BPK_COUNT(10);
     if (a.n == 0 || b.n == 0) return Rat{0, 1};
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n * b.n, 1, e);
     uint64_t g1 = (b.d == 1) ? 1 : gcd_u64(uabs64(a.n), (uint64_t)b.d);
@@ -314,18 +395,40 @@ BPK_HDNI Rat rat_mul_nl(Rat a, Rat b, Err& e) {
     return fit128((i128)an * bn, (i128)ad * bd, e);
 }
 
+BPK_HDNI RatE rat_mul_nl_v(Rat a, Rat b) {
+    Err e{ERR_NONE};
+    const Rat r = rat_mul_nl_body(a, b, e);
+    return RatE{r, e.code};
+}
+BPK_HD Rat rat_mul_nl(Rat a, Rat b, Err& e) {
+    const RatE x = rat_mul_nl_v(a, b);
+    if (x.err) e.set(x.err);
+    return x.r;
+}
+
 // operator/ (rational.hpp:36-39): b == 0 -> domain_error.
 BPK_HD Rat rat_mul(Rat a, Rat b, Err& e) {
     if (a.d == 1 && b.d == 1) return fit128((i128)a.n * b.n, 1, e);
     return rat_mul_nl(a, b, e);
 }
 
-BPK_HDNI Rat rat_div(Rat a, Rat b, Err& e) {
+BPK_HD Rat rat_div_body(Rat a, Rat b, Err& e) {
     if (b.n == 0) { e.set(ERR_DOMAIN); return Rat{0, 1}; }
     // a / b = a * (b.d / b.n); keep the sign on the numerator.
     if (b.n == INT64_MIN) return from128((i128)a.n * b.d, (i128)a.d * b.n, e);
     Rat inv = b.n < 0 ? Rat{-b.d, -b.n} : Rat{b.d, b.n};
     return rat_mul(a, inv, e);
+}
+
+BPK_HDNI RatE rat_div_v(Rat a, Rat b) {
+    Err e{ERR_NONE};
+    const Rat r = rat_div_body(a, b, e);
+    return RatE{r, e.code};
+}
+BPK_HD Rat rat_div(Rat a, Rat b, Err& e) {
+    const RatE x = rat_div_v(a, b);
+    if (x.err) e.set(x.err);
+    return x.r;
 }
 
 // Comparisons cross-multiply in 128 bits and never throw (lines 47-56).

@@ -15,6 +15,10 @@
 
 using namespace bpk;
 
+#ifdef BPK_OPSTATS
+unsigned long long bpk::bpk_opstats[16];
+#endif
+
 namespace {
 
 const int64_t INF = INT64_MAX / 4;
@@ -269,6 +273,20 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
     if (getenv("BPEMU_STATS"))
         fprintf(stderr, "emu refine: queries %lld iterations %lld evaluated steps %lld (max %lld) moves %lld exact %lld\n",
                 (long long)r_q, (long long)r_it, (long long)r_ev, (long long)r_max, (long long)r_mv, (long long)r_ex);
+#ifdef BPK_OPSTATS
+    if (getenv("BPEMU_STATS")) {
+        fprintf(stderr, "opstats");
+        for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", bpk_opstats[k]);
+        fprintf(stderr, "\n");
+    }
+#endif
+    if (getenv("BPEMU_REFINE_ONLY")) {
+        for (int i = 0; i < nq; ++i)
+            if (B.qs[i].refined) fprintf(stderr, "q %d N %d L %lld evals %lld moves %lld\n", i, HB.q[i].N,
+                                         (long long)net_view(B.P, HB.q[i].net).L, (long long)B.qs[i].refine_evals,
+                                         (long long)B.qs[i].refine_moves);
+        return 0;
+    }
     for (int64_t c = 0; c < HB.ncand; ++c) prune_candidate(B, c);
     int64_t exact_n = 0, exact_ovf = 0, fast_n = 0;
     const size_t mn = (size_t)std::max(1, HB.max_N);
