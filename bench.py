@@ -167,6 +167,18 @@ def rooflines(stats, steps, clocks, problem, step_ms):
             traffic = json.load(f)
     except Exception:
         traffic = {}
+    # counters without launches (critical paths, moves, trials) are reported
+    # beside the kernels, not as kernels
+    counters = {k: stats[k]["work"] for k in list(stats) if stats[k]["launches"] == 0 and k != "refine_critical_path"}
+    for k in counters:
+        stats.pop(k)
+    # the prune phase is four launches (keys + list, representatives, members'
+    # shared estimates, members' own prunes); its work counter covers all of
+    # them, so its rate is quoted on the phase
+    parts = [k for k in ("prune_list", "prune", "prune_members", "prune_members_full") if k in stats]
+    if "prune" in stats and len(parts) > 1:
+        stats["prune"] = {"ms": sum(stats.pop(k)["ms"] for k in parts if k != "prune") + stats["prune"]["ms"],
+                          "launches": stats["prune"]["launches"], "work": stats["prune"]["work"]}
     kern = {}
     for k, v in stats.items():
         ms = v["ms"] / max(1, v["launches"])
@@ -178,6 +190,7 @@ def rooflines(stats, steps, clocks, problem, step_ms):
         kern[k] = e
     crit = stats.pop("refine_critical_path", None)
     kern.pop("refine_critical_path", None)
+    kern["counters"] = counters
     dom = max(stats, key=lambda k: stats[k]["ms"])
     d = kern[dom]
     u = work_unit(dom)
