@@ -529,15 +529,9 @@ __global__ void k_prune_members(BatchDev B, int pass) {
             B.cs[ci].mem0_from = (int32_t)r;
             B.cs[ci].mem0_buf = ef == 1 ? 0 : 1;
         } else if (ef == 1) {   // copy the estimate
-            for (int s = 0; s < N; ++s) {
-                B.sF[so + s] = B.sF[sr + s];
-                B.sB[so + s] = B.sB[sr + s];
-                B.sW[so + s] = B.sW[sr + s];
-                B.sMem[so + s] = B.sMem[sr + s];
-                B.sA[so + s] = B.sA[sr + s];
-                B.sSR[so + s] = B.sSR[sr + s];
-                if (B.details) B.stages[so + s] = B.stages[sr + s];
-            }
+            // (the estimate scratch itself is read by nothing after prune)
+            if (B.details)
+                for (int s = 0; s < N; ++s) B.stages[so + s] = B.stages[sr + s];
             cd.est_minibatch = rd.est_minibatch;
             cd.bubble = rd.bubble;
             cd.heuristic = rd.heuristic;

@@ -109,8 +109,10 @@ def full(path, tag):
     traffic = {}
     seen = {}
     for r in rows[2:]:
-        name = bench_name(r[hdr.index("Kernel Name")], seen)
-        out.append(f"## {name}")
+        raw = r[hdr.index("Kernel Name")]
+        name = bench_name(raw, seen)
+        short = re.sub(r"^.*::", "", raw.split("(")[0].replace("void ", "").split("<")[0])
+        out.append(f"## {name}" + (f" (`{short}`)" if short.lstrip("k_") != name else ""))
         out.append("")
         for key, label in WANT:
             if key in hdr:
@@ -120,7 +122,7 @@ def full(path, tag):
         if "dram__bytes_read.sum" in hdr:
             i, j = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
             rd, wr = to_bytes(r[i], units[i]), to_bytes(r[j], units[j])
-            traffic[name] = max(traffic.get(name, 0.0), rd + wr)
+            traffic[name] = traffic.get(name, 0.0) + rd + wr   # a phase's launches add up
         stalls = [(hdr[i], r[i]) for i in range(len(hdr))
                   if hdr[i].startswith("smsp__average_warps_issue_stalled_")
                   and hdr[i].endswith("_per_issue_active.ratio") and r[i] not in ("", "nan", "-nan")]

@@ -9,5 +9,5 @@ timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/$TAG/pytest_gpu.lo
 timeout 600 python bench.py > gpurun_out/$TAG/bench.json 2> gpurun_out/$TAG/bench.err
 timeout 600 python bench.py --impl reference > gpurun_out/$TAG/bench_ref.json 2> gpurun_out/$TAG/bench_ref.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/$TAG/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/$TAG/ncu_launch.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sim_exact|k_sim_flow|k_refine_smem|k_partition|k_prune" -c 7 -o gpurun_out/$TAG/full python tests/prof_sweep.py > gpurun_out/$TAG/ncu_full.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_sim_exact|k_sim_flow|k_refine_smem|k_partition|k_prune" -c 12 -o gpurun_out/$TAG/full python tests/prof_sweep.py > gpurun_out/$TAG/ncu_full.log 2>&1
 ls -la gpurun_out/$TAG
