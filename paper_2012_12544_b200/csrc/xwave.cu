@@ -32,6 +32,27 @@ namespace {
 // twice as many candidates share an SM.
 constexpr int FLOW_Q = 4;
 
+// Block-wide sync and OR-reduction of per-thread flags.  One warp (NT = 32):
+// a warp reduction, no barrier.  Two warps: one barrier per round on a
+// shared word, three words in rotation so that resetting the next round's
+// word never races with a slow reader of the previous one.
+template <int NT>
+__device__ __forceinline__ void flow_sync() {
+    if constexpr (NT == 32) __syncwarp();
+    else __syncthreads();
+}
+template <int NT>
+__device__ __forceinline__ unsigned flow_or(unsigned f, unsigned* red, int round) {
+    if constexpr (NT == 32) {
+        return __reduce_or_sync(0xffffffffu, f);
+    } else {
+        if (threadIdx.x == 0) red[(round + 1) % 3] = 0;
+        if (f) atomicOr(&red[round % 3], f);
+        __syncthreads();
+        return red[round % 3];
+    }
+}
+
 template <int NT>
 struct FlowSmem {
     Rat qF[NT][FLOW_Q];     // qF[s]: arrivals into stage s from s-1
@@ -39,6 +60,7 @@ struct FlowSmem {
     int prodF[NT], consF[NT];
     int prodB[NT], consB[NT];
     Rat fr[NT];
+    unsigned red[3];
 };
 
 template <int NT>
@@ -86,12 +108,14 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
             w = warmup_depth(kind, N, s + 1);
             if (w > M) w = M;
         }
-        __syncthreads();
+        if (s < 3) sm.red[s] = 0;
+        flow_sync<NT>();
         int64_t p = 0;                 // this stage's next position
         bool done = s >= N;
         bool aborted = false;
         volatile FlowSmem<NT>& vs = sm;
-        for (;;) {
+        int round = 0;
+        for (;; ++round) {
             bool ran = false;
             if (!done) {
                 const StageOp op = op_at(p, w, M);
@@ -137,15 +161,17 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
                     if (++p == 2 * M) done = true;
                 }
             }
-            if (__syncthreads_or(e.bad())) {
+            // bit 0: an error, bit 1: a stage not done, bit 2: a stage moved
+            const unsigned f = flow_or<NT>((e.bad() ? 1u : 0u) | (done ? 0u : 2u) | (ran ? 4u : 0u), sm.red, round);
+            if (f & 1u) {
                 aborted = true;
                 break;
             }
-            if (__syncthreads_and(done)) break;
-            if (!__syncthreads_or(ran)) __trap();   // no stage could move: impossible for a valid schedule
+            if (!(f & 2u)) break;
+            if (!(f & 4u)) __trap();   // no stage could move: impossible for a valid schedule
         }
         sm.fr[s] = fr;
-        __syncthreads();
+        flow_sync<NT>();
         // makespan (simulator.hpp:173-180)
         Rat mk{0, 1};
         for (int t = 0; t < N; ++t)
@@ -156,7 +182,8 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
             // link busy fraction Rat(M * SR) / makespan (239-244)
             if (s + 1 < N && mk.n != 0) (void)rat_div(R(M * srlink), mk, e);
         }
-        const bool bad = __syncthreads_or(aborted || e.bad());
+        // every thread left the loop in the same round: the next word is clean
+        const bool bad = flow_or<NT>((aborted || e.bad()) ? 1u : 0u, sm.red, round + 1) != 0;
         if (s == 0) {
             bp_candidate& out = B.cand[ci];
             if (bad) {
@@ -166,7 +193,7 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
                 out.status = BP_C_OK;
             }
         }
-        __syncthreads();
+        flow_sync<NT>();
     }
 }
 
