@@ -136,7 +136,9 @@ enum {
     BP_IP_SHARED_FULL = 5,    /* "stage <d2>: shared boundary layer must be fractional" */
     BP_IP_LEAD_UNSHARED = 6,  /* "stage <d2>: fractional lead without shared layer" */
     BP_IP_LAST = 7,           /* "last stage must end at layer L with full ownership" */
-    BP_IP_COVERAGE = 8        /* "layer <d2> coverage sums to <aux>, expected 1" */
+    BP_IP_COVERAGE = 8,       /* "layer <d2> coverage sums to <aux>, expected 1" */
+    BP_IP_STAGE_COUNT = 9,    /* "plan stage count != cluster size" (simulator.hpp:271-272) */
+    BP_IP_M = 10              /* "M >= 1 required" (simulator.hpp:83) */
 };
 
 typedef struct {
@@ -247,8 +249,76 @@ int bp_set_profiling(bp_ctx* ctx, int enable);
  *   comm-coarsened DP per (that, a_th), simulations per identical inputs --
  *   and share the results; 0 evaluates every query and candidate
  *   independently. */
-enum { BP_OPT_DEDUP = 1 };
+enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2 };
+/*   BP_OPT_PLAN_ONLY (default 0): each candidate stops after balance_partition,
+ *   its estimate and the memory check -- the reference's `bapipe plan`
+ *   (tools/bapipe.cpp:152-170), which calls balance_partition for one
+ *   (kind, M) with no min-micro filter and no simulation.  Feasible candidates
+ *   get BP_C_OK with makespan 0/1; want_details gives their plans. */
 int bp_set_option(bp_ctx* ctx, int option, int64_t value);
+
+/* ---- one plan: full-timeline simulate and estimate ----------------------
+ * simulate(kind, plan, net, cluster, M, micro, mini_batches)
+ * (simulator.hpp:264-274, 81-246) and estimate(kind, plan, net, cluster, M,
+ * micro) (cost_models.hpp:124-166) for a caller-given plan on network
+ * `network` and the first n_stages accelerators of cluster `cluster`.  The
+ * caller checks the kind against the cluster's mode (check_mode) first. */
+typedef struct {
+    int32_t network;
+    int32_t cluster;
+    int32_t kind;                  /* BP_KIND_* */
+    int32_t n_stages;              /* the plan's stage count */
+    int64_t M;
+    int64_t micro;                 /* micro-batch size */
+    int64_t mini_batches;          /* simulate only; the CLI uses 1 */
+    const int32_t* lo;             /* [n_stages], 1-based layers */
+    const int32_t* hi;
+    const bp_rat* lead;            /* leading / trailing fractions */
+    const bp_rat* trail;
+} bp_plan_request;
+
+/* Timeline event (simulator.hpp:16-36); kind: 0 FP, 1 BP, 2 SEND_F,
+ * 3 RECV_F, 4 SEND_B, 5 RECV_B. */
+typedef struct {
+    int64_t stage;                 /* 1-based */
+    int32_t kind;
+    int32_t pad;
+    int64_t micro_batch;           /* 1-based, numbered across mini-batches */
+    bp_rat start;
+    bp_rat end;
+} bp_event;
+
+typedef struct {
+    int32_t status;                /* BP_C_OK, BP_C_ERR_OVERFLOW, BP_C_ERR_DOMAIN,
+                                      BP_C_ERR_INVALID_PLAN, BP_C_REF_UB */
+    int32_t pad;
+    int64_t detail;                /* BP_IP_* for BP_C_ERR_INVALID_PLAN */
+    int64_t detail2;               /* stage / layer */
+    bp_rat aux;                    /* coverage sum for BP_IP_COVERAGE */
+    bp_rat makespan;               /* Timeline::makespan */
+    int64_t n_events;
+} bp_timeline_result;
+
+/* events: [cap] in the reference's order (stage, start, kind, micro-batch);
+ * cap >= mini_batches * (2*n*M + 4*(n-1)*M) always suffices.  highwater,
+ * weight_static: [n_stages]; busy: [n_stages - 1] (per_stage_feature_highwater,
+ * per_stage_weight_static, per_link_busy_fraction).  Returns BP_OK when the
+ * device ran (the outcome is in res->status), else an error code. */
+int bp_simulate_plan(bp_ctx* ctx, const bp_plan_request* req, bp_timeline_result* res, bp_event* events,
+                     int64_t cap, bp_rat* highwater, bp_rat* weight_static, bp_rat* busy);
+
+typedef struct {
+    int32_t status;                /* BP_C_OK, BP_C_ERR_OVERFLOW, BP_C_ERR_DOMAIN, BP_C_REF_UB */
+    int32_t heuristic;
+    bp_rat minibatch_time;
+    bp_rat bubble_fraction;
+} bp_estimate_result;
+
+/* stages: [n_stages]; echoes the plan and fills features, weights and
+ * bw_demand (link k in stages[k-1]); mem_infeasible: [n_stages], 1 where
+ * features + weights exceed the accelerator's capacity. */
+int bp_estimate_plan(bp_ctx* ctx, const bp_plan_request* req, bp_estimate_result* res, bp_stage* stages,
+                     int32_t* mem_infeasible);
 /* Copies up to cap entries: names (NUL-separated, 48 bytes each), total ms,
  * launch counts and algorithmic work units.  Returns the entry count. */
 int bp_kernel_stats(const bp_ctx* ctx, char* names48, double* ms, int64_t* launches,

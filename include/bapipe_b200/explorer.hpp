@@ -138,6 +138,12 @@ inline ExecutionMode mode_of(ScheduleKind k) {
     return (k == ScheduleKind::OneFOneB_AS || k == ScheduleKind::FBP_AS) ? ExecutionMode::Asynchronous
                                                                          : ExecutionMode::Synchronous;
 }
+// schedule_kind.hpp:59-64
+inline void check_mode(ScheduleKind k, ExecutionMode mode) {
+    if (mode_of(k) != mode)
+        throw IncompatibleSchedule(std::string(to_string(k)) + " requires " + to_string(mode_of(k)) +
+                                   " execution, cluster is " + to_string(mode));
+}
 inline std::int64_t warmup_depth(ScheduleKind k, std::int64_t n_stages, std::int64_t stage) {
     std::int64_t d = n_stages - stage + 1;
     return (k == ScheduleKind::FBP_AS || k == ScheduleKind::OneFOneB_SO) ? 2 * d : d;
@@ -303,6 +309,34 @@ struct ExplorationResult {
     std::optional<double> dp_baseline_minibatch_time;
 };
 
+// simulator.hpp:16-44
+enum class EventKind { FP, BP, SEND_F, RECV_F, SEND_B, RECV_B };
+inline const char* to_string(EventKind k) {
+    switch (k) {
+        case EventKind::FP: return "FP";
+        case EventKind::BP: return "BP";
+        case EventKind::SEND_F: return "SEND_F";
+        case EventKind::RECV_F: return "RECV_F";
+        case EventKind::SEND_B: return "SEND_B";
+        case EventKind::RECV_B: return "RECV_B";
+    }
+    return "?";
+}
+struct Event {
+    std::int64_t stage = 1;
+    EventKind kind = EventKind::FP;
+    std::int64_t micro_batch = 1;
+    Rat start{0};
+    Rat end{0};
+};
+struct Timeline {
+    std::vector<Event> events;
+    Rat makespan{0};
+    std::vector<Rat> per_stage_feature_highwater;
+    std::vector<Rat> per_stage_weight_static;
+    std::vector<Rat> per_link_busy_fraction;
+};
+
 // ------------------------------------------------------------------ device context
 class Explorer {
 public:
@@ -314,8 +348,32 @@ public:
     Explorer& operator=(const Explorer&) = delete;
 
     ExplorationResult explore(const NetworkProfile& net, const ClusterSpec& cluster, const TrainingConfig& cfg);
+    // partition.hpp:441-474 for one (kind, M, micro) -- `bapipe plan`
+    PartitionPlan balance_partition(const NetworkProfile& net, const ClusterSpec& cluster, ScheduleKind kind,
+                                    std::int64_t M, std::int64_t micro_batch_size = 1);
+    // cost_models.hpp:124-166 on a given plan
+    CostEstimate estimate(ScheduleKind kind, const PartitionPlan& plan, const NetworkProfile& net,
+                          const ClusterSpec& cluster, std::int64_t M, std::int64_t micro_batch_size = 1);
+    // simulator.hpp:264-274: the full event timeline of a plan
+    Timeline simulate(ScheduleKind kind, const PartitionPlan& plan, const NetworkProfile& net,
+                      const ClusterSpec& cluster, std::int64_t M, std::int64_t micro_batch_size = 1,
+                      std::int64_t mini_batches = 1);
 
 private:
+    // SoA tables of (net, cluster) on the device: network 0, cluster 0.  The
+    // host copies stay alive until the next upload (an ABI implementation may
+    // read them until the evaluating call returns).
+    void upload(const NetworkProfile& net, const ClusterSpec& cluster);
+    struct Tables {
+        std::vector<std::int64_t> fp, bp, w, a, caps, mm, bw;
+        std::vector<std::int32_t> types;
+    } tables_;
+    struct PlanBuf {
+        std::vector<std::int32_t> lo, hi;
+        std::vector<bp_rat> lead, trail;
+    };
+    static bp_plan_request plan_request(const PartitionPlan& plan, PlanBuf& buf, ScheduleKind kind,
+                                        std::int64_t M, std::int64_t micro, std::int64_t mini);
     void check(int rc, const char* what) {
         if (rc != BP_OK) throw DeviceError(std::string(what) + ": " + bp_last_error(ctx_));
     }
@@ -331,6 +389,20 @@ inline Explorer& default_explorer() {
 inline ExplorationResult explore(const NetworkProfile& net, const ClusterSpec& cluster, const TrainingConfig& cfg) {
     return default_explorer().explore(net, cluster, cfg);
 }
+inline PartitionPlan balance_partition(const NetworkProfile& net, const ClusterSpec& cluster, ScheduleKind kind,
+                                       std::int64_t M, std::int64_t micro_batch_size = 1) {
+    return default_explorer().balance_partition(net, cluster, kind, M, micro_batch_size);
+}
+inline CostEstimate estimate(ScheduleKind kind, const PartitionPlan& plan, const NetworkProfile& net,
+                             const ClusterSpec& cluster, std::int64_t M, std::int64_t micro_batch_size = 1) {
+    return default_explorer().estimate(kind, plan, net, cluster, M, micro_batch_size);
+}
+inline Timeline simulate(ScheduleKind kind, const PartitionPlan& plan, const NetworkProfile& net,
+                         const ClusterSpec& cluster, std::int64_t M, std::int64_t micro_batch_size = 1,
+                         std::int64_t mini_batches = 1) {
+    return default_explorer().simulate(kind, plan, net, cluster, M, micro_batch_size, mini_batches);
+}
+inline std::vector<Rat> memory_highwater(const Timeline& t) { return t.per_stage_feature_highwater; }
 
 namespace detail {
 inline Rat R(const bp_rat& r) { return Rat::raw(r.num, r.den); }
@@ -348,22 +420,26 @@ inline std::string invalid_plan_message(const bp_candidate& c) {
         case BP_IP_LAST: return "last stage must end at layer L with full ownership";
         case BP_IP_COVERAGE:
             return "layer " + std::to_string(c.detail2) + " coverage sums to " + R(c.aux).str() + ", expected 1";
+        case BP_IP_STAGE_COUNT: return "plan stage count != cluster size";
+        case BP_IP_M: return "M >= 1 required";
         default: return "invalid plan";
+    }
+}
+
+// an escaping device status as the reference throws it
+[[noreturn]] inline void throw_status(int status, const std::string& invalid_plan_msg) {
+    switch (status) {
+        case BP_C_ERR_OVERFLOW: throw std::overflow_error("Rat: overflow");
+        case BP_C_ERR_DOMAIN: throw std::domain_error("Rat: division by zero");
+        case BP_C_ERR_INVALID_PLAN: throw InvalidPlan(invalid_plan_msg);
+        case BP_C_REF_UB:
+            throw UndefinedInReference("a plan stage reads a layer outside net.layers (plan.hpp:90-158)");
+        default: throw SchemaError("plan rejected by the device library");
     }
 }
 }  // namespace detail
 
-inline ExplorationResult Explorer::explore(const NetworkProfile& net, const ClusterSpec& cluster,
-                                           const TrainingConfig& cfg) {
-    // the reference's own validation order (explorer.hpp:82-83, 87-89)
-    validate_pair(net, cluster);
-    if (cfg.mini_batch_size < 1) throw SchemaError("mini_batch_size >= 1 required");
-    for (ScheduleKind k : feasible_kinds(cluster.execution_mode)) (void)candidate_Ms(cfg, cluster, k);
-    // an explicit empty list yields no candidates (the ABI reads n_m == 0 as
-    // "all divisors", so this case is answered here, as explorer.hpp:135-141)
-    if (cfg.micro_batch_candidates && cfg.micro_batch_candidates->empty())
-        throw NoFeasiblePlan("all 0 candidates rejected");
-
+inline void Explorer::upload(const NetworkProfile& net, const ClusterSpec& cluster) {
     // SoA: global accelerator-type ids over the cluster's types and the
     // network's map keys; 0 marks a missing entry.
     std::map<std::string, int> tid;
@@ -373,7 +449,12 @@ inline ExplorationResult Explorer::explore(const NetworkProfile& net, const Clus
         for (auto& kv : l.bp_time) tid.emplace(kv.first, (int)tid.size());
     }
     const int T = (int)tid.size(), L = (int)net.L(), N = (int)cluster.N();
-    std::vector<std::int64_t> fp((std::size_t)T * L, 0), bp((std::size_t)T * L, 0), w(L), a(L);
+    Tables& tb = tables_;
+    tb.fp.assign((std::size_t)T * L, 0);
+    tb.bp.assign((std::size_t)T * L, 0);
+    tb.w.assign(L, 0);
+    tb.a.assign(L, 0);
+    auto &fp = tb.fp, &bp = tb.bp, &w = tb.w, &a = tb.a;
     for (int j = 0; j < L; ++j) {
         const LayerProfile& l = net.layers[j];
         for (auto& [t, v] : l.fp_time) fp[(std::size_t)tid[t] * L + j] = v;
@@ -381,8 +462,12 @@ inline ExplorationResult Explorer::explore(const NetworkProfile& net, const Clus
         w[j] = l.weight_bytes;
         a[j] = l.out_activation_bytes;
     }
-    std::vector<std::int32_t> types(N);
-    std::vector<std::int64_t> caps(N), mm((std::size_t)N * 4), bw(cluster.link_bandwidth);
+    tb.types.assign(N, 0);
+    tb.caps.assign(N, 0);
+    tb.mm.assign((std::size_t)N * 4, 0);
+    tb.bw = cluster.link_bandwidth;
+    auto &types = tb.types;
+    auto &caps = tb.caps, &mm = tb.mm, &bw = tb.bw;
     for (int i = 0; i < N; ++i) {
         types[i] = tid[cluster.accelerators[i].accel_type];
         caps[i] = cluster.accelerators[i].mem_capacity_bytes;
@@ -394,6 +479,20 @@ inline ExplorationResult Explorer::explore(const NetworkProfile& net, const Clus
                   types.data(), caps.data(), mm.data(), bw.data()};
     check(bp_set_networks(ctx_, &bn, 1), "bp_set_networks");
     check(bp_set_clusters(ctx_, &bc, 1), "bp_set_clusters");
+}
+
+inline ExplorationResult Explorer::explore(const NetworkProfile& net, const ClusterSpec& cluster,
+                                           const TrainingConfig& cfg) {
+    // the reference's own validation order (explorer.hpp:82-83, 87-89)
+    validate_pair(net, cluster);
+    if (cfg.mini_batch_size < 1) throw SchemaError("mini_batch_size >= 1 required");
+    for (ScheduleKind k : feasible_kinds(cluster.execution_mode)) (void)candidate_Ms(cfg, cluster, k);
+    // an explicit empty list yields no candidates (the ABI reads n_m == 0 as
+    // "all divisors", so this case is answered here, as explorer.hpp:135-141)
+    if (cfg.micro_batch_candidates && cfg.micro_batch_candidates->empty())
+        throw NoFeasiblePlan("all 0 candidates rejected");
+    upload(net, cluster);
+    const int N = (int)cluster.N();
     std::vector<std::int64_t> mlist;
     bp_query q{};
     q.network = 0;
@@ -505,6 +604,162 @@ inline ExplorationResult Explorer::explore(const NetworkProfile& net, const Clus
     for (auto& kv : ranked) out.ranked.push_back(std::move(kv.second));
     out.best = out.ranked.front();
     return out;
+}
+
+inline bp_plan_request Explorer::plan_request(const PartitionPlan& plan, PlanBuf& buf, ScheduleKind kind,
+                                              std::int64_t M, std::int64_t micro, std::int64_t mini) {
+    for (const StageAssignment& st : plan.stages) {
+        buf.lo.push_back((std::int32_t)std::max<std::int64_t>(INT32_MIN, std::min<std::int64_t>(INT32_MAX, st.lo)));
+        buf.hi.push_back((std::int32_t)std::max<std::int64_t>(INT32_MIN, std::min<std::int64_t>(INT32_MAX, st.hi)));
+        buf.lead.push_back(bp_rat{st.leading_fraction.num(), st.leading_fraction.den()});
+        buf.trail.push_back(bp_rat{st.trailing_fraction.num(), st.trailing_fraction.den()});
+    }
+    bp_plan_request q{};
+    q.network = 0;
+    q.cluster = 0;
+    q.kind = (std::int32_t)kind;
+    q.n_stages = (std::int32_t)plan.stages.size();
+    q.M = M;
+    q.micro = micro;
+    q.mini_batches = mini;
+    q.lo = buf.lo.data();
+    q.hi = buf.hi.data();
+    q.lead = buf.lead.data();
+    q.trail = buf.trail.data();
+    return q;
+}
+
+inline PartitionPlan Explorer::balance_partition(const NetworkProfile& net, const ClusterSpec& cluster,
+                                                 ScheduleKind kind, std::int64_t M, std::int64_t micro) {
+    check_mode(kind, cluster.execution_mode);   // partition.hpp:443-444
+    validate_pair(net, cluster);
+    // the device enumerates (kind, M) candidates of a mini-batch M * micro
+    if (M < 1 || micro < 1) throw SchemaError("balance_partition: M >= 1 and micro-batch size >= 1 required");
+    upload(net, cluster);
+    const int N = (int)cluster.N();
+    std::int64_t mlist[1] = {M};
+    bp_query q{};
+    q.n_stages = N;
+    q.mini_batch = M * micro;
+    q.n_m = 1;
+    q.m_list = mlist;
+    std::int64_t ncand = 0, nst = 0;
+    check(bp_layout(ctx_, &q, 1, &ncand, &nst), "bp_layout");
+    bp_query_result res{};
+    std::vector<bp_candidate> cand((std::size_t)std::max<std::int64_t>(ncand, 1));
+    std::vector<bp_stage> stg((std::size_t)std::max<std::int64_t>(nst, 1));
+    check(bp_set_option(ctx_, BP_OPT_PLAN_ONLY, 1), "bp_set_option");
+    const int rc = bp_explore_batch(ctx_, &q, 1, &res, cand.data(), stg.data(), nullptr);
+    bp_set_option(ctx_, BP_OPT_PLAN_ONLY, 0);
+    check(rc, "bp_explore_batch");
+    const std::vector<ScheduleKind> kinds = feasible_kinds(cluster.execution_mode);
+    const std::size_t slot = (std::size_t)(std::find(kinds.begin(), kinds.end(), kind) - kinds.begin());
+    const bp_candidate& c = cand[slot];
+    switch (c.status) {
+        case BP_C_OK: {
+            PartitionPlan plan;
+            const bp_stage* st = stg.data() + slot * (std::size_t)N;
+            for (int k = 0; k < N; ++k) {
+                StageAssignment sa;
+                sa.accelerator_id = cluster.accelerators[k].id;
+                sa.lo = st[k].lo;
+                sa.hi = st[k].hi;
+                sa.leading_fraction = detail::R(st[k].lead);
+                sa.trailing_fraction = detail::R(st[k].trail);
+                plan.stages.push_back(sa);
+            }
+            return plan;
+        }
+        case BP_C_REJ_COARSEN:
+            throw Infeasible("coarsening for communication leaves " + std::to_string(c.detail) + " blocks for " +
+                             std::to_string(N) + " stages");
+        case BP_C_REJ_FINETUNE:
+            throw Infeasible(std::string("no contiguous plan satisfies memory for ") + to_string(kind) +
+                             ", M=" + std::to_string(M));
+        case BP_C_REJ_FINETUNE_NOCONV: throw Infeasible("memory fine-tune did not converge");
+        case BP_C_REJ_SHAPE:
+            throw InfeasibleShape(std::to_string(c.detail) + " partition units for " + std::to_string(N) + " stages");
+        case BP_C_REJ_MEM_POST:
+            // a balanced plan whose final estimate is over capacity: memory_fine_tune
+            // only returns plans within capacity, so this is not reached
+            throw Infeasible("memory");
+        default: detail::throw_status(c.status, detail::invalid_plan_message(c));
+    }
+}
+
+inline CostEstimate Explorer::estimate(ScheduleKind kind, const PartitionPlan& plan, const NetworkProfile& net,
+                                       const ClusterSpec& cluster, std::int64_t M, std::int64_t micro) {
+    check_mode(kind, cluster.execution_mode);   // cost_models.hpp:127-129
+    if (plan.n_stages() != cluster.N()) throw InvalidPlan("plan stage count != cluster size");
+    upload(net, cluster);
+    PlanBuf buf;
+    const bp_plan_request q = plan_request(plan, buf, kind, M, micro, 1);
+    const std::size_t N = plan.stages.size();
+    bp_estimate_result r{};
+    std::vector<bp_stage> st(N);
+    std::vector<std::int32_t> inf(N);
+    check(bp_estimate_plan(ctx_, &q, &r, st.data(), inf.data()), "bp_estimate_plan");
+    if (r.status != BP_C_OK) detail::throw_status(r.status, "");
+    CostEstimate e;
+    e.schedule = kind;
+    e.M = M;
+    e.N = (std::int64_t)N;
+    e.minibatch_time = detail::R(r.minibatch_time);
+    e.bubble_fraction = detail::R(r.bubble_fraction);
+    e.heuristic = r.heuristic != 0;
+    for (std::size_t i = 0; i < N; ++i) {
+        e.features_mem.push_back(detail::R(st[i].features));
+        e.weights_mem.push_back(detail::R(st[i].weights));
+        e.mem_infeasible.push_back(inf[i] != 0);
+        if (i + 1 < N) e.bandwidth_demand.push_back(detail::R(st[i].bw_demand));
+    }
+    return e;
+}
+
+inline Timeline Explorer::simulate(ScheduleKind kind, const PartitionPlan& plan, const NetworkProfile& net,
+                                   const ClusterSpec& cluster, std::int64_t M, std::int64_t micro,
+                                   std::int64_t mini_batches) {
+    check_mode(kind, cluster.execution_mode);   // simulator.hpp:268
+    if (plan.stages.empty()) throw InvalidPlan("plan has no stages");
+    if (mini_batches < 1) throw SchemaError("simulate: mini_batches >= 1 required");
+    upload(net, cluster);
+    PlanBuf buf;
+    const bp_plan_request q = plan_request(plan, buf, kind, M, micro, mini_batches);
+    const std::int64_t N = plan.n_stages(), Mp = std::max<std::int64_t>(M, 0);
+    const std::int64_t cap = mini_batches * (2 * N * Mp + 4 * (N - 1) * Mp);
+    std::vector<bp_event> ev((std::size_t)std::max<std::int64_t>(cap, 1));
+    std::vector<bp_rat> hw((std::size_t)N), ws((std::size_t)N), busy((std::size_t)std::max<std::int64_t>(N - 1, 1));
+    bp_timeline_result r{};
+    check(bp_simulate_plan(ctx_, &q, &r, ev.data(), cap, hw.data(), ws.data(), busy.data()), "bp_simulate_plan");
+    if (r.status != BP_C_OK) {
+        std::string msg;
+        if (r.status == BP_C_ERR_INVALID_PLAN) {
+            bp_candidate c{};
+            c.detail = r.detail;
+            c.detail2 = r.detail2;
+            c.aux = r.aux;
+            msg = detail::invalid_plan_message(c);
+            if (r.detail == BP_IP_RANGE) {   // the plan is at hand: the reference's full message
+                const StageAssignment& st = plan.stages[(std::size_t)r.detail2 - 1];
+                msg = "stage " + std::to_string(r.detail2) + ": layer range [" + std::to_string(st.lo) + "," +
+                      std::to_string(st.hi) + "] out of bounds";
+            }
+        }
+        detail::throw_status(r.status, msg);
+    }
+    Timeline t;
+    t.makespan = detail::R(r.makespan);
+    t.events.reserve((std::size_t)r.n_events);
+    for (std::int64_t i = 0; i < r.n_events; ++i) {
+        const bp_event& x = ev[(std::size_t)i];
+        t.events.push_back({x.stage, (EventKind)x.kind, x.micro_batch, detail::R(x.start), detail::R(x.end)});
+    }
+    for (std::int64_t s = 0; s < N; ++s) {
+        t.per_stage_feature_highwater.push_back(detail::R(hw[(std::size_t)s]));
+        t.per_stage_weight_static.push_back(detail::R(ws[(std::size_t)s]));
+    }
+    for (std::int64_t k = 0; k + 1 < N; ++k) t.per_link_busy_fraction.push_back(detail::R(busy[(std::size_t)k]));
+    return t;
 }
 
 }  // namespace bapipe_b200

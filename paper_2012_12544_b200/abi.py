@@ -84,19 +84,45 @@ class bp_best_record(C.Structure):
                 ("query_id", C.c_int64), ("pad", C.c_int64)]
 
 
+class bp_plan_request(C.Structure):
+    _fields_ = [("network", C.c_int32), ("cluster", C.c_int32), ("kind", C.c_int32), ("n_stages", C.c_int32),
+                ("M", C.c_int64), ("micro", C.c_int64), ("mini_batches", C.c_int64), ("lo", P32), ("hi", P32),
+                ("lead", C.POINTER(bp_rat)), ("trail", C.POINTER(bp_rat))]
+
+
+class bp_event(C.Structure):
+    _fields_ = [("stage", C.c_int64), ("kind", C.c_int32), ("pad", C.c_int32), ("micro_batch", C.c_int64),
+                ("start", bp_rat), ("end", bp_rat)]
+
+
+class bp_timeline_result(C.Structure):
+    _fields_ = [("status", C.c_int32), ("pad", C.c_int32), ("detail", C.c_int64), ("detail2", C.c_int64),
+                ("aux", bp_rat), ("makespan", bp_rat), ("n_events", C.c_int64)]
+
+
+class bp_estimate_result(C.Structure):
+    _fields_ = [("status", C.c_int32), ("heuristic", C.c_int32), ("minibatch_time", bp_rat),
+                ("bubble_fraction", bp_rat)]
+
+
 assert C.sizeof(bp_query) == 48
 assert C.sizeof(bp_candidate) == 152
 assert C.sizeof(bp_stage) == 96
 assert C.sizeof(bp_best_record) == 80
+assert C.sizeof(bp_plan_request) == 72
+assert C.sizeof(bp_event) == 56
+assert C.sizeof(bp_timeline_result) == 64
 
 # Every symbol include/bapipe_b200.h declares (checked by tests/test_abi.py).
 PRODUCT_SYMBOLS = (
     "bp_create", "bp_destroy", "bp_last_error", "bp_abi_version", "bp_set_networks",
     "bp_set_clusters", "bp_layout", "bp_explore_batch", "bp_batch_prepare", "bp_batch_run",
     "bp_batch_fetch", "bp_batch_best", "bp_batch_free", "bp_launch_count", "bp_set_profiling",
-    "bp_kernel_stats", "bp_transfer_stats", "bp_best_less", "bp_set_option",
+    "bp_kernel_stats", "bp_transfer_stats", "bp_best_less", "bp_set_option", "bp_simulate_plan",
+    "bp_estimate_plan",
 )
 BP_OPT_DEDUP = 1
+BP_OPT_PLAN_ONLY = 2
 
 
 def _sig(lib, name, res, args):
@@ -131,6 +157,11 @@ def bind_product(lib: C.CDLL) -> C.CDLL:
          [vp, C.c_char_p, C.POINTER(C.c_double), P64, C.POINTER(C.c_double), C.c_int])
     _sig(lib, "bp_transfer_stats", C.c_int, [vp, P64, P64])
     _sig(lib, "bp_best_less", C.c_int, [C.POINTER(bp_best_record), C.POINTER(bp_best_record)])
+    _sig(lib, "bp_simulate_plan", C.c_int,
+         [vp, C.POINTER(bp_plan_request), C.POINTER(bp_timeline_result), C.POINTER(bp_event), C.c_int64,
+          C.POINTER(bp_rat), C.POINTER(bp_rat), C.POINTER(bp_rat)])
+    _sig(lib, "bp_estimate_plan", C.c_int,
+         [vp, C.POINTER(bp_plan_request), C.POINTER(bp_estimate_result), C.POINTER(bp_stage), P32])
     return lib
 
 

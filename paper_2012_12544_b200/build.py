@@ -18,8 +18,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbapipe_b200.so")
-SOURCES = ["api.cu", "kernels.cu", "dp.cu", "sim.cu", "xwave.cu"]
-HEADERS = ["rat.cuh", "common.cuh", "model.cuh", "batch.cuh", "phases.cuh", "kernels.h", "host_prep.hpp"]
+SOURCES = ["api.cu", "kernels.cu", "dp.cu", "sim.cu", "xwave.cu", "timeline.cu"]
+HEADERS = ["rat.cuh", "common.cuh", "model.cuh", "batch.cuh", "phases.cuh", "kernels.h", "host_prep.hpp", "timeline.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -78,7 +78,7 @@ def build_cli(force=False):
     if not os.path.exists(os.path.join(JSON_DIR, "json.hpp")):
         return None
     src = os.path.join(HERE, "cli", "bapipe.cpp")
-    deps = [src, SO] + [os.path.join(ROOT, "include", "bapipe_b200", f) for f in ("explorer.hpp", "io.hpp")]
+    deps = [src, SO] + [os.path.join(ROOT, "include", "bapipe_b200", f) for f in ("explorer.hpp", "io.hpp", "gantt.hpp")]
     if not force and not _stale(CLI, deps):
         return CLI
     os.makedirs(os.path.dirname(CLI), exist_ok=True)

@@ -107,6 +107,7 @@ struct bp_ctx {
     int max_T = 1;
     bool prof = false;
     bool dedup = true;       // BP_OPT_DEDUP
+    bool plan_only = false;  // BP_OPT_PLAN_ONLY
     std::map<std::string, KStat> stats;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -428,6 +429,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     BatchDev& D = B->dev;
     const HostBatch& hb = B->hb;
     D.dedup = c->dedup ? 1 : 0;
+    D.plan_only = c->plan_only ? 1 : 0;
     cudaError_t e;
     e = cudaMemsetAsync(D.cand, 0, (size_t)hb.ncand * sizeof(bp_candidate), st);
     if (e == cudaSuccess && D.stages) e = cudaMemsetAsync(D.stages, 0, (size_t)hb.nstage * sizeof(bp_stage), st);
@@ -474,6 +476,12 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "prune", st, [&] { launch_prune(D, -1, st, 2); });
     timed(c, "prune_members", st, [&] { launch_prune(D, -1, st, 4); });
     timed(c, "prune_members_full", st, [&] { launch_prune(D, -1, st, 8); });
+    if (D.plan_only) {   // `bapipe plan`: no simulation
+        timed(c, "plan_finish", st, [&] { launch_plan_finish(D, st); });
+        timed(c, "rank", st, [&] { launch_rank(D, st); });
+        e = cudaGetLastError();
+        return e == cudaSuccess ? BP_OK : cuda_fail(c, e, "kernel launch");
+    }
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
@@ -721,8 +729,51 @@ int bp_set_option(bp_ctx* c, int option, int64_t value) {
     if (!c) return BP_BAD_INPUT;
     switch (option) {
         case BP_OPT_DEDUP: c->dedup = value != 0; return BP_OK;
+        case BP_OPT_PLAN_ONLY: c->plan_only = value != 0; return BP_OK;
         default: return fail(c, BP_BAD_INPUT, "unknown option " + std::to_string(option));
     }
+}
+
+static int plan_request_ok(bp_ctx* c, const bp_plan_request* q) {
+    if (!c || !q) return fail(c, BP_BAD_INPUT, "null argument");
+    if (!c->have_nets || !c->have_cls) return fail(c, BP_BAD_INPUT, "bp_set_networks / bp_set_clusters first");
+    if (q->network < 0 || q->network >= (int)c->hn.desc.size() || q->cluster < 0 ||
+        q->cluster >= (int)c->hc.desc.size())
+        return fail(c, BP_BAD_INPUT, "network / cluster index out of range");
+    if (q->n_stages < 1 || !q->lo || !q->hi || !q->lead || !q->trail)
+        return fail(c, BP_BAD_INPUT, "plan with no stages");
+    if (q->kind < 0 || q->kind > 3) return fail(c, BP_BAD_INPUT, "unknown schedule kind");
+    for (int s = 0; s < q->n_stages; ++s)
+        if (q->lead[s].den <= 0 || q->trail[s].den <= 0) return fail(c, BP_BAD_INPUT, "fraction with den <= 0");
+    return BP_OK;
+}
+
+int bp_simulate_plan(bp_ctx* c, const bp_plan_request* q, bp_timeline_result* res, bp_event* events, int64_t cap,
+                     bp_rat* highwater, bp_rat* weight_static, bp_rat* busy) {
+    int rc = plan_request_ok(c, q);
+    if (rc != BP_OK) return rc;
+    if (!res) return fail(c, BP_BAD_INPUT, "null result");
+    if (q->mini_batches < 1) return fail(c, BP_BAD_INPUT, "mini_batches >= 1 required");
+    const cudaError_t e = timeline_simulate(c->P, c->hc.desc[(size_t)q->cluster].N, *q, res, events, cap, highwater,
+                                            weight_static, busy, &c->h2d, &c->d2h);
+    c->launches += 2;
+    if (e != cudaSuccess) return cuda_fail(c, e, "bp_simulate_plan");
+    if (res->status == BP_C_OK && res->n_events > cap && events) return fail(c, BP_BAD_INPUT, "event capacity too small");
+    return BP_OK;
+}
+
+int bp_estimate_plan(bp_ctx* c, const bp_plan_request* q, bp_estimate_result* res, bp_stage* stages,
+                     int32_t* mem_infeasible) {
+    int rc = plan_request_ok(c, q);
+    if (rc != BP_OK) return rc;
+    if (!res) return fail(c, BP_BAD_INPUT, "null result");
+    if (q->n_stages > c->hc.desc[(size_t)q->cluster].N)
+        return fail(c, BP_BAD_INPUT, "plan longer than the cluster");
+    const cudaError_t e = timeline_estimate(c->P, c->hc.desc[(size_t)q->cluster].N, *q, res, stages, mem_infeasible,
+                                            &c->h2d, &c->d2h);
+    c->launches += 1;
+    if (e != cudaSuccess) return cuda_fail(c, e, "bp_estimate_plan");
+    return BP_OK;
 }
 
 int bp_kernel_stats(const bp_ctx* c, char* names48, double* ms, int64_t* launches, double* work, int cap) {

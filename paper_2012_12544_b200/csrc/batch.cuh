@@ -148,6 +148,7 @@ struct BatchDev {
     int32_t* crep;            // [cmask+1] smallest mslot index per hash
     int32_t cmask;
     int32_t dedup;            // BP_OPT_DEDUP: share identical subproblems
+    int32_t plan_only;        // BP_OPT_PLAN_ONLY: stop after balance_partition + estimate
     int32_t* rlist;           // [nq] queries to refine this run (compacted)
     int32_t* rcount;          // [2] list length, next entry
     int32_t* plist;           // [ncand] candidates to prune this run (compacted)

@@ -547,6 +547,15 @@ __global__ void k_prune_members(BatchDev B, int pass) {
     B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;   // pruned by the second k_prune
 }
 
+// BP_OPT_PLAN_ONLY: a candidate that passed the estimate and memory check is
+// done (`bapipe plan` does not simulate)
+__global__ void k_plan_finish(BatchDev B) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= B.ncand || !B.cs[ci].sim_ready || B.cand[ci].status != C_PENDING) return;
+    B.cand[ci].status = BP_C_OK;
+    B.cand[ci].makespan = bp_rat{0, 1};
+}
+
 __global__ void k_rank(BatchDev B) {
     int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi < B.nq) rank_query(B, qi);
@@ -747,6 +756,9 @@ void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part) {
         k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
     }
     if (part & 8) k_prune<<<grid, 32, 0, st>>>(B, -1);
+}
+void launch_plan_finish(const BatchDev& B, cudaStream_t st) {
+    if (B.ncand) k_plan_finish<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
 }
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);

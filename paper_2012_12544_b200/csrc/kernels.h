@@ -32,6 +32,13 @@ void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st);
 void launch_sim_flow(const BatchDev& B, int k, int sms, cudaStream_t st);
 size_t sim_exact_state_bytes(int sms, int max_N);
 void launch_rank(const BatchDev& B, cudaStream_t st);
+void launch_plan_finish(const BatchDev& B, cudaStream_t st);
+// one caller-given plan (timeline.cu)
+cudaError_t timeline_simulate(const Pools& P, int clusterN, const bp_plan_request& q, bp_timeline_result* res,
+                              bp_event* events, int64_t cap, bp_rat* highwater, bp_rat* wstatic, bp_rat* busy,
+                              int64_t* h2d, int64_t* d2h);
+cudaError_t timeline_estimate(const Pools& P, int clusterN, const bp_plan_request& q, bp_estimate_result* res,
+                              bp_stage* stages, int32_t* infeasible, int64_t* h2d, int64_t* d2h);
 void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,
                  cudaStream_t st);
 

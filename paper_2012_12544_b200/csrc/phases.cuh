@@ -55,7 +55,8 @@ BPK_HDNI void setup_query(const BatchDev& B, int qi) {
             cd.micro = Q.mini / cd.M;
             cd.rank = -1;
             cd.n_stages = Q.N;
-            cd.status = (Q.mini / cd.M >= min_micro) ? C_PENDING : BP_C_REJ_MIN_MICRO;
+            // (`bapipe plan` calls balance_partition with no min-micro filter)
+            cd.status = (B.plan_only || Q.mini / cd.M >= min_micro) ? C_PENDING : BP_C_REJ_MIN_MICRO;
             B.cand[ci] = cd;
             B.cs[ci] = CState{};
             B.cq[ci] = qi;

@@ -46,6 +46,19 @@ int bp_layout(bp_ctx* c, bp_query* q, int nq, int64_t* tc, int64_t* ts) {
     *ts = hb.nstage;
     return BP_OK;
 }
+int bp_set_option(bp_ctx*, int option, int64_t value) {
+    if (option == BP_OPT_PLAN_ONLY) bpemu_set_plan_only(value != 0);
+    return option == BP_OPT_DEDUP || option == BP_OPT_PLAN_ONLY ? BP_OK : BP_BAD_INPUT;
+}
+int bp_simulate_plan(bp_ctx* c, const bp_plan_request* q, bp_timeline_result* res, bp_event* events, int64_t cap,
+                     bp_rat* hw, bp_rat* ws, bp_rat* busy) {
+    return bpemu_plan(c->nets.data(), (int)c->nets.size(), c->cls.data(), (int)c->cls.size(), q, res, events, cap,
+                      hw, ws, busy, nullptr, nullptr, nullptr);
+}
+int bp_estimate_plan(bp_ctx* c, const bp_plan_request* q, bp_estimate_result* res, bp_stage* st, int32_t* inf) {
+    return bpemu_plan(c->nets.data(), (int)c->nets.size(), c->cls.data(), (int)c->cls.size(), q, nullptr, nullptr,
+                      0, nullptr, nullptr, nullptr, res, st, inf);
+}
 int bp_explore_batch(bp_ctx* c, const bp_query* q, int nq, bp_query_result* res, bp_candidate* cand,
                      bp_stage* stages, void*) {
     uint64_t work = 0;

@@ -12,6 +12,7 @@
 
 #include "../../paper_2012_12544_b200/csrc/host_prep.hpp"
 #include "../../paper_2012_12544_b200/csrc/phases.cuh"
+#include "../../paper_2012_12544_b200/csrc/timeline.cuh"
 
 using namespace bpk;
 
@@ -182,6 +183,108 @@ T* vec(std::vector<T>& v, size_t n) {
 
 }  // namespace
 
+static int g_plan_only = 0;   // BP_OPT_PLAN_ONLY
+
+static Pools host_pools(const HostNets& HN, const HostCls& HC) {
+    Pools P{};
+    P.nets = HN.desc.data();
+    P.cls = HC.desc.data();
+    P.fp = HN.fp.data();
+    P.bp = HN.bp.data();
+    P.w = HN.w.data();
+    P.a = HN.a.data();
+    P.asort = HN.asort.data();
+    P.Pfp = HN.Pfp.data();
+    P.Pbp = HN.Pbp.data();
+    P.Pc = HN.Pc.data();
+    P.Pw = HN.Pw.data();
+    P.type_ok = HN.type_ok.data();
+    P.ctype = HC.ctype.data();
+    P.cap = HC.cap.data();
+    P.minm = HC.minm.data();
+    P.bw = HC.bw.data();
+    return P;
+}
+
+extern "C" void bpemu_set_plan_only(int v) { g_plan_only = v; }
+
+// bp_simulate_plan / bp_estimate_plan replayed on the host (timeline.cuh)
+extern "C" int bpemu_plan(const bp_network* nets, int n_nets, const bp_cluster* cls, int n_cls,
+                          const bp_plan_request* q, bp_timeline_result* tres, bp_event* events, int64_t cap,
+                          bp_rat* hw, bp_rat* ws, bp_rat* busy, bp_estimate_result* eres, bp_stage* st, int32_t* inf) {
+    std::string err;
+    HostNets HN;
+    HostCls HC;
+    if (!build_nets(nets, n_nets, HN, err, true) || !build_clusters(cls, n_cls, HC, err)) return BP_BAD_INPUT;
+    const Pools P = host_pools(HN, HC);
+    const int N = q->n_stages, clusterN = HC.desc[(size_t)q->cluster].N;
+    TlArgs A{};
+    A.v = net_view(P, q->network);
+    A.c = chain_view(P, q->cluster, N < clusterN ? N : clusterN);
+    A.N = N;
+    A.kind = q->kind;
+    A.clusterN = clusterN;
+    A.M = q->M;
+    A.micro = q->micro;
+    A.mini = q->mini_batches;
+    A.lo = q->lo;
+    A.hi = q->hi;
+    A.lead = reinterpret_cast<const Rat*>(q->lead);
+    A.trail = reinterpret_cast<const Rat*>(q->trail);
+    std::vector<Rat> F(N), Bv(N), W(N);
+    std::vector<int64_t> a(N), SR(N), off(N + 1);
+    if (eres) {   // estimate
+        std::vector<Rat> scr(7 * (size_t)N);
+        std::vector<int64_t> scr64(2 * (size_t)N);
+        *eres = bp_estimate_result{};
+        tl_estimate(A, *eres, st, inf, scr.data(), scr64.data());
+        return BP_OK;
+    }
+    const int64_t M = q->M > 0 ? q->M : 0, mini = q->mini_batches;
+    const size_t NM = (size_t)N * M, LM = (size_t)(N > 1 ? N - 1 : 0) * M;
+    const size_t nev = (size_t)mini * (2 * NM + 4 * LM);
+    std::vector<Rat> sF(NM + 1), eF(NM + 1), sB(NM + 1), eB(NM + 1), tFs(LM + 1), tFe(LM + 1), tBs(LM + 1),
+        tBe(LM + 1), mk(1);
+    std::vector<bp_event> ev(nev + 1), evt(nev + 1);
+    std::vector<TlPoint> pts(2 * M + 1), tmp(2 * M + 1);
+    std::vector<Rat> hwv(N), wsv(N), busyv(N);
+    A.F = F.data();
+    A.B = Bv.data();
+    A.W = W.data();
+    A.a = a.data();
+    A.SR = SR.data();
+    A.sF = sF.data();
+    A.eF = eF.data();
+    A.sB = sB.data();
+    A.eB = eB.data();
+    A.tFs = tFs.data();
+    A.tFe = tFe.data();
+    A.tBs = tBs.data();
+    A.tBe = tBe.data();
+    A.makespan1 = mk.data();
+    A.ev = ev.data();
+    A.ev_tmp = evt.data();
+    A.off = off.data();
+    bp_timeline_result r{};
+    r.status = BP_C_OK;
+    if (tl_chain(A, r) && tl_walk(A, r)) {
+        uint32_t code = 0;
+        for (int s = 1; s <= N && !code; ++s) code = tl_stage(A, s, pts.data(), tmp.data(), hwv.data(), wsv.data());
+        if (!code) code = tl_busy(A, busyv.data());
+        if (code) r.status = (int32_t)code;
+    }
+    *tres = r;
+    if (r.status == BP_C_OK) {
+        for (int64_t i = 0; i < r.n_events && i < cap; ++i) events[i] = ev[(size_t)i];
+        for (int s = 0; s < N; ++s) {
+            hw[s] = bp_rat{hwv[s].n, hwv[s].d};
+            ws[s] = bp_rat{wsv[s].n, wsv[s].d};
+            if (s + 1 < N) busy[s] = bp_rat{busyv[s].n, busyv[s].d};
+        }
+    }
+    return BP_OK;
+}
+
 extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_cluster* cls, int n_cls,
                                    const bp_query* qs, int nq, bp_query_result* res, bp_candidate* cand,
                                    bp_stage* stages, uint64_t* dp_work) {
@@ -195,6 +298,7 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
     for (int i = 0; i < nq; ++i)
         if (qs[i].cand_offset != HB.q[i].cand_off || qs[i].stage_offset != HB.q[i].stage_off) return BP_BAD_INPUT;
     BatchDev B{};
+    B.plan_only = g_plan_only;
     B.P.nets = HN.desc.data();
     B.P.cls = HC.desc.data();
     B.P.fp = HN.fp.data();
@@ -288,6 +392,18 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
         return 0;
     }
     for (int64_t c = 0; c < HB.ncand; ++c) prune_candidate(B, c);
+    if (B.plan_only) {   // `bapipe plan`: no simulation (k_plan_finish)
+        for (int64_t c = 0; c < HB.ncand; ++c)
+            if (B.cs[c].sim_ready && B.cand[c].status == C_PENDING) {
+                B.cand[c].status = BP_C_OK;
+                B.cand[c].makespan = bp_rat{0, 1};
+            }
+        for (int i = 0; i < nq; ++i) rank_query(B, i);
+        if (stages) for (int64_t i = 0; i < HB.nstage; ++i) stages[i] = B.stages[i];
+        for (int64_t i = 0; i < HB.ncand; ++i) cand[i] = B.cand[i];
+        for (int i = 0; i < nq; ++i) res[i] = B.res[i];
+        return 0;
+    }
     int64_t exact_n = 0, exact_ovf = 0, fast_n = 0;
     const size_t mn = (size_t)std::max(1, HB.max_N);
     std::vector<Rat> s_fr(mn), s_pf(mn), s_pb(mn), s_f(mn), s_b(mn);

@@ -1,4 +1,5 @@
-"""Golden outputs of the `bapipe` CLI (validate / explore) from the reference.
+"""Golden outputs of the `bapipe` CLI (validate / plan / explore / simulate)
+from the reference.
 
 Writes the input files under tests/golden/cli/ (networks and clusters of the
 reference's explorer unit tests, C1 and C3 of SURVEY.md 8d, a heterogeneous
@@ -6,7 +7,9 @@ random chain, and malformed / schema-violating inputs), then runs
 paper_2012_12544_b200/cli/bapipe.cpp built with -DUSE_REFERENCE against the
 reference headers (oracle/Makefile target `cli`) on every case, with argv[0] =
 "bapipe" and cwd = tests/golden/cli, and stores stdout, stderr, the exit code
-and any -o file in tests/golden/cli/expected.json.
+and any -o / --gantt file in tests/golden/cli/expected.json.  Plan files for
+`simulate` are hand-written (valid whole-layer and fractional plans, and
+invalid ones) or made by the reference's own `plan -o` (plan_c1/c3/rand).
 """
 import json
 import os
@@ -100,6 +103,23 @@ def write_inputs():
     for name, obj in files.items():
         with open(os.path.join(CLI_DIR, name), "w") as f:
             json.dump(obj, f, indent=1)
+    # plans for `simulate`
+    def stage(acc, lo, hi, lead="1", trail="1"):
+        return {"accelerator": acc, "layers": [lo, hi], "leading_fraction": lead, "trailing_fraction": trail}
+    plans = {
+        "plan_tri_whole.json": [stage("g0", 1, 1), stage("g1", 2, 2), stage("g2", 3, 3)],
+        "plan_tri_frac.json": [stage("g0", 1, 2, "1", "1/2"), stage("g1", 2, 3, "1/2", "1/3"),
+                               stage("g2", 3, 3, "2/3", "1")],
+        "plan_tri_twostage.json": [stage("g0", 1, 2), stage("g1", 3, 3)],
+        "plan_bad_range.json": [stage("g0", 1, 1), stage("g1", 2, 2), stage("g2", 3, 4)],
+        "plan_bad_cover.json": [stage("g0", 1, 2, "1", "1/2"), stage("g1", 2, 3, "1/3", "1"),
+                                stage("g2", 3, 3, "1/2", "1")],
+        "plan_bad_frac.json": [stage("g0", 1, 1), stage("g1", 2, 2, "1", "3/2"), stage("g2", 3, 3)],
+        "plan_bad_contig.json": [stage("g0", 1, 1), stage("g1", 3, 3), stage("g2", 3, 3)],
+    }
+    for name, st in plans.items():
+        with open(os.path.join(CLI_DIR, name), "w") as f:
+            json.dump({"stages": st}, f, indent=1)
     with open(os.path.join(CLI_DIR, "bad_syntax.json"), "w") as f:
         f.write('{"name": "x", "layers": [}\n')
     with open(os.path.join(CLI_DIR, "bad_array.json"), "w") as f:
@@ -131,18 +151,85 @@ CASES = [
     ["validate", "bad_array.json", "tri_roomy.json"],
     ["validate", "missing_file.json", "tri_roomy.json"],
     ["validate", "tri_net.json", "c3_cluster.json"],
+    # plan (tools/bapipe.cpp:152-190): balance_partition + estimate, no min-micro filter
+    ["plan", "tri_net.json", "tri_roomy.json", "--schedule", "1f1b-sno", "--micro", "4"],
+    ["plan", "tri_net.json", "tri_roomy.json", "--schedule", "1f1b-so", "--micro", "4", "--format", "json",
+     "-o", "best_plan.json"],
+    ["plan", "tri_net.json", "tri_roomy.json", "--schedule", "1f1b-sno", "--minibatch", "8"],
+    ["plan", "tri_net.json", "tri_floor.json", "--schedule", "1f1b-as", "--micro", "8", "--minibatch", "8",
+     "--format", "json"],
+    ["plan", "tri_net.json", "tri_floor.json", "--schedule", "fbp-as", "--micro", "2", "--minibatch", "8"],
+    ["plan", "tri_net.json", "tri_tight.json", "--schedule", "1f1b-so", "--micro", "2", "--minibatch", "8"],
+    ["plan", "tri_net.json", "tri_tiny.json", "--schedule", "1f1b-sno", "--micro", "2"],
+    ["plan", "tri_net.json", "tri_roomy.json", "--schedule", "1f1b-as", "--micro", "4"],
+    ["plan", "tri_net.json", "tri_roomy.json", "--schedule", "gpipe", "--micro", "4"],
+    ["plan", "tri_net.json", "tri_roomy.json", "--schedule", "1f1b-sno"],
+    ["plan", "tri_net.json", "tri_roomy.json", "--schedule", "1f1b-sno", "--micro", "3", "--minibatch", "8"],
+    ["plan", "c1_vgg16.json", "c1_cluster.json", "--schedule", "1f1b-sno", "--micro", "8", "--minibatch", "32",
+     "--format", "json"],
+    ["plan", "c3_gnmt.json", "c3_cluster.json", "--schedule", "1f1b-so", "--micro", "16", "--minibatch", "64"],
+    # simulate (tools/bapipe.cpp:234-256): full timeline, --trace / --gantt
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_whole.json", "--schedule", "1f1b-sno", "--micro", "4"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_whole.json", "--schedule", "1f1b-so", "--micro", "4",
+     "--format", "json", "--trace"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_whole.json", "--schedule", "1f1b-sno", "--micro", "3",
+     "--gantt", "gantt.csv"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_frac.json", "--schedule", "1f1b-so", "--micro", "3",
+     "--minibatch", "6", "--format", "json", "--trace", "--gantt", "gantt.svg"],
+    ["simulate", "tri_net.json", "tri_floor.json", "plan_tri_whole.json", "--schedule", "1f1b-as", "--micro", "4",
+     "--trace"],
+    ["simulate", "tri_net.json", "tri_floor.json", "plan_tri_frac.json", "--schedule", "fbp-as", "--micro", "5",
+     "--format", "json", "--trace"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_twostage.json", "--schedule", "1f1b-sno", "--micro", "2"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_bad_range.json", "--schedule", "1f1b-sno", "--micro", "2"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_bad_cover.json", "--schedule", "1f1b-sno", "--micro", "2"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_bad_frac.json", "--schedule", "1f1b-sno", "--micro", "2"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_bad_contig.json", "--schedule", "1f1b-sno", "--micro", "2"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_whole.json", "--schedule", "fbp-as", "--micro", "2"],
+    ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_whole.json", "--schedule", "1f1b-sno", "--micro", "3",
+     "--minibatch", "4"],
+    ["simulate", "c1_vgg16.json", "c1_cluster.json", "plan_c1.json", "--schedule", "1f1b-sno", "--micro", "8",
+     "--minibatch", "32", "--format", "json", "--trace"],
+    ["simulate", "c3_gnmt.json", "c3_cluster.json", "plan_c3.json", "--schedule", "1f1b-so", "--micro", "16",
+     "--minibatch", "64", "--gantt", "gantt.svg"],
+    ["simulate", "rand_net.json", "rand_cluster.json", "plan_rand.json", "--schedule", "RAND_KIND", "--micro", "16",
+     "--minibatch", "16", "--format", "json", "--trace"],
+    ["plan", "rand_net.json", "rand_cluster.json", "--schedule", "RAND_KIND", "--micro", "4", "--minibatch", "16"],
 ]
+
+# plans made by the reference's own `plan -o` (written before the cases run)
+PLAN_SOURCES = [
+    ("plan_c1.json", ["plan", "c1_vgg16.json", "c1_cluster.json", "--schedule", "1f1b-sno", "--micro", "8",
+                      "--minibatch", "32"]),
+    ("plan_c3.json", ["plan", "c3_gnmt.json", "c3_cluster.json", "--schedule", "1f1b-so", "--micro", "16",
+                      "--minibatch", "64"]),
+    ("plan_rand.json", ["plan", "rand_net.json", "rand_cluster.json", "--schedule", "RAND_KIND", "--micro", "16",
+                        "--minibatch", "16"]),
+]
+
+OUT_FILES = ("best_plan.json", "gantt.csv", "gantt.svg")
+
+
+def rand_kind():
+    with open(os.path.join(CLI_DIR, "rand_cluster.json")) as f:
+        return "1f1b-so" if json.load(f)["execution_mode"] == "sync" else "fbp-as"
+
+
+def resolve(args):
+    return [rand_kind() if a == "RAND_KIND" else a for a in args]
 
 
 def run_case(exe, args):
-    out_file = os.path.join(CLI_DIR, "best_plan.json")
-    if os.path.exists(out_file):
-        os.remove(out_file)
+    for name in OUT_FILES:
+        if os.path.exists(os.path.join(CLI_DIR, name)):
+            os.remove(os.path.join(CLI_DIR, name))
     p = subprocess.run(["bapipe"] + args, executable=exe, cwd=CLI_DIR, capture_output=True, text=True, timeout=600)
     rec = {"args": args, "rc": p.returncode, "stdout": p.stdout, "stderr": p.stderr}
-    if os.path.exists(out_file):
-        rec["out_file"] = open(out_file).read()
-        os.remove(out_file)
+    for name in OUT_FILES:
+        path = os.path.join(CLI_DIR, name)
+        if os.path.exists(path):
+            rec["out_file" if name == "best_plan.json" else name] = open(path).read()
+            os.remove(path)
     return rec
 
 
@@ -150,7 +237,11 @@ def main():
     write_inputs()
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "cli"], check=True)
     exe = os.path.join(ROOT, "oracle", "_ref", "bapipe_ref")
-    expected = [run_case(exe, c) for c in CASES]
+    for name, args in PLAN_SOURCES:
+        p = subprocess.run(["bapipe"] + resolve(args) + ["-o", name], executable=exe, cwd=CLI_DIR,
+                           capture_output=True, text=True, timeout=600)
+        assert p.returncode == 0, (name, p.stderr)
+    expected = [run_case(exe, resolve(c)) for c in CASES]
     with open(os.path.join(CLI_DIR, "expected.json"), "w") as f:
         json.dump(expected, f, indent=1)
     for r in expected:

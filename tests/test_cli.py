@@ -1,9 +1,10 @@
 """The `bapipe` CLI (paper_2012_12544_b200/cli/bapipe.cpp; SURVEY.md 8f rows
-F1, F2): JSON ingest with the reference's schema errors, canonical JSON /
+F1, F2, F3): validate / plan / explore / simulate (full timeline, --trace,
+--gantt csv/svg); JSON ingest with the reference's schema errors, canonical JSON /
 table reports, the run manifest and exit codes, against the reference's own
 outputs (tests/golden/make_cli_golden.py -> tests/golden/cli/expected.json).
-Every case compares stdout, stderr, the exit code and the -o plan file byte
-for byte.
+Every case compares stdout, stderr, the exit code and the -o / --gantt files
+byte for byte.
   * CPU: the CLI linked with tests/cpp/emu_abi_shim.cpp (kernel phase code
     replayed on the host);
   * GPU: the CLI linked with libbapipe_b200.so.
@@ -36,16 +37,19 @@ def build(out, extra):
 
 def check_all(exe, tmp_path):
     bad = []
+    out_files = ("best_plan.json", "gantt.csv", "gantt.svg")
     for want in expected():
-        out_file = os.path.join(CLI_DIR, "best_plan.json")
-        if os.path.exists(out_file):
-            os.remove(out_file)
+        for name in out_files:
+            if os.path.exists(os.path.join(CLI_DIR, name)):
+                os.remove(os.path.join(CLI_DIR, name))
         p = subprocess.run(["bapipe"] + want["args"], executable=exe, cwd=CLI_DIR, capture_output=True, text=True,
                            timeout=600)
         got = {"args": want["args"], "rc": p.returncode, "stdout": p.stdout, "stderr": p.stderr}
-        if os.path.exists(out_file):
-            got["out_file"] = open(out_file).read()
-            os.remove(out_file)
+        for name in out_files:
+            path = os.path.join(CLI_DIR, name)
+            if os.path.exists(path):
+                got["out_file" if name == "best_plan.json" else name] = open(path).read()
+                os.remove(path)
         if got != want:
             diff = [k for k in want if got.get(k) != want[k]] + [k for k in got if k not in want]
             bad.append((" ".join(want["args"]), diff, got.get("stderr", "")[:200]))
@@ -62,7 +66,10 @@ def test_cli_usage_errors(tmp_path):
     exe = str(tmp_path / "bapipe")
     build(exe, [os.path.join(ROOT, "tests", "cpp", "emu_abi_shim.cpp")])
     for args in (["explore", "tri_net.json", "tri_roomy.json"],        # --minibatch required
-                 ["plan", "tri_net.json", "tri_roomy.json"], ["frobnicate"], [],
+                 ["plan", "tri_net.json", "tri_roomy.json"],            # --schedule required
+                 ["simulate", "tri_net.json", "tri_roomy.json", "plan_tri_whole.json", "--schedule", "1f1b-sno"],
+                 ["simulate", "tri_net.json", "tri_roomy.json", "--schedule", "1f1b-sno", "--micro", "2"],
+                 ["frobnicate"], [],
                  ["explore", "tri_net.json", "tri_roomy.json", "--minibatch", "x"]):
         p = subprocess.run(["bapipe"] + args, executable=exe, cwd=CLI_DIR, capture_output=True, text=True)
         assert p.returncode == 1 and p.stdout == "", (args, p.stdout, p.stderr)
