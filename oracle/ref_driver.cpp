@@ -124,7 +124,37 @@ void classify_invalid(const std::string& m, bp_candidate& c) {
         auto p = m.find("sums to ") + 8;
         auto e = m.find(',', p);
         c.aux = R(rat_from_string(m.substr(p, e - p)));
+    } else if (m.find("stage count != cluster size") != std::string::npos) {
+        c.detail = BP_IP_STAGE_COUNT;
+        c.detail2 = 0;
+    } else if (m.find("M >= 1 required") != std::string::npos) {
+        c.detail = BP_IP_M;
+        c.detail2 = 0;
     } else c.detail = 0;
+}
+
+PartitionPlan to_plan(const bp_plan_request& q) {
+    PartitionPlan p;
+    for (int s = 0; s < q.n_stages; ++s)
+        p.stages.push_back({"d" + std::to_string(s), q.lo[s], q.hi[s], Rat(q.lead[s].num, q.lead[s].den),
+                            Rat(q.trail[s].num, q.trail[s].den)});
+    return p;
+}
+
+// outcome of a reference call on one plan, as the ABI status codes
+template <class F>
+int32_t run_plan_call(F&& f, bp_candidate& c) {
+    try {
+        f();
+        return BP_C_OK;
+    } catch (const InvalidPlan& e) {
+        classify_invalid(e.what(), c);
+        return BP_C_ERR_INVALID_PLAN;
+    } catch (const std::overflow_error&) {
+        return BP_C_ERR_OVERFLOW;
+    } catch (const std::domain_error&) {
+        return BP_C_ERR_DOMAIN;
+    }
 }
 
 struct QueryCtx {
@@ -350,6 +380,66 @@ int bpref_explore_timed(const bp_network* nets, int n_nets, const bp_cluster* cl
         std::vector<std::thread> pool;
         for (int t = 0; t < threads; ++t) pool.emplace_back(work);
         for (auto& th : pool) th.join();
+    }
+    return BP_OK;
+}
+
+// simulate() / estimate() of one plan (simulator.hpp:264-274,
+// cost_models.hpp:124-166): the reference side of bp_simulate_plan /
+// bp_estimate_plan.  The caller guarantees a mode-compatible kind.
+int bpref_simulate_plan(const bp_network* nets, int, const bp_cluster* cls, int, const bp_plan_request* q,
+                        bp_timeline_result* res, bp_event* ev, int64_t cap, bp_rat* hw, bp_rat* ws, bp_rat* busy) {
+    NetworkProfile net = to_network(nets[q->network]);
+    ClusterSpec cl = to_cluster(cls[q->cluster], 0);
+    PartitionPlan plan = to_plan(*q);
+    Timeline t;
+    bp_candidate c{};
+    std::memset(res, 0, sizeof(*res));
+    res->status = run_plan_call(
+        [&] { t = simulate((ScheduleKind)q->kind, plan, net, cl, q->M, q->micro, q->mini_batches); }, c);
+    if (res->status == BP_C_ERR_INVALID_PLAN) {
+        res->detail = c.detail;
+        res->detail2 = c.detail2;
+        res->aux = c.aux;
+    }
+    if (res->status != BP_C_OK) return BP_OK;
+    res->makespan = R(t.makespan);
+    res->n_events = (int64_t)t.events.size();
+    for (int64_t i = 0; i < res->n_events && i < cap; ++i) {
+        const Event& e = t.events[(size_t)i];
+        ev[i] = bp_event{e.stage, (int32_t)e.kind, 0, e.micro_batch, R(e.start), R(e.end)};
+    }
+    for (size_t s = 0; s < t.per_stage_feature_highwater.size(); ++s) {
+        hw[s] = R(t.per_stage_feature_highwater[s]);
+        ws[s] = R(t.per_stage_weight_static[s]);
+    }
+    for (size_t k = 0; k < t.per_link_busy_fraction.size(); ++k) busy[k] = R(t.per_link_busy_fraction[k]);
+    return BP_OK;
+}
+
+int bpref_estimate_plan(const bp_network* nets, int, const bp_cluster* cls, int, const bp_plan_request* q,
+                        bp_estimate_result* res, bp_stage* st, int32_t* inf) {
+    NetworkProfile net = to_network(nets[q->network]);
+    ClusterSpec cl = to_cluster(cls[q->cluster], 0);
+    PartitionPlan plan = to_plan(*q);
+    CostEstimate e;
+    bp_candidate c{};
+    std::memset(res, 0, sizeof(*res));
+    res->status = run_plan_call([&] { e = estimate((ScheduleKind)q->kind, plan, net, cl, q->M, q->micro); }, c);
+    if (res->status != BP_C_OK) return BP_OK;
+    res->heuristic = e.heuristic ? 1 : 0;
+    res->minibatch_time = R(e.minibatch_time);
+    res->bubble_fraction = R(e.bubble_fraction);
+    for (int s = 0; s < q->n_stages; ++s) {
+        st[s] = bp_stage{};
+        st[s].lo = q->lo[s];
+        st[s].hi = q->hi[s];
+        st[s].lead = q->lead[s];
+        st[s].trail = q->trail[s];
+        st[s].features = R(e.features_mem[(size_t)s]);
+        st[s].weights = R(e.weights_mem[(size_t)s]);
+        st[s].bw_demand = s + 1 < q->n_stages ? R(e.bandwidth_demand[(size_t)s]) : bp_rat{0, 1};
+        inf[s] = e.mem_infeasible[(size_t)s] ? 1 : 0;
     }
     return BP_OK;
 }

@@ -104,6 +104,24 @@ class Explorer:
         if rc != 0:
             raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
 
+    def plan_call(self, req, which, cap=0):
+        """bp_simulate_plan (which='simulate') or bp_estimate_plan on a
+        bp_plan_request for this context's loaded problem.  Returns the raw
+        result records (see tests/timeline_util.py)."""
+        n = req.n_stages
+        if which == "simulate":
+            res = abi.bp_timeline_result()
+            ev = (abi.bp_event * max(cap, 1))()
+            hw, ws, busy = (abi.bp_rat * n)(), (abi.bp_rat * n)(), (abi.bp_rat * max(n - 1, 1))()
+            self._check(self.lib.bp_simulate_plan(self.ctx, C.byref(req), C.byref(res), ev, cap, hw, ws, busy),
+                        "bp_simulate_plan")
+            return res, ev, hw, ws, busy
+        res = abi.bp_estimate_result()
+        st = (abi.bp_stage * n)()
+        inf = (C.c_int32 * n)()
+        self._check(self.lib.bp_estimate_plan(self.ctx, C.byref(req), C.byref(res), st, inf), "bp_estimate_plan")
+        return res, st, inf
+
     def kernel_stats(self):
         cap = 64
         names = C.create_string_buffer(48 * cap)
