@@ -646,8 +646,14 @@ BPK_HD int refine_fast_step_body(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_t
         while (uk * ud > un) --uk;
         while ((uk + 1) * ud <= un) ++uk;
         const int64_t k = (int64_t)uk, kc = k + (uk * ud != un ? 1 : 0);
-        Err le{ERR_NONE};
-        const Rat qlo = rat_nd(k, 1024, le), qhi = rat_nd(kc, 1024, le);
+        // k / 1024 reduced: the gcd is a power of two (0 <= k <= 1024)
+        auto over1024 = [](int64_t q) {
+            if (q == 0) return Rat{0, 1};
+            int tz = bpk_ffs64((long long)q) - 1;
+            tz = tz < 10 ? tz : 10;
+            return Rat{q >> tz, (int64_t)1024 >> tz};
+        };
+        const Rat qlo = over1024(k), qhi = over1024(kc);
         if (rat_ge(qhi, avail)) {
             x = qlo;
         } else {
@@ -731,6 +737,10 @@ BPK_HDNI StepOut refine_exact_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c
 // stage_bp_time, plan.hpp:90-113) cannot overflow: every partial sum is at
 // most t and its reduced denominator divides den(lead) * den(trail).
 BPK_HD bool stage_time_safe(Rat t, Rat lead, Rat trail) {
+    // a double estimate settles all but the borderline cases
+    const double x = (double)t.n * (double)lead.d * (double)trail.d, y = 0x1p62 * (double)t.d;
+    if (x < y * (1 - 0x1p-40)) return true;
+    if (x > y * (1 + 0x1p-40)) return false;
     return (i128)t.n * lead.d * trail.d < ((i128)1 << 62) * t.d;
 }
 

@@ -12,6 +12,7 @@
 // Errors do not throw: the first error is latched into an Err word and the
 // caller stops at its next check (exception emulation, first-error-wins).
 #pragma once
+#include <math.h>
 #include <stdint.h>
 
 // The emulation code is __host__ __device__ so tests/emu can run it on the
@@ -435,6 +436,13 @@ BPK_HD Rat rat_div(Rat a, Rat b, Err& e) {
 BPK_HD bool rat_eq(Rat a, Rat b) { return a.n == b.n && a.d == b.d; }
 BPK_HD bool rat_lt(Rat a, Rat b) {
     if (a.d == b.d) return a.n < b.n;
+    // the cross products in double decide unless they are within a few ulps
+    // of each other (each carries a relative error below 2^-51); otherwise
+    // the exact 128-bit products do
+    const double x = (double)a.n * (double)b.d, y = (double)b.n * (double)a.d;
+    const double m = 0x1p-48 * fmax(fabs(x), fabs(y));
+    if (x < y - m) return true;
+    if (x > y + m) return false;
     return (i128)a.n * b.d < (i128)b.n * a.d;
 }
 BPK_HD bool rat_gt(Rat a, Rat b) { return rat_lt(b, a); }
