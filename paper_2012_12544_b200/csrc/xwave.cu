@@ -126,36 +126,29 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
                 const bool out_ok = op.is_f ? (s + 1 >= N || vs.consF[s + 1] >= m - FLOW_Q)
                                             : (s == 0 || vs.consB[s - 1] >= m - FLOW_Q);
                 if (in_ok && out_ok) {
+                    // one code path for F and B lanes (operands selected, not
+                    // branched), so a warp with both kinds of op runs each
+                    // Rat operation once
                     __threadfence_block();
+                    const bool f = op.is_f;
+                    const bool has_in = f ? s > 0 : s + 1 < N;
+                    const bool has_out = f ? s + 1 < N : s > 0;
                     Rat ready = fr;
-                    if (op.is_f) {
-                        if (s > 0) {
-                            const Rat arr{vs.qF[s][k].n, vs.qF[s][k].d};
-                            vs.consF[s] = m;
-                            if (rat_gt(arr, ready)) ready = arr;
-                        }
-                        fr = rat_add(ready, Fd, e);
-                        if (s + 1 < N) {
-                            const Rat out = async ? fr : rat_add(fr, R(srlink), e);
-                            vs.qF[s + 1][k].n = out.n;
-                            vs.qF[s + 1][k].d = out.d;
-                            __threadfence_block();
-                            vs.prodF[s + 1] = m;
-                        }
-                    } else {
-                        if (s + 1 < N) {
-                            const Rat arr{vs.qB[s][k].n, vs.qB[s][k].d};
-                            vs.consB[s] = m;
-                            if (rat_gt(arr, ready)) ready = arr;
-                        }
-                        fr = rat_add(ready, Bd, e);
-                        if (s > 0) {
-                            const Rat out = async ? fr : rat_add(fr, R(srin), e);
-                            vs.qB[s - 1][k].n = out.n;
-                            vs.qB[s - 1][k].d = out.d;
-                            __threadfence_block();
-                            vs.prodB[s - 1] = m;
-                        }
+                    if (has_in) {
+                        volatile Rat* q = f ? &vs.qF[s][k] : &vs.qB[s][k];
+                        const Rat arr{q->n, q->d};
+                        *(f ? &vs.consF[s] : &vs.consB[s]) = m;
+                        if (rat_gt(arr, ready)) ready = arr;
+                    }
+                    fr = rat_add(ready, f ? Fd : Bd, e);
+                    if (has_out) {
+                        const Rat out = async ? fr : rat_add(fr, R(f ? srlink : srin), e);
+                        const int t = f ? s + 1 : s - 1;
+                        volatile Rat* q = f ? &vs.qF[t][k] : &vs.qB[t][k];
+                        q->n = out.n;
+                        q->d = out.d;
+                        __threadfence_block();
+                        *(f ? &vs.prodF[t] : &vs.prodB[t]) = m;
                     }
                     ran = true;
                     if (++p == 2 * M) done = true;
