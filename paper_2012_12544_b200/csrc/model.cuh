@@ -609,6 +609,65 @@ BPK_HD Rat reduce_pos(i128 n, i128 d) {       // n >= 0, d > 0, both < 2^62
     return Rat{(int64_t)udiv_exact64((uint64_t)n, g), (int64_t)udiv_exact64((uint64_t)d, g)};
 }
 
+// The same step when the common scale D < 2^31, both stage times are below
+// 2^20 and c_from + c_to < 2^20: then every scaled quantity below is under
+// 2^62 by construction (Th, Tl < 2^51; D*cs < 2^51; x*1024 and the scores
+// < 2^62; at acceptance den(x) <= 1024), so the step runs in int64 with no
+// per-product checks.  Returns -1 when the bounds do not hold.
+BPK_HD int refine_small_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat& x, Rat& nh, Rat& nl) {
+    const int64_t B31 = (int64_t)1 << 31, B20 = (int64_t)1 << 20;
+    if (t_hi.d >= B31 || t_lo.d >= B31 || c_from >= B20 / 2 || c_to >= B20 / 2) return -1;
+    if (t_hi.n >= (t_hi.d << 20) || t_lo.n >= (t_lo.d << 20)) return -1;
+    const uint32_t g = gcd_u32((uint32_t)t_hi.d, (uint32_t)t_lo.d);
+    const int64_t mh = (uint32_t)t_lo.d / g, ml = (uint32_t)t_hi.d / g;
+    const int64_t D = t_hi.d * mh;
+    if (D >= B31) return -1;
+    const int64_t cs = c_from + c_to;
+    const int64_t Th = t_hi.n * mh, Tl = t_lo.n * ml;   // < 2^20 * D < 2^51
+    x = reduce_pos(Th - Tl, D * cs);
+    if (!rat_lt(x, avail)) {
+        // x = avail - Rat(1, 1024)
+        if (avail.d >= ((int64_t)1 << 40) || avail.n >= ((int64_t)1 << 40)) return -1;
+        Err le{ERR_NONE};
+        x = rat_sub(avail, Rat{1, 1024}, le);
+        if (le.bad()) return -1;
+        if (x.n <= 0) return FS_NOMOVE;
+    }
+    if (x.d > 1024) {                                     // quantize (257-265)
+        if (x.d >= ((int64_t)1 << 51)) return -1;
+        const int64_t num = x.n * 1024;                   // x < avail <= 1: x.n < x.d
+        const uint64_t un = (uint64_t)num, ud = (uint64_t)x.d;
+        uint64_t uk = (uint64_t)((double)un / (double)ud);
+        while (uk * ud > un) --uk;
+        while ((uk + 1) * ud <= un) ++uk;
+        const int64_t k = (int64_t)uk, kc = k + (uk * ud != un ? 1 : 0);
+        auto over1024 = [](int64_t q) {
+            if (q == 0) return Rat{0, 1};
+            int tz = bpk_ffs64((long long)q) - 1;
+            tz = tz < 10 ? tz : 10;
+            return Rat{q >> tz, (int64_t)1024 >> tz};
+        };
+        const Rat qlo = over1024(k), qhi = over1024(kc);
+        if (rat_ge(qhi, avail)) {
+            x = qlo;
+        } else {
+            const int64_t a1 = Th * 1024 - k * c_from * D, a2 = Tl * 1024 + k * c_to * D;
+            const int64_t b1 = Th * 1024 - kc * c_from * D, b2 = Tl * 1024 + kc * c_to * D;
+            const int64_t s_lo = a1 > a2 ? a1 : a2, s_hi = b1 > b2 ? b1 : b2;
+            x = s_lo <= s_hi ? qlo : qhi;
+        }
+    }
+    if (x.n <= 0 || !rat_lt(x, avail)) return FS_NOMOVE;
+    if (x.d > 1024) return -1;                            // (not reached: den(x) <= 1024 here)
+    const int64_t Dx = D * x.d;
+    const int64_t TH = Th * x.d, NH = TH - x.n * c_from * D, NL = Tl * x.d + x.n * c_to * D;
+    if ((NH > NL ? NH : NL) >= TH) return FS_NOMOVE;
+    if (NH < 0) return -1;
+    nh = reduce_pos(NH, Dx);
+    nl = reduce_pos(NL, Dx);
+    return FS_MOVE;
+}
+
 // Every product below is formed from two int64 factors already checked
 // against 2^62 (64x64 -> 128-bit multiplies only: a 128x128 product is ~60
 // instructions and this step runs millions of times).
@@ -616,6 +675,8 @@ BPK_HD int refine_fast_step_body(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_t
                                  Rat& nl) {
     const i128 B62 = (i128)1 << 62;
     if (t_hi.n < 0 || t_lo.n < 0 || avail.n <= 0) return FS_FALLBACK;
+    const int small = refine_small_step(t_hi, t_lo, c_from, c_to, avail, x, nh, nl);
+    if (small >= 0) return small;
     const uint64_t g = gcd_u64((uint64_t)t_hi.d, (uint64_t)t_lo.d);
     const int64_t mh = (int64_t)udiv_exact64((uint64_t)t_lo.d, g), ml = (int64_t)udiv_exact64((uint64_t)t_hi.d, g);
     const i128 D128 = (i128)t_hi.d * mh;
