@@ -748,7 +748,7 @@ struct StepOut {
     uint32_t err;
     Rat x, nh, nl;
 };
-BPK_HDNI StepOut refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail) {
+BPK_HD StepOut refine_fast_step(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail) {
     StepOut o{};
     o.fs = refine_fast_step_body(t_hi, t_lo, c_from, c_to, avail, o.x, o.nh, o.nl);
     return o;

@@ -137,8 +137,7 @@ BPK_HD uint32_t umod_u64_u32(uint64_t x, uint32_t m) {
 
 // out of line: inlined at its ~20 call sites it dominated the kernels' code
 // size (instruction-cache misses were the top stall in refine and prune)
-BPK_HDNI uint64_t gcd_u64(uint64_t u, uint64_t v) {
-    if (((u | v) >> 32) == 0) return gcd_u32((uint32_t)u, (uint32_t)v);
+BPK_HDNI uint64_t gcd_u64_wide(uint64_t u, uint64_t v) {
     if (u == 0) return v;
     if (v == 0) return u;
     const uint64_t o = u | v;
@@ -161,6 +160,12 @@ BPK_HDNI uint64_t gcd_u64(uint64_t u, uint64_t v) {
         v = hi - lo;
     } while (v != 0);
     return u << shift;
+}
+
+// the common case (both below 2^32) inline, the wide one out of line
+BPK_HD uint64_t gcd_u64(uint64_t u, uint64_t v) {
+    if (((u | v) >> 32) == 0) return gcd_u32((uint32_t)u, (uint32_t)v);
+    return gcd_u64_wide(u, v);
 }
 
 // a / g for g dividing a exactly: shift out the twos, multiply by the
