@@ -123,3 +123,41 @@ def test_ranked_lists_sorted_on_c5_sample(ex):
                 for c in ranked]
         assert keys == sorted(keys)
         assert (res[qi]["status"] == 0) == bool(ranked)
+
+
+def test_plan_only_matches_explore(ex):
+    """BP_OPT_PLAN_ONLY (`bapipe plan`: balance_partition + estimate, no
+    min-micro filter, no simulation) agrees with the full explore on every
+    candidate both evaluate: the same plan, estimate and prune-phase outcome;
+    candidates explore drops at simulate() are feasible plans here."""
+    import ctypes as C
+    from paper_2012_12544_b200 import abi
+    sim_phase = {0, 7, 8, 9}                     # OK, or an error raised by simulate()
+    for p in (scenarios.c5_sample(61), W.random_problem(3, n_queries=80, max_L=30, max_N=12,
+                                                          cap_range=(1000, 60000), bw_range=(1, 500),
+                                                          act_max=3000)):
+        _, full, full_st = ex.explore(p, details=True)
+        assert ex.lib.bp_set_option(ex.ctx, abi.BP_OPT_PLAN_ONLY, 1) == 0
+        try:
+            _, po, po_st = ex.explore(p, details=True)
+        finally:
+            ex.lib.bp_set_option(ex.ctx, abi.BP_OPT_PLAN_ONLY, 0)
+        n_ok = 0
+        for qi in range(p.queries.size):
+            lo = int(p.queries["cand_offset"][qi])
+            N = int(p.queries["n_stages"][qi]) or p.clusters[int(p.queries["cluster"][qi])].N
+            so = int(p.queries["stage_offset"][qi])
+            for i in range(lo, lo + int(p.n_candidates[qi])):
+                f, g = full[i], po[i]
+                if f["status"] == 1:                 # min-micro: not evaluated by explore
+                    continue
+                if f["status"] in sim_phase and g["status"] == 0:
+                    if f["status"] == 0:
+                        n_ok += 1
+                        for k in ("est_minibatch", "bubble", "heuristic", "peak_memory", "max_bw_demand"):
+                            assert f[k].tobytes() == g[k].tobytes(), (qi, i, k)
+                        s0 = so + (i - lo) * N
+                        assert full_st[s0:s0 + N].tobytes() == po_st[s0:s0 + N].tobytes(), (qi, i)
+                    continue
+                assert f["status"] == g["status"] and f["detail"] == g["detail"], (qi, i, f, g)
+        assert n_ok > 0
