@@ -6,14 +6,21 @@
 //                      stage_*_time's per-call sums, partition.hpp:78-131,
 //                      plan.hpp:90-132)
 //   k_setup        K0  candidate records, thread per query
+//   k_sched_*          scheduling orders (CUB radix sort of query keys)
+//   k_dedup_*          batch classes: one DP / refine per (network, N, types)
 //   k_bottleneck   K1b comm-bottleneck test, a_th, coarse block count; queues
-//                      the coarse DP items (thread per query)
-//   k_refine       K3a intra_layer_refine, thread per query
-//   k_prune        K3b balance_partition branches + estimate + memory
-//                      fine-tune, thread per candidate
-//   k_sim          K4  schedule simulation, thread per candidate
+//                      one coarse DP per distinct (class, a_th)
+//   k_refine_smem  K3a intra_layer_refine, a warp (lane 0) per class
+//                      representative, caches in shared memory; k_refine is
+//                      the thread-per-query global-memory variant
+//   k_prune*       K3b balance_partition branches + estimate + memory
+//                      fine-tune: keys, compacted lists, persistent warps;
+//                      first estimates shared across capacity tiers
+//   k_plan_finish      BP_OPT_PLAN_ONLY: candidates stop after the estimate
 //   k_rank         K5  ranking / query outcome, thread per query
 //   k_best             argmin of the per-query bests (multi-GPU exchange record)
+// The simulators (K4) are in sim.cu and xwave.cu, the DP (K2) in dp.cu, the
+// one-plan timeline / estimate (F3) in timeline.cu.
 #include <cub/cub.cuh>
 
 #include "kernels.h"

@@ -503,7 +503,7 @@ void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st) {
     k_xsort_count<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);
     k_xsort_scan<<<1, 1024, 0, st>>>(B);
     k_xsort_scatter<<<blocks_for(B.ncand, 256), 256, 0, st>>>(B);
-    static const int wps = getenv("BP_XSIM_WPS") ? atoi(getenv("BP_XSIM_WPS")) : XSIM_WARPS_PER_SM;   // EXPERIMENT
+    const int wps = XSIM_WARPS_PER_SM;
     k_sim_exact<<<sms * wps / 8, 256, 0, st>>>(B);
 }
 
