@@ -8,6 +8,8 @@
 // the reference performs is bounds-checked (so its undefined behaviour is
 // reported, not silently different).  The first error wins.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace bpk {
@@ -107,9 +109,19 @@ BPK_HD int64_t link_sr(const PS& p, const NetView& v, const ChainView& c, int k0
 }
 
 // estimate(kind, plan, net, cluster, M, micro), cost_models.hpp:124-166.
+BPK_HD bool ft_int_ok(const NetView& v, const ChainView& c, int64_t M, int64_t micro);
+BPK_HD void estimate_whole_int(const WholePlan& p, const NetView& v, const ChainView& c, int kind, int64_t M,
+                               int64_t micro, const EstScratch& s, EstOut& o, Err& e);
+
 template <class PS>
 BPK_HD void estimate_body(const PS& p, const NetView& v, const ChainView& c, int kind, int64_t M, int64_t micro,
                          const EstScratch& s, EstOut& o, const EstStageOut* so, Err& e) {
+    if constexpr (std::is_same<PS, WholePlan>::value) {
+        if (!so && ft_int_ok(v, c, M, micro)) {   // every value an integer in range: int64 (below)
+            estimate_whole_int(p, v, c, kind, M, micro, s, o, e);
+            return;
+        }
+    }
     const int N = c.N;
     // stage_costs (103-119), stage order F, B, w, a, SR
     for (int i = 0; i < N; ++i) {
@@ -381,6 +393,71 @@ BPK_HD bool ft_int_ok(const NetView& v, const ChainView& c, int64_t M, int64_t m
     const i128 mem = 2 * (i128)N * A + 2 * (i128)v.Pw[v.L];
     if ((i128)N * mem >= lim) return false;
     return (i128)(M + N) * ((i128)ft + bt) + 4 * (i128)(M + N) * A < lim;
+}
+
+// estimate() (cost_models.hpp:124-166) of a whole-layer plan under ft_int_ok:
+// every value it forms is an integer below 2^61, so the same values come from
+// int64 arithmetic and no operation can raise (the UB reads are checked as
+// in the exact path, in the same order).  Of the outputs only the bubble
+// fraction and the largest bandwidth demand are fractions: every link's
+// demand has the same denominator (Fm, or Fm + Bm for fbp-as), so the largest
+// cut activation gives the largest demand -- one reduction each instead of
+// one per link.
+BPK_HD void estimate_whole_int(const WholePlan& p, const NetView& v, const ChainView& c, int kind, int64_t M,
+                               int64_t micro, const EstScratch& s, EstOut& o, Err& e) {
+    const int N = c.N;
+    for (int i = 0; i < N; ++i) {   // stage_costs (103-119)
+        p.FBW(i, s.F[i], s.B[i], s.W[i], e);
+        if (e.bad()) return;
+        const int64_t act = (i >= 1) ? act_at(v, p.H(i - 1), e) : act_at(v, p.H(0), e);
+        if (e.bad()) return;
+        s.A[i] = act * micro;
+        s.SR[i] = (i >= 1) ? link_sr(p, v, c, i - 1, micro, e) : 0;
+        if (e.bad()) return;
+    }
+    int64_t Fm = 0, Bm = 0, SRm = 0;
+    bool balanced = true;
+    for (int i = 0; i < N; ++i) {
+        if (s.F[i].n != s.F[0].n || s.B[i].n != s.B[0].n) balanced = false;
+        if (s.F[i].n > Fm) Fm = s.F[i].n;
+        if (s.B[i].n > Bm) Bm = s.B[i].n;
+        if (s.SR[i] > SRm) SRm = s.SR[i];
+    }
+    for (int i = 1; i < N; ++i)
+        if (s.SR[i] != s.SR[N > 1 ? 1 : 0]) balanced = false;
+    o.Fm = R(Fm);
+    o.Bm = R(Bm);
+    int64_t mb = (M + N - 1) * (Fm + Bm);                         // minibatch_time (50-63)
+    if (kind == KIND_SNO) mb += (N + M - 2 - ceil_div64(M - 1, N)) * 2 * SRm;
+    else if (kind == KIND_SO) mb += (int64_t)(N - 1) * 2 * SRm;
+    o.minibatch = R(mb);
+    if (N == 1) o.bubble = Rat{0, 1};                               // bubble_fraction (65-82)
+    else if (kind == KIND_SNO)
+        o.bubble = rat_div(R((int64_t)(N - 1) * (Fm + Bm + 2 * SRm) + (M - 1 - ceil_div64(M - 1, N)) * 2 * SRm),
+                           R(mb), e);
+    else if (kind == KIND_SO) o.bubble = rat_div(R((int64_t)(N - 1) * (Fm + Bm + 2 * SRm)), R(mb), e);
+    else o.bubble = rat_nd(N - 1, M + N - 1, e);
+    o.heuristic = (!balanced || M < N) ? 1 : 0;
+    if (e.bad()) return;
+    o.feasible = 1;
+    const int64_t fmul = (kind == KIND_FBP || kind == KIND_SO) ? 2 : 1;
+    int64_t peak = 0;
+    for (int i = 0; i < N; ++i) {                                   // memory check (152-160)
+        const int64_t mem = (int64_t)(N - i) * s.A[i] * fmul + 2 * s.W[i].n;
+        s.Mem[i] = R(mem);
+        if (mem > c.cap[i]) o.feasible = 0;
+        if (mem > peak) peak = mem;
+    }
+    o.peak_mem = R(peak);
+    int64_t amax = 0;                                               // bandwidth_demand (161-164)
+    for (int k = 0; k + 1 < N; ++k) {
+        const int64_t a = act_at(v, p.H(k), e) * micro;
+        if (e.bad()) return;
+        if (a > amax) amax = a;
+    }
+    if (N < 2) o.max_bw = Rat{0, 1};
+    else if (kind == KIND_FBP) o.max_bw = rat_div(R(2 * amax), R(Fm + Bm), e);
+    else o.max_bw = rat_div(R(amax), R(Fm), e);
 }
 
 // memory_fine_tune's trial loop (partition.hpp:375-433) under ft_int_ok: the
