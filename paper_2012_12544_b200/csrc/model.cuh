@@ -167,6 +167,29 @@ BPK_HD void estimate_body(const PS& p, const NetView& v, const ChainView& c, int
     }
     // bandwidth_demand (97-100) per link (161-164)
     o.max_bw = Rat{0, 1};
+    if (!so && N > 1) {
+        // every link's demand is a / Fm (2a / (Fm + Bm) for fbp-as): one
+        // denominator, so the largest cut activation gives the largest
+        // demand.  When a_max * den(Fm) < 2^62 no link's quotient can leave
+        // int64, and the first error (if any) is the first out-of-range layer
+        // read, exactly as the per-link loop would raise them.
+        int64_t amax = 0;
+        int kub = N - 1;
+        for (int k = 0; k + 1 < N; ++k) {
+            const int64_t j = p.H(k);
+            if (j < 1 || j > v.L) { kub = k; break; }
+            const int64_t a = v.a[j - 1] * micro;
+            if (a > amax) amax = a;
+        }
+        Err le{ERR_NONE};
+        const Rat den = (kind == KIND_FBP) ? rat_add(Fm, Bm, le) : Fm;
+        const i128 top = (kind == KIND_FBP) ? 2 * (i128)amax : (i128)amax;
+        if (!le.bad() && den.n > 0 && amax >= 0 && top * den.d < ((i128)1 << 62)) {
+            if (kub < N - 1) { e.set(ERR_UB); return; }
+            o.max_bw = rat_div(R((int64_t)top), den, e);
+            return;
+        }
+    }
     for (int k = 0; k + 1 < N; ++k) {
         Rat a = R(act_at(v, p.H(k), e) * micro);
         Rat d;
