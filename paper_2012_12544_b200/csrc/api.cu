@@ -103,6 +103,7 @@ struct bp_ctx {
     HostCls hc;
     bool have_nets = false, have_cls = false;
     DevBuf nets_mem, cls_mem;
+    HostPinned stage_tables;   // pinned staging of the network / cluster tables
     Pools P{};
     int max_T = 1;
     bool prof = false;
@@ -186,16 +187,21 @@ int upload_networks(bp_ctx* c) {
     size_t o_w = L.take<int64_t>(H.w.size());
     size_t o_a = L.take<int64_t>(H.a.size());
     size_t o_as = L.take<int64_t>(H.asort.size());
-    size_t o_Pfp = L.take<int64_t>(H.Pfp.size());
-    size_t o_Pbp = L.take<int64_t>(H.Pbp.size());
-    size_t o_Pc = L.take<int64_t>(H.Pc.size());
-    size_t o_Pw = L.take<int64_t>(H.Pw.size());
+    size_t o_Pfp = L.take<int64_t>(H.n_tpref);
+    size_t o_Pbp = L.take<int64_t>(H.n_tpref);
+    size_t o_Pc = L.take<int64_t>(H.n_tpref);
+    size_t o_Pw = L.take<int64_t>(H.n_pref);
     size_t o_tok = L.take<uint8_t>(H.type_ok.size());
     if (!c->nets_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(networks)");
+    if (!c->stage_tables.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(tables)");
     void* b = c->nets_mem.p;
+    // through pinned staging (one DMA per table, no pageable bounce)
     auto up = [&](size_t off, const void* src, size_t bytes) {
         c->h2d += (int64_t)bytes;
-        return bytes ? cudaMemcpy(dptr<char>(b, off), src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+        if (!bytes) return cudaSuccess;
+        std::memcpy(static_cast<char*>(c->stage_tables.p) + off, src, bytes);
+        return cudaMemcpyAsync(dptr<char>(b, off), static_cast<char*>(c->stage_tables.p) + off, bytes,
+                               cudaMemcpyHostToDevice, 0);
     };
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(NetDesc));
@@ -242,16 +248,21 @@ int upload_clusters(bp_ctx* c) {
     size_t o_mm = L.take<int64_t>(H.minm.size());
     size_t o_bw = L.take<int64_t>(H.bw.size());
     if (!c->cls_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(clusters)");
+    if (!c->stage_tables.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(tables)");
     void* b = c->cls_mem.p;
     auto up = [&](size_t off, const void* src, size_t bytes) {
         c->h2d += (int64_t)bytes;
-        return bytes ? cudaMemcpy(dptr<char>(b, off), src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+        if (!bytes) return cudaSuccess;
+        std::memcpy(static_cast<char*>(c->stage_tables.p) + off, src, bytes);
+        return cudaMemcpyAsync(dptr<char>(b, off), static_cast<char*>(c->stage_tables.p) + off, bytes,
+                               cudaMemcpyHostToDevice, 0);
     };
     cudaError_t e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(ClDesc));
     if (e == cudaSuccess) e = up(o_t, H.ctype.data(), H.ctype.size() * 4);
     if (e == cudaSuccess) e = up(o_cap, H.cap.data(), H.cap.size() * 8);
     if (e == cudaSuccess) e = up(o_mm, H.minm.data(), H.minm.size() * 8);
     if (e == cudaSuccess) e = up(o_bw, H.bw.data(), H.bw.size() * 8);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);   // the staging buffer is reused
     if (e != cudaSuccess) return cuda_fail(c, e, "upload clusters");
     c->P.cls = dptr<ClDesc>(b, o_desc);
     c->P.ctype = dptr<int32_t>(b, o_t);
@@ -583,6 +594,7 @@ void bp_destroy(bp_ctx* c) {
     if (c->cached) bp_batch_free(c, c->cached);
     c->nets_mem.release();
     c->cls_mem.release();
+    c->stage_tables.release();
     for (auto e : c->event_pool) cudaEventDestroy(e);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->fork) cudaEventDestroy(c->fork);
@@ -595,9 +607,18 @@ int bp_set_networks(bp_ctx* c, const bp_network* nets, int n) {
     try {
         cudaSetDevice(c->device);
         std::string err;
-        if (!build_nets(nets, n, c->hn, err, true)) return fail(c, BP_BAD_INPUT, err);
+        static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!build_nets(nets, n, c->hn, err, false)) return fail(c, BP_BAD_INPUT, err);
+        const auto t1 = std::chrono::steady_clock::now();
         int rc = upload_networks(c);
         c->have_nets = rc == BP_OK;
+        if (timing) {
+            const auto t2 = std::chrono::steady_clock::now();
+            fprintf(stderr, "bp_set_networks: build %.2f ms, upload + prefix %.2f ms\n",
+                    std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                    std::chrono::duration<double, std::milli>(t2 - t1).count());
+        }
         return rc;
     } catch (const std::bad_alloc&) {
         return fail(c, BP_OUT_OF_MEMORY, "host allocation failed");

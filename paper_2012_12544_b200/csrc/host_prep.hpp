@@ -25,6 +25,9 @@ struct HostNets {
     std::vector<int64_t> fp, bp, w, a, asort, Pfp, Pbp, Pc, Pw;
     std::vector<uint8_t> type_ok;
     int max_L = 0, max_T = 0;
+    // lengths of the prefix tables (Pw; Pfp / Pbp / Pc): the device builds
+    // them (k_cost_prefix); the host arrays are filled only when asked
+    size_t n_pref = 0, n_tpref = 0;
 };
 
 struct HostCls {
@@ -48,8 +51,8 @@ inline bool build_nets(const bp_network* nets, int n, HostNets& H, std::string& 
         d.T = b.n_types;
         d.off_layer = (int64_t)H.w.size();
         d.off_typed = (int64_t)H.fp.size();
-        d.off_pref = (int64_t)H.Pw.size();
-        d.off_tpref = (int64_t)H.Pfp.size();
+        d.off_pref = (int64_t)H.n_pref;
+        d.off_tpref = (int64_t)H.n_tpref;
         d.off_tflag = (int64_t)H.type_ok.size();
         const int64_t L = b.n_layers;
         bool valid = L >= 1;
@@ -68,46 +71,52 @@ inline bool build_nets(const bp_network* nets, int n, HostNets& H, std::string& 
         }
         d.valid = valid ? 1 : 0;
         H.desc.push_back(d);
-        for (int t = 0; t < b.n_types; ++t) {
-            H.type_ok.push_back(valid ? tok[t] : 0);
-            for (int64_t j = 0; j < L; ++j) {
-                H.fp.push_back(b.fp_us[(size_t)t * L + j]);
-                H.bp.push_back(b.bp_us[(size_t)t * L + j]);
-            }
-        }
-        std::vector<int64_t> as;
-        for (int64_t j = 0; j < L; ++j) {
-            H.w.push_back(b.weight_bytes[j]);
-            H.a.push_back(b.out_act_bytes[j]);
-            if (j + 1 < L) as.push_back(b.out_act_bytes[j]);
-        }
+        for (int t = 0; t < b.n_types; ++t) H.type_ok.push_back(valid ? tok[t] : 0);
+        H.fp.insert(H.fp.end(), b.fp_us, b.fp_us + (size_t)b.n_types * L);
+        H.bp.insert(H.bp.end(), b.bp_us, b.bp_us + (size_t)b.n_types * L);
+        H.w.insert(H.w.end(), b.weight_bytes, b.weight_bytes + L);
+        H.a.insert(H.a.end(), b.out_act_bytes, b.out_act_bytes + L);
+        std::vector<int64_t> as(b.out_act_bytes, b.out_act_bytes + (L > 0 ? L - 1 : 0));
         std::sort(as.begin(), as.end());
         as.resize((size_t)L, 0);
         H.asort.insert(H.asort.end(), as.begin(), as.end());
-        // prefix sums (always on the host for the magnitude check; the
-        // device tables are rebuilt by the cost_prefix kernel)
+        // the magnitude check on the (clamped, non-decreasing) prefix sums:
+        // their totals bound every partial sum.  The tables themselves are
+        // built on the device (k_cost_prefix); the host copy only when asked
+        // (the test emulator).
         int64_t sw = 0;
-        H.Pw.push_back(0);
         for (int64_t j = 0; j < L; ++j) {
             sw += std::max<int64_t>(b.weight_bytes[j], 0);
             if (sw >= LIM) { err = "network " + std::to_string(i) + ": weight sum beyond 2^62"; return false; }
-            H.Pw.push_back(sw);
         }
         for (int t = 0; t < b.n_types; ++t) {
             int64_t sf = 0, sb = 0;
-            H.Pfp.push_back(0);
-            H.Pbp.push_back(0);
-            H.Pc.push_back(0);
             for (int64_t j = 0; j < L; ++j) {
                 sf += std::max<int64_t>(b.fp_us[(size_t)t * L + j], 0);
                 sb += std::max<int64_t>(b.bp_us[(size_t)t * L + j], 0);
                 if (sf + sb >= LIM) { err = "network " + std::to_string(i) + ": time sum beyond 2^62"; return false; }
-                H.Pfp.push_back(sf);
-                H.Pbp.push_back(sb);
-                H.Pc.push_back(sf + sb);
             }
         }
-        (void)prefix;
+        H.n_pref += (size_t)L + 1;
+        H.n_tpref += (size_t)b.n_types * ((size_t)L + 1);
+        if (prefix) {
+            sw = 0;
+            H.Pw.push_back(0);
+            for (int64_t j = 0; j < L; ++j) H.Pw.push_back(sw += std::max<int64_t>(b.weight_bytes[j], 0));
+            for (int t = 0; t < b.n_types; ++t) {
+                int64_t sf = 0, sb = 0;
+                H.Pfp.push_back(0);
+                H.Pbp.push_back(0);
+                H.Pc.push_back(0);
+                for (int64_t j = 0; j < L; ++j) {
+                    sf += std::max<int64_t>(b.fp_us[(size_t)t * L + j], 0);
+                    sb += std::max<int64_t>(b.bp_us[(size_t)t * L + j], 0);
+                    H.Pfp.push_back(sf);
+                    H.Pbp.push_back(sb);
+                    H.Pc.push_back(sf + sb);
+                }
+            }
+        }
         H.max_L = std::max<int>(H.max_L, (int)L);
         H.max_T = std::max<int>(H.max_T, b.n_types);
     }
