@@ -30,19 +30,23 @@ def compare(impl_cls, count):
     if not os.path.exists(os.path.join(T.ROOT, "oracle", "_ref", "libbapipe_ref.so")):
         pytest.skip("oracle/_ref not built")
     stats = {"ok": 0, "invalid": 0, "overflow": 0, "other": 0}
+    codes = set()
     for name, p in problems():
         ref, impl = T.Ref(p), impl_cls(p)
         for i, (q, _buf) in enumerate(T.cases(p, seed={"rand": 11, "heavy": 23}[name], count=count)):
             want, got = ref.simulate(q), impl.simulate(q)
             assert got == want, (name, i, {k: (got.get(k), want.get(k)) for k in want if got.get(k) != want.get(k)})
             st = want["status"]
+            if st == 8:
+                codes.add(want["invalid"][0])
             stats["ok" if st == 0 else "invalid" if st == 8 else "overflow" if st == 7 else "other"] += 1
             if st == 0:
                 want_e, got_e = ref.estimate(q), impl.estimate(q)
                 assert got_e == want_e, (name, i, got_e, want_e)
     # the random plans must exercise every outcome
-    print("timeline outcomes", stats)
+    print("timeline outcomes", stats, "invalid codes", sorted(codes))
     assert stats["ok"] > 0 and stats["invalid"] > 0 and stats["overflow"] > 0, stats
+    assert {1, 2, 4, 8, 9, 10}.issubset(codes), codes   # range, fraction, gap, coverage, stage count, M
 
 
 def test_timeline_emulator_matches_reference():

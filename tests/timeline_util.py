@@ -49,15 +49,19 @@ def random_plan(rng, L, N, den_max=64, big=False):
             lo[k + 1] = hi[k]
             trail[k] = (n // g, d // g)
             lead[k + 1] = ((d - n) // g, d // g)
-    if rng.random() < 0.1:   # break something
+    if rng.random() < 0.15:   # break something
         k = int(rng.integers(0, N))
-        what = int(rng.integers(0, 3))
+        what = int(rng.integers(0, 5))
         if what == 0:
             hi[k] = L + 1
         elif what == 1:
             trail[k] = (3, 2)
-        else:
+        elif what == 2:
             lead[k] = (1, 3)
+        elif what == 3 and k + 1 < N:       # a gap: not contiguous
+            lo[k + 1] = hi[k] + 2
+        elif k + 1 < N and lo[k + 1] == hi[k]:   # shared layer, fractions not summing to 1
+            lead[k + 1] = (1, 7) if lead[k + 1] != (1, 7) else (2, 7)
     return lo, hi, lead, trail
 
 
@@ -194,11 +198,10 @@ def cases(problem, seed, count, big_every=5):
         L = problem.networks[net].L
         kinds = KIND_ASYNC if cls.mode == 1 else KIND_SYNC
         kind = int(kinds[int(rng.integers(0, 2))])
-        M = int(rng.integers(1, 9))
+        M = int(rng.integers(1, 9)) if rng.random() > 0.04 else 0   # M < 1: InvalidPlan("M >= 1 required")
         micro = int(rng.integers(1, 5))
         mini = 1 if rng.random() < 0.8 else 2
-        plan = random_plan(rng, L, N, big=(i % big_every == big_every - 1))
-        if rng.random() < 0.05:   # stage count != cluster size
-            plan = tuple(x[:-1] for x in plan) if N > 1 else plan
+        n_plan = N - 1 if (N > 1 and rng.random() < 0.05) else N   # a valid plan, wrong stage count
+        plan = random_plan(rng, L, n_plan, big=(i % big_every == big_every - 1))
         out.append(request(net, cl, kind, N, M, micro, mini, plan))
     return out
