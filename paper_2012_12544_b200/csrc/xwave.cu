@@ -140,9 +140,9 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
                         *(f ? &vs.consF[s] : &vs.consB[s]) = m;
                         if (rat_gt(arr, ready)) ready = arr;
                     }
-                    fr = rat_add(ready, f ? Fd : Bd, e);
+                    fr = rat_addsub_body(ready, f ? Fd : Bd, +1, e);
                     if (has_out) {
-                        const Rat out = async ? fr : rat_add(fr, R(f ? srlink : srin), e);
+                        const Rat out = async ? fr : rat_addsub_body(fr, R(f ? srlink : srin), +1, e);
                         const int t = f ? s + 1 : s - 1;
                         volatile Rat* q = f ? &vs.qF[t][k] : &vs.qB[t][k];
                         q->n = out.n;
