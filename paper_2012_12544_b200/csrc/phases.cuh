@@ -525,10 +525,10 @@ BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S_in) {
                     Rat arr = chain ? cv : S.mf(s);
                     if (rat_gt(arr, ready)) ready = arr;
                 }
-                Rat end = rat_add(ready, S.dF(s), e);
+                Rat end = rat_addsub_body(ready, S.dF(s), +1, e);
                 S.f(s) = end;
                 if (s + 1 < N) {
-                    ov = async ? end : rat_add(end, R(S.sr(s)), e);
+                    ov = async ? end : rat_addsub_body(end, R(S.sr(s)), +1, e);
                     out = true;
                 }
             }
@@ -551,10 +551,10 @@ BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S_in) {
                     Rat arr = chain ? cv : S.mb(s);
                     if (rat_gt(arr, ready)) ready = arr;
                 }
-                Rat end = rat_add(ready, S.dB(s), e);
+                Rat end = rat_addsub_body(ready, S.dB(s), +1, e);
                 S.f(s) = end;
                 if (s > 0) {
-                    ov = async ? end : rat_add(end, R(S.sr(s - 1)), e);
+                    ov = async ? end : rat_addsub_body(end, R(S.sr(s - 1)), +1, e);
                     out = true;
                 }
             }
