@@ -172,6 +172,8 @@ def rooflines(stats, steps, clocks, problem, step_ms):
     counters = {k: stats[k]["work"] for k in list(stats) if stats[k]["launches"] == 0 and k != "refine_critical_path"}
     for k in counters:
         stats.pop(k)
+    # phase spans (several launches over both streams) are reported apart
+    phases = {k: stats.pop(k)["ms"] / steps for k in list(stats) if k.startswith("phase_")}
     # the prune phase is four launches (keys + list, representatives, members'
     # shared estimates, members' own prunes); its work counter covers all of
     # them, so its rate is quoted on the phase
@@ -191,6 +193,7 @@ def rooflines(stats, steps, clocks, problem, step_ms):
     crit = stats.pop("refine_critical_path", None)
     kern.pop("refine_critical_path", None)
     kern["counters"] = counters
+    kern["phases_ms_per_step"] = phases
     dom = max(stats, key=lambda k: stats[k]["ms"])
     d = kern[dom]
     u = work_unit(dom)

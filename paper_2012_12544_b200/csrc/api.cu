@@ -159,6 +159,21 @@ void timed(bp_ctx* c, const char* name, cudaStream_t st, F&& f, int n_kernels = 
     }
 }
 
+// Phase spans (several launches, possibly on both streams) for the profile:
+// an event on the main stream before the phase and one after its join.
+cudaEvent_t phase_begin(bp_ctx* c, cudaStream_t st) {
+    if (!c->prof) return nullptr;
+    cudaEvent_t a = get_event(c);
+    cudaEventRecord(a, st);
+    return a;
+}
+void phase_end(bp_ctx* c, const char* name, cudaStream_t st, cudaEvent_t a) {
+    if (!a) return;
+    cudaEvent_t b = get_event(c);
+    cudaEventRecord(b, st);
+    c->pending.push_back({name, {a, b}});
+}
+
 void collect(bp_ctx* c) {
     for (auto& p : c->pending) {
         float ms = 0;
@@ -469,6 +484,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
         cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
     }
     launch_prune_reset(D, st);
+    cudaEvent_t ph = phase_begin(c, st);
     cudaEventRecord(c->fork, st);
     cudaStreamWaitEvent(c->side, c->fork, 0);
     if (hb.nmslot > 0) {
@@ -483,6 +499,8 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     // (pruning the coarse-path candidates on the side stream while refine runs,
     // launch_prune(D, 0, side), was measured no faster overall: refine's
     // single-lane walks slow down by as much as the overlap saves)
+    phase_end(c, "phase_refine", st, ph);   // coarse DP beside refine, up to the join
+    ph = phase_begin(c, st);
     timed(c, "prune_list", st, [&] { launch_prune(D, -1, st, 1); }, 2);
     timed(c, "prune", st, [&] { launch_prune(D, -1, st, 2); });
     timed(c, "prune_members", st, [&] { launch_prune(D, -1, st, 4); });
@@ -493,6 +511,8 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
         e = cudaGetLastError();
         return e == cudaSuccess ? BP_OK : cuda_fail(c, e, "kernel launch");
     }
+    phase_end(c, "phase_prune", st, ph);
+    ph = phase_begin(c, st);
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
@@ -508,6 +528,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "sim_flow32", st, [&] { launch_sim_flow(D, 0, c->sm_count, st); });
     cudaStreamWaitEvent(st, c->join, 0);
     timed(c, "sim_share", st, [&] { launch_sim_share(D, st); });
+    phase_end(c, "phase_sims", st, ph);
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "kernel launch");
