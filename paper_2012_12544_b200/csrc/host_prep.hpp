@@ -170,8 +170,13 @@ struct HostBatch {
 
 inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const HostCls& HC, HostBatch& HB,
                         std::string& err) {
-    HB = HostBatch();
+    // reuse the vectors' capacity across calls (a sweep is re-prepared per step)
     HB.q.resize(nq);
+    HB.Mpool.clear();
+    HB.whole_items.clear();
+    HB.whole_items.reserve(nq);
+    HB.ncand = HB.nstage = HB.nqstage = HB.nmslot = 0;
+    HB.max_units = HB.max_N = HB.max_nbase = 0;
     std::unordered_map<int64_t, std::pair<int64_t, int>> divisors;   // mini -> (offset, count)
     for (int i = 0; i < nq; ++i) {
         const bp_query& b = qs[i];
