@@ -345,7 +345,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     int32_t ctab = 1;
     while (ctab < 2 * std::max<int64_t>(1, (int64_t)nms)) ctab <<= 1;
     size_t o_ckey = L.take<unsigned long long>((size_t)ctab), o_crep = L.take<int32_t>((size_t)ctab);
-    size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(SIM_CLASSES);
+    size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(2 * SIM_CLASSES);   // counts, then hand-out counters
     if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
     void* b = B->mem.p;
     // stage the inputs in pinned memory and copy once

@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
 static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
-    cudaMemsetAsync(B.sim_count, 0, SIM_CLASSES * sizeof(int32_t), st);
+    cudaMemsetAsync(B.sim_count, 0, 2 * SIM_CLASSES * sizeof(int32_t), st);
     cudaMemsetAsync(B.skey, 0, ((size_t)B.smask + 1) * sizeof(unsigned long long), st);
     cudaMemsetAsync(B.srep, 0x7f, ((size_t)B.smask + 1) * sizeof(int32_t), st);
     if (B.ncand) {

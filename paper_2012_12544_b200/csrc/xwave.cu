@@ -61,6 +61,7 @@ struct FlowSmem {
     int prodB[NT], consB[NT];
     Rat fr[NT];
     unsigned red[3];
+    int next;               // the block's next candidate (dynamic assignment)
 };
 
 template <int NT>
@@ -68,7 +69,10 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
     __shared__ FlowSmem<NT> sm;
     const int s = threadIdx.x;
     const int count = B.sim_count[cls];
-    for (int idx = blockIdx.x; idx < count; idx += gridDim.x) {
+    // candidates are handed out dynamically (their event counts differ by
+    // orders of magnitude): a block that finishes takes the next one
+    int* ctr = B.sim_count + SIM_CLASSES + cls;
+    for (int idx = blockIdx.x; idx < count; idx = sm.next) {
         const int64_t ci = B.sim_list[(int64_t)cls * B.ncand + idx];
         const bp_candidate& cd = B.cand[ci];
         const CState cs = B.cs[ci];
@@ -185,6 +189,7 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
                 out.makespan = bp_rat{mk.n, mk.d};
                 out.status = BP_C_OK;
             }
+            sm.next = (int)gridDim.x + atomicAdd(ctr, 1);
         }
         flow_sync<NT>();
     }
