@@ -237,8 +237,16 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
     const int gpw = 32 / G;
     const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x / 32);
     const int64_t warp_global = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
-    // persistent: each warp walks groups base, base + warps_total*gpw, ...
-    for (int64_t base = warp_global * gpw; base < count; base += warps_total * gpw) {
+    // persistent warps; after the first chunk, chunks of gpw candidates are
+    // handed out dynamically (event counts differ by orders of magnitude)
+    int* ctr = B.sim_count + SIM_CLASSES + cls;
+    auto next_chunk = [&]() -> int64_t {
+        int nb = 0;
+        if (lane == 0) nb = atomicAdd(ctr, 1);
+        nb = __shfl_sync(FULL, nb, 0);
+        return (warps_total + nb) * gpw;
+    };
+    for (int64_t base = warp_global * gpw; base < count; base = next_chunk()) {
     const int64_t gid = base + lane / G;
     const bool active = gid < count;
     int64_t ci = active ? B.sim_list[(int64_t)cls * B.ncand + gid] : -1;
