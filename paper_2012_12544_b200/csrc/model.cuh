@@ -1010,7 +1010,13 @@ BPK_HD void refine_body(const NetView& v, const ChainView& c, int32_t* lo, int32
 BPK_HDNI uint32_t refine_v(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail,
                            Rat* tF, Rat* tB, Rat* tT, uint8_t* dirty, int64_t* stats, uint32_t ecode) {
     Err e{ecode};
-    refine_body(v, c, lo, hi, lead, trail, tF, tB, tT, dirty, stats, e);
+    // register copies: through the references (and the stats pointer) every
+    // field access after an out-of-line call was a reload from local memory
+    const NetView vv = v;
+    const ChainView cc = c;
+    int64_t st[4];
+    refine_body(vv, cc, lo, hi, lead, trail, tF, tB, tT, dirty, st, e);
+    for (int k = 0; k < 4; ++k) stats[k] = st[k];
     return e.code;
 }
 BPK_HD void refine(const NetView& v, const ChainView& c, int32_t* lo, int32_t* hi, Rat* lead, Rat* trail, Rat* tF,
