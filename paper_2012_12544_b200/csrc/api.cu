@@ -459,7 +459,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     cudaError_t e;
     e = cudaMemsetAsync(D.cand, 0, (size_t)hb.ncand * sizeof(bp_candidate), st);
     if (e == cudaSuccess && D.stages) e = cudaMemsetAsync(D.stages, 0, (size_t)hb.nstage * sizeof(bp_stage), st);
-    if (e == cudaSuccess) e = cudaMemsetAsync(D.dp_count + 1, 0, sizeof(int32_t), st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(D.dp_count + 1, 0, 3 * sizeof(int32_t), st);   // [1], hand-out [2..3]
     if (e == cudaSuccess) e = cudaMemsetAsync(D.work, 0, WORK_SLOTS * sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_fail(c, e, "memset");
     const int T = c->max_T, maxN = std::max(1, hb.max_N);

@@ -107,7 +107,16 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
     __shared__ int64_t s_T, s_F;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_items = B.dp_count[which];
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
+    // items are handed out dynamically after each block's first (their sizes
+    // differ by orders of magnitude; the list is heaviest first)
+    __shared__ int s_next;
+    auto next_item = [&]() {
+        __syncthreads();
+        if (tid == 0) s_next = (int)gridDim.x + atomicAdd(&B.dp_count[2 + which], 1);
+        __syncthreads();
+        return s_next;
+    };
+    for (int it = blockIdx.x; it < n_items; it = next_item()) {
         DPItem item = B.dp_items[(which == 0 ? 0 : B.nq) + it];
         if (which == 0 && B.qrep[item.q] != item.q) continue;   // shared: k_dedup_copy_dp
         const QDesc Q = B.q[item.q];
