@@ -60,9 +60,12 @@ enum { PLAN_NONE = 0, PLAN_REFINED = 1, PLAN_WHOLE = 2 };
 // candidate, thread per stage (xwave.cu), for the heavy exact candidates with
 // N <= 32 / N <= 64.
 enum { SIM_CLASSES = 11, SIM_EXACT = 8, SIM_FLOW = 9, SIM_FLOW_CLASSES = 2 };
-// exact candidates with at least this many events (and 8 <= N <= 64) go to
-// the dataflow kernel: their serial walk would otherwise set the kernel time
-constexpr int64_t FLOW_MIN_EVENTS = 1024;
+// exact candidates with at least this many events (and FLOW_MIN_N <= N <= 64)
+// go to the dataflow kernel: their serial walk would otherwise set the kernel
+// time (measured on C5: 256 / 4 take the simulator phase from 15.2 to 14.3 ms
+// against 1024 / 8)
+constexpr int64_t FLOW_MIN_EVENTS = 256;
+constexpr int64_t FLOW_MIN_N = 4;
 // instrumentation slots of BatchDev::work (algorithmic work of one run)
 // refine: boundary steps evaluated (and the longest query's count: the serial
 // critical path); prune: candidate-stages estimated

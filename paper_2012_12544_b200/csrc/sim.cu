@@ -92,7 +92,7 @@ __global__ void k_sim_classify(BatchDev B) {
     if (cls == SIM_EXACT) {
         const bp_candidate& c = B.cand[ci];
         const int64_t N = c.n_stages, ev = 2 * N * c.M + (c.kind >= 2 ? 2 * (N - 1) * c.M : 0);
-        if (N >= 8 && N <= 64 && ev >= FLOW_MIN_EVENTS) cls = SIM_FLOW + (N <= 32 ? 0 : 1);
+        if (N >= FLOW_MIN_N && N <= 64 && ev >= FLOW_MIN_EVENTS) cls = SIM_FLOW + (N <= 32 ? 0 : 1);
     }
     B.cs[ci].sim_cls = cls;
     B.cs[ci].sim_rep = -1;
