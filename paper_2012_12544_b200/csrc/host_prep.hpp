@@ -38,7 +38,13 @@ struct HostCls {
 };
 
 inline bool build_nets(const bp_network* nets, int n, HostNets& H, std::string& err, bool prefix) {
-    H = HostNets();
+    // reuse the vectors' capacity across calls (a sweep re-uploads its tables
+    // every step): no fresh pages to fault in
+    for (auto* v : {&H.fp, &H.bp, &H.w, &H.a, &H.asort, &H.Pfp, &H.Pbp, &H.Pc, &H.Pw}) v->clear();
+    H.desc.clear();
+    H.type_ok.clear();
+    H.max_L = H.max_T = 0;
+    H.n_pref = H.n_tpref = 0;
     const int64_t LIM = (int64_t)1 << 62;
     for (int i = 0; i < n; ++i) {
         const bp_network& b = nets[i];
