@@ -11,8 +11,10 @@
 //     ranges (dense, in query order, the same rule as bp_layout()).
 #pragma once
 #include <algorithm>
+#include <atomic>
 #include <cstdint>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -37,94 +39,157 @@ struct HostCls {
     int max_N = 0;
 };
 
-inline bool build_nets(const bp_network* nets, int n, HostNets& H, std::string& err, bool prefix) {
-    // reuse the vectors' capacity across calls (a sweep re-uploads its tables
-    // every step): no fresh pages to fault in
-    for (auto* v : {&H.fp, &H.bp, &H.w, &H.a, &H.asort, &H.Pfp, &H.Pbp, &H.Pc, &H.Pw}) v->clear();
-    H.desc.clear();
-    H.type_ok.clear();
-    H.max_L = H.max_T = 0;
-    H.n_pref = H.n_tpref = 0;
+// Run f(i) for i in [0, n) on up to 8 host threads (serially when n is small).
+template <class F>
+inline void host_parallel_for(int n, F&& f) {
+    const int hw = (int)std::thread::hardware_concurrency();
+    const int nt = std::min(std::min(8, hw > 0 ? hw : 1), n / 8);
+    if (nt <= 1) {
+        for (int i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::atomic<int> next{0};
+    std::vector<std::thread> pool;
+    for (int t = 0; t < nt; ++t)
+        pool.emplace_back([&] {
+            for (int i; (i = next.fetch_add(1)) < n;) f(i);
+        });
+    for (auto& th : pool) th.join();
+}
+
+// One network's tables into its slices of H (layout already in H.desc[i]):
+// schema flags, the SoA copies, the sorted activations, the magnitude check
+// and, when asked, the host prefix tables.  Returns 0, 2 (weight sum beyond
+// 2^62) or 3 (time sum beyond 2^62).
+inline int fill_net(const bp_network& b, HostNets& H, NetDesc& d, bool prefix) {
     const int64_t LIM = (int64_t)1 << 62;
-    for (int i = 0; i < n; ++i) {
-        const bp_network& b = nets[i];
-        if (b.n_layers < 0 || b.n_types < 1 || (b.n_layers > 0 && (!b.fp_us || !b.bp_us || !b.weight_bytes || !b.out_act_bytes))) {
-            err = "network " + std::to_string(i) + ": bad array arguments";
-            return false;
+    const int64_t L = b.n_layers;
+    const int T = b.n_types;
+    bool valid = L >= 1;
+    uint8_t* tok = H.type_ok.data() + d.off_tflag;
+    for (int t = 0; t < T; ++t) tok[t] = 1;
+    for (int64_t j = 0; j < L; ++j) {
+        bool anyf = false, anyb = false;
+        for (int t = 0; t < T; ++t) {
+            int64_t f = b.fp_us[(size_t)t * L + j], bb = b.bp_us[(size_t)t * L + j];
+            if (f < 0 || bb < 0) valid = false;          // present but < 1
+            anyf |= f != 0;
+            anyb |= bb != 0;
+            if (f == 0 || bb == 0) tok[t] = 0;
         }
-        NetDesc d{};
-        d.L = b.n_layers;
-        d.T = b.n_types;
-        d.off_layer = (int64_t)H.w.size();
-        d.off_typed = (int64_t)H.fp.size();
-        d.off_pref = (int64_t)H.n_pref;
-        d.off_tpref = (int64_t)H.n_tpref;
-        d.off_tflag = (int64_t)H.type_ok.size();
-        const int64_t L = b.n_layers;
-        bool valid = L >= 1;
-        std::vector<uint8_t> tok(b.n_types, 1);
+        if (!anyf || !anyb) valid = false;                // maps must be non-empty
+        if (b.weight_bytes[j] < 0 || b.out_act_bytes[j] < 0) valid = false;
+    }
+    d.valid = valid ? 1 : 0;
+    if (!valid)
+        for (int t = 0; t < T; ++t) tok[t] = 0;
+    std::copy(b.fp_us, b.fp_us + (size_t)T * L, H.fp.data() + d.off_typed);
+    std::copy(b.bp_us, b.bp_us + (size_t)T * L, H.bp.data() + d.off_typed);
+    std::copy(b.weight_bytes, b.weight_bytes + L, H.w.data() + d.off_layer);
+    std::copy(b.out_act_bytes, b.out_act_bytes + L, H.a.data() + d.off_layer);
+    int64_t* as = H.asort.data() + d.off_layer;   // the L-1 cut activations, sorted, then a 0
+    if (L > 0) {
+        std::copy(b.out_act_bytes, b.out_act_bytes + (L - 1), as);
+        std::sort(as, as + (L - 1));
+        as[L - 1] = 0;
+    }
+    // the magnitude check on the (clamped, non-decreasing) prefix sums:
+    // their totals bound every partial sum.  The tables themselves are built
+    // on the device (k_cost_prefix); the host copy only when asked (the test
+    // emulator).
+    int64_t sw = 0;
+    for (int64_t j = 0; j < L; ++j) {
+        sw += std::max<int64_t>(b.weight_bytes[j], 0);
+        if (sw >= LIM) return 2;
+    }
+    for (int t = 0; t < T; ++t) {
+        int64_t sf = 0, sb = 0;
         for (int64_t j = 0; j < L; ++j) {
-            bool anyf = false, anyb = false;
-            for (int t = 0; t < b.n_types; ++t) {
-                int64_t f = b.fp_us[(size_t)t * L + j], bb = b.bp_us[(size_t)t * L + j];
-                if (f < 0 || bb < 0) valid = false;          // present but < 1
-                anyf |= f != 0;
-                anyb |= bb != 0;
-                if (f == 0 || bb == 0) tok[t] = 0;
-            }
-            if (!anyf || !anyb) valid = false;                // maps must be non-empty
-            if (b.weight_bytes[j] < 0 || b.out_act_bytes[j] < 0) valid = false;
+            sf += std::max<int64_t>(b.fp_us[(size_t)t * L + j], 0);
+            sb += std::max<int64_t>(b.bp_us[(size_t)t * L + j], 0);
+            if (sf + sb >= LIM) return 3;
         }
-        d.valid = valid ? 1 : 0;
-        H.desc.push_back(d);
-        for (int t = 0; t < b.n_types; ++t) H.type_ok.push_back(valid ? tok[t] : 0);
-        H.fp.insert(H.fp.end(), b.fp_us, b.fp_us + (size_t)b.n_types * L);
-        H.bp.insert(H.bp.end(), b.bp_us, b.bp_us + (size_t)b.n_types * L);
-        H.w.insert(H.w.end(), b.weight_bytes, b.weight_bytes + L);
-        H.a.insert(H.a.end(), b.out_act_bytes, b.out_act_bytes + L);
-        std::vector<int64_t> as(b.out_act_bytes, b.out_act_bytes + (L > 0 ? L - 1 : 0));
-        std::sort(as.begin(), as.end());
-        as.resize((size_t)L, 0);
-        H.asort.insert(H.asort.end(), as.begin(), as.end());
-        // the magnitude check on the (clamped, non-decreasing) prefix sums:
-        // their totals bound every partial sum.  The tables themselves are
-        // built on the device (k_cost_prefix); the host copy only when asked
-        // (the test emulator).
-        int64_t sw = 0;
-        for (int64_t j = 0; j < L; ++j) {
-            sw += std::max<int64_t>(b.weight_bytes[j], 0);
-            if (sw >= LIM) { err = "network " + std::to_string(i) + ": weight sum beyond 2^62"; return false; }
-        }
-        for (int t = 0; t < b.n_types; ++t) {
+    }
+    if (prefix) {
+        int64_t* Pw = H.Pw.data() + d.off_pref;
+        sw = 0;
+        Pw[0] = 0;
+        for (int64_t j = 0; j < L; ++j) Pw[j + 1] = (sw += std::max<int64_t>(b.weight_bytes[j], 0));
+        for (int t = 0; t < T; ++t) {
+            int64_t* Pf = H.Pfp.data() + d.off_tpref + (size_t)t * (L + 1);
+            int64_t* Pb = H.Pbp.data() + d.off_tpref + (size_t)t * (L + 1);
+            int64_t* Pc = H.Pc.data() + d.off_tpref + (size_t)t * (L + 1);
             int64_t sf = 0, sb = 0;
+            Pf[0] = Pb[0] = Pc[0] = 0;
             for (int64_t j = 0; j < L; ++j) {
                 sf += std::max<int64_t>(b.fp_us[(size_t)t * L + j], 0);
                 sb += std::max<int64_t>(b.bp_us[(size_t)t * L + j], 0);
-                if (sf + sb >= LIM) { err = "network " + std::to_string(i) + ": time sum beyond 2^62"; return false; }
+                Pf[j + 1] = sf;
+                Pb[j + 1] = sb;
+                Pc[j + 1] = sf + sb;
             }
         }
-        H.n_pref += (size_t)L + 1;
-        H.n_tpref += (size_t)b.n_types * ((size_t)L + 1);
-        if (prefix) {
-            sw = 0;
-            H.Pw.push_back(0);
-            for (int64_t j = 0; j < L; ++j) H.Pw.push_back(sw += std::max<int64_t>(b.weight_bytes[j], 0));
-            for (int t = 0; t < b.n_types; ++t) {
-                int64_t sf = 0, sb = 0;
-                H.Pfp.push_back(0);
-                H.Pbp.push_back(0);
-                H.Pc.push_back(0);
-                for (int64_t j = 0; j < L; ++j) {
-                    sf += std::max<int64_t>(b.fp_us[(size_t)t * L + j], 0);
-                    sb += std::max<int64_t>(b.bp_us[(size_t)t * L + j], 0);
-                    H.Pfp.push_back(sf);
-                    H.Pbp.push_back(sb);
-                    H.Pc.push_back(sf + sb);
-                }
-            }
+    }
+    return 0;
+}
+
+inline bool build_nets(const bp_network* nets, int n, HostNets& H, std::string& err, bool prefix) {
+    // pass 1: argument checks and the layout (offsets of every network's
+    // slices); pass 2, over networks in parallel: the tables themselves.
+    // Errors are reported for the first failing network, as a serial pass
+    // would (a network's magnitude error before a later one's bad arrays).
+    H.desc.assign((size_t)std::max(n, 0), NetDesc{});
+    H.max_L = H.max_T = 0;
+    size_t nl = 0, ntl = 0, np = 0, ntp = 0, nf = 0;
+    int m = n;   // networks [0, m) have well-formed arguments
+    for (int i = 0; i < n; ++i) {
+        const bp_network& b = nets[i];
+        if (b.n_layers < 0 || b.n_types < 1 ||
+            (b.n_layers > 0 && (!b.fp_us || !b.bp_us || !b.weight_bytes || !b.out_act_bytes))) {
+            m = i;
+            break;
         }
-        H.max_L = std::max<int>(H.max_L, (int)L);
+        NetDesc& d = H.desc[(size_t)i];
+        d.L = b.n_layers;
+        d.T = b.n_types;
+        d.off_layer = (int64_t)nl;
+        d.off_typed = (int64_t)ntl;
+        d.off_pref = (int64_t)np;
+        d.off_tpref = (int64_t)ntp;
+        d.off_tflag = (int64_t)nf;
+        nl += (size_t)b.n_layers;
+        ntl += (size_t)b.n_types * (size_t)b.n_layers;
+        np += (size_t)b.n_layers + 1;
+        ntp += (size_t)b.n_types * ((size_t)b.n_layers + 1);
+        nf += (size_t)b.n_types;
+        H.max_L = std::max<int>(H.max_L, b.n_layers);
         H.max_T = std::max<int>(H.max_T, b.n_types);
+    }
+    // (the vectors keep their capacity across calls: a sweep re-uploads its
+    // tables every step, with no fresh pages to fault in)
+    H.fp.resize(ntl);
+    H.bp.resize(ntl);
+    H.w.resize(nl);
+    H.a.resize(nl);
+    H.asort.resize(nl);
+    H.type_ok.resize(nf);
+    H.n_pref = np;
+    H.n_tpref = ntp;
+    H.Pw.resize(prefix ? np : 0);
+    H.Pfp.resize(prefix ? ntp : 0);
+    H.Pbp.resize(prefix ? ntp : 0);
+    H.Pc.resize(prefix ? ntp : 0);
+    std::vector<int> status((size_t)m, 0);
+    host_parallel_for(m, [&](int i) { status[(size_t)i] = fill_net(nets[i], H, H.desc[(size_t)i], prefix); });
+    for (int i = 0; i < m; ++i)
+        if (status[(size_t)i]) {
+            err = "network " + std::to_string(i) + (status[(size_t)i] == 2 ? ": weight sum beyond 2^62"
+                                                                           : ": time sum beyond 2^62");
+            return false;
+        }
+    if (m < n) {
+        err = "network " + std::to_string(m) + ": bad array arguments";
+        return false;
     }
     return true;
 }
