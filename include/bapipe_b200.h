@@ -225,7 +225,10 @@ int bp_explore_batch(bp_ctx* ctx, const bp_query* q, int nq, bp_query_result* re
                      bp_candidate* cand, bp_stage* stages, void* stream);
 
 /* Split form for device-resident timing: prepare uploads the queries once,
- * run launches only the kernels (inputs already in HBM), fetch copies back. */
+ * run launches only the kernels (inputs already in HBM), fetch copies back.
+ * A prepared batch refers to the context's current network / cluster tables:
+ * after a later bp_set_networks / bp_set_clusters, run / fetch / best return
+ * BP_BAD_INPUT for it (prepare it again). */
 bp_batch* bp_batch_prepare(bp_ctx* ctx, const bp_query* q, int nq, int want_details,
                            void* stream);
 int bp_batch_run(bp_ctx* ctx, bp_batch* b, void* stream);

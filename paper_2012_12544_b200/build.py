@@ -19,7 +19,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libbapipe_b200.so")
 SOURCES = ["api.cu", "kernels.cu", "dp.cu", "sim.cu", "xwave.cu", "timeline.cu"]
-HEADERS = ["rat.cuh", "common.cuh", "model.cuh", "batch.cuh", "phases.cuh", "kernels.h", "host_prep.hpp", "timeline.cuh"]
+HEADERS = ["rat.cuh", "common.cuh", "model.cuh", "refine_fast.cuh", "batch.cuh", "phases.cuh", "kernels.h", "host_prep.hpp", "timeline.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

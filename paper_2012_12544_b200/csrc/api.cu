@@ -91,6 +91,9 @@ struct bp_batch {
     bool details = false;
     int nq = 0;
     int dp_grid = 0, dp_max_units = 0;
+    int refine_grid = 0;       // slim refine kernel: persistent grid, 0 = not used
+    size_t refine_bytes = 0;   // its dynamic shared memory
+    uint64_t gen = 0;          // bp_ctx::gen at prepare: the device tables it points at
 };
 
 struct bp_ctx {
@@ -102,6 +105,7 @@ struct bp_ctx {
     HostNets hn;
     HostCls hc;
     bool have_nets = false, have_cls = false;
+    uint64_t gen = 0;        // bumped by every bp_set_networks / bp_set_clusters
     DevBuf nets_mem, cls_mem;
     HostPinned stage_tables;   // pinned staging of the network / cluster tables
     Pools P{};
@@ -296,7 +300,12 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     for (int i = 0; i < nq; ++i)
         if (q[i].cand_offset != hb.q[i].cand_off || q[i].stage_offset != hb.q[i].stage_off)
             return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
+    // candidate and stage-slot indices are int32 in the kernels' work lists
+    if (hb.ncand >= INT32_MAX || hb.nstage >= ((int64_t)1 << 40))
+        return fail(c, BP_BAD_INPUT, "batch too large (" + std::to_string(hb.ncand) +
+                                         " candidates; at most 2^31 - 1 per batch: split it)");
     B->nq = nq;
+    B->gen = c->gen;
     B->details = details != 0;
     const size_t nqs = (size_t)nq, nc = (size_t)hb.ncand, ns = (size_t)hb.nstage, nqst = (size_t)hb.nqstage,
                  nms = (size_t)hb.nmslot;
@@ -339,7 +348,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     int32_t stab = 1;
     while (stab < 2 * std::max<int64_t>(1, hb.ncand)) stab <<= 1;
     size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
-    size_t o_rlist = L.take<int32_t>(nqs), o_rcount = L.take<int32_t>(2);
+    size_t o_rlist = L.take<int32_t>(2 * nqs), o_rcount = L.take<int32_t>(4);
     size_t o_plist = L.take<int32_t>(nc), o_pctr = L.take<int32_t>(2);
     size_t o_pkey = L.take<unsigned long long>((size_t)stab), o_pbest = L.take<unsigned long long>((size_t)stab);
     int32_t ctab = 1;
@@ -441,6 +450,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     if (per_sm > 8) per_sm = 8;
     B->dp_grid = c->sm_count * per_sm;
     B->dp_max_units = max_units;
+    B->refine_grid = refine_setup(std::max(1, hb.max_N), max_units, c->max_T, &B->refine_bytes);
     return BP_OK;
 }
 
@@ -493,7 +503,10 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
         timed(c, "dedup_copy", c->side, [&] { launch_coarse_copy(D, c->side); });
     }
     cudaEventRecord(c->join, c->side);
-    timed(c, "refine", st, [&] { launch_refine(D, c->sm_count, st); }, 2);
+    const int refine_launches = (refine_region_bytes(maxN) > 200 * 1024 || !D.dedup) ? 1 : B->refine_grid ? 3 : 2;
+    timed(c, "refine", st, [&] {
+        launch_refine(D, c->sm_count, B->refine_grid, B->refine_bytes, B->dp_max_units, T, st);
+    }, refine_launches);
     timed(c, "dedup_copy", st, [&] { launch_dedup_copy_refine(D, st); });
     cudaStreamWaitEvent(st, c->join, 0);
     // (pruning the coarse-path candidates on the side stream while refine runs,
@@ -630,6 +643,12 @@ int bp_set_networks(bp_ctx* c, const bp_network* nets, int n) {
         std::string err;
         static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
         const auto t0 = std::chrono::steady_clock::now();
+        // batches prepared before this call point at the old tables: they are
+        // refused from now on (bp_batch_*: generation check), and whatever
+        // is still in flight on any stream finishes before the tables change
+        ++c->gen;
+        c->have_nets = false;
+        cudaDeviceSynchronize();
         if (!build_nets(nets, n, c->hn, err, false)) return fail(c, BP_BAD_INPUT, err);
         const auto t1 = std::chrono::steady_clock::now();
         int rc = upload_networks(c);
@@ -651,6 +670,9 @@ int bp_set_clusters(bp_ctx* c, const bp_cluster* cls, int n) {
     try {
         cudaSetDevice(c->device);
         std::string err;
+        ++c->gen;
+        c->have_cls = false;
+        cudaDeviceSynchronize();
         if (!build_clusters(cls, n, c->hc, err)) return fail(c, BP_BAD_INPUT, err);
         int rc = upload_clusters(c);
         c->have_cls = rc == BP_OK;
@@ -700,8 +722,12 @@ bp_batch* bp_batch_prepare(bp_ctx* c, const bp_query* q, int nq, int want_detail
     }
 }
 
+static bool stale(const bp_ctx* c, const bp_batch* B) { return B->gen != c->gen; }
+static const char* STALE = "batch prepared before the last bp_set_networks / bp_set_clusters: prepare it again";
+
 int bp_batch_run(bp_ctx* c, bp_batch* B, void* stream) {
     if (!c || !B) return fail(c, BP_BAD_INPUT, "bad arguments");
+    if (stale(c, B)) return fail(c, BP_BAD_INPUT, STALE);
     cudaSetDevice(c->device);
     return run(c, B, (cudaStream_t)stream);
 }
@@ -709,12 +735,14 @@ int bp_batch_run(bp_ctx* c, bp_batch* B, void* stream) {
 int bp_batch_fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_stage* stages,
                    void* stream) {
     if (!c || !B) return fail(c, BP_BAD_INPUT, "bad arguments");
+    if (stale(c, B)) return fail(c, BP_BAD_INPUT, STALE);
     cudaSetDevice(c->device);
     return fetch(c, B, res, cand, stages, (cudaStream_t)stream);
 }
 
 int bp_batch_best(bp_ctx* c, bp_batch* B, void* dev_out, int64_t query_base, void* stream) {
     if (!c || !B || !dev_out) return fail(c, BP_BAD_INPUT, "bad arguments");
+    if (stale(c, B)) return fail(c, BP_BAD_INPUT, STALE);
     cudaSetDevice(c->device);
     cudaStream_t st = (cudaStream_t)stream;
     timed(c, "best", st, [&] { launch_best(B->dev, (bp_best_record*)dev_out, query_base, nullptr, st); });

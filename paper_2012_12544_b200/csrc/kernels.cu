@@ -21,10 +21,13 @@
 //   k_best             argmin of the per-query bests (multi-GPU exchange record)
 // The simulators (K4) are in sim.cu and xwave.cu, the DP (K2) in dp.cu, the
 // one-plan timeline / estimate (F3) in timeline.cu.
+#include <atomic>
+
 #include <cub/cub.cuh>
 
 #include "kernels.h"
 #include "phases.cuh"
+#include "refine_fast.cuh"
 
 namespace bpk {
 
@@ -326,7 +329,9 @@ __global__ void k_refine_list(BatchDev B) {
     if (refine_wanted(B, qi)) B.rlist[atomicAdd(B.rcount, 1)] = qi;
 }
 
-__global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm) {
+// The general kernel over a query list (list[ctr[0]] entries, hand-out
+// counter ctr[1]): every query the slim kernel below could not finish.
+__global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm, const int32_t* list, int32_t* ctr) {
     extern __shared__ __align__(16) unsigned char rsm[];
     if (threadIdx.x != 0) return;
     unsigned char* base = rsm;
@@ -339,16 +344,192 @@ __global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm) {
     sc.lo = reinterpret_cast<int32_t*>(sc.tT + nm);
     sc.hi = sc.lo + nm;
     sc.dirty = reinterpret_cast<uint8_t*>(sc.hi + nm);
-    const int count = B.rcount[0];
+    const int count = ctr[0];
     // dynamic: the list is heaviest-first (scheduling order), so a warp that
     // finishes early takes the next query instead of a fixed stride's
-    for (int i = atomicAdd(&B.rcount[1], 1); i < count; i = atomicAdd(&B.rcount[1], 1)) {
-        const int qi = B.rlist[i];
+    for (int i = atomicAdd(&ctr[1], 1); i < count; i = atomicAdd(&ctr[1], 1)) {
+        const int qi = list[i];
         refine_query_at(B, qi, &sc);
         atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
         atomicMax(&B.work[WORK_REFINE_MAX], (unsigned long long)B.qs[qi].refine_evals);
         atomicAdd(&B.work[WORK_REFINE_MOVES], (unsigned long long)B.qs[qi].refine_moves);
         atomicAdd(&B.work[WORK_REFINE_EXACT], (unsigned long long)B.qs[qi].refine_exact);
+    }
+}
+
+// ---- K3a slim: intra_layer_refine in the bounded regime of refine_fast.cuh.
+// One warp per query: all lanes stage the layer tables (int32 fp+bp per type,
+// out_act) and the DP plan into shared memory, lane 0 walks, then the lanes
+// write the plan back and form the refined plan's stage sums in parallel.  A
+// query outside the regime goes to the general kernel's list unchanged.
+struct FastLayout {
+    size_t t, lead, trail, lo, hi, type, memo, cost, act, bytes;
+};
+__host__ __device__ inline FastLayout fast_layout(int mN, int mL, int mT) {
+    FastLayout f;
+    size_t o = 0;
+    auto take = [&](size_t n) { const size_t r = o; o = (o + n + 15) & ~(size_t)15; return r; };
+    f.t = take((size_t)mN * sizeof(Rat));
+    f.lead = take((size_t)mN * sizeof(Rat));
+    f.trail = take((size_t)mN * sizeof(Rat));
+    f.lo = take((size_t)mN * 4);
+    f.hi = take((size_t)mN * 4);
+    f.type = take((size_t)mN * 4);
+    f.memo = take((size_t)mN);
+    f.cost = take((size_t)mT * mL * 4);
+    f.act = take((size_t)mL * 4);
+    f.bytes = o;
+    return f;
+}
+
+__device__ __forceinline__ int64_t lcm_sat_warp(int64_t D) {
+    for (int o = 16; o; o >>= 1) D = lcm_sat(D, __shfl_xor_sync(0xffffffffu, D, o));
+    return D;
+}
+
+// The tail of refine_query_at (phases.cuh) for a plan in shared memory, one
+// stage per lane: write the plan back, the refined plan's stage sums in
+// estimate's order (first error in (stage, F, B, W) order), the simulator
+// scale D (lcm, saturating) and sum (F+B)*D, then validate_plan on lane 0.
+__device__ void refine_tail_warp(const BatchDev& B, int qi, const int32_t* lo, const int32_t* hi, const Rat* lead,
+                                 const Rat* trail, const int64_t* st) {
+    const int lane = threadIdx.x & 31;
+    const QDesc Q = B.q[qi];
+    QState& qs = B.qs[qi];
+    const NetView v = net_view(B.P, Q.net);
+    const ChainView c = chain_view(B.P, Q.cl, Q.N);
+    const int N = Q.N;
+    const int64_t o = Q.qstage_off;
+    int first = 0x7fffffff;
+    int64_t D = 1;
+    for (int s = lane; s < N; s += 32) {
+        B.qlo[o + s] = lo[s];
+        B.qhi[o + s] = hi[s];
+        B.qlead[o + s] = lead[s];
+        B.qtrail[o + s] = trail[s];
+        Err e{ERR_NONE};
+        const int32_t t = c.type[s];
+        const Rat F = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pfp + (int64_t)t * (v.L + 1), e);
+        const Rat Bt = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pbp + (int64_t)t * (v.L + 1), e);
+        const Rat W = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pw, e);
+        B.qF[o + s] = F;
+        B.qB[o + s] = Bt;
+        B.qW[o + s] = W;
+        if (e.bad() && first == 0x7fffffff) first = s * 16 + (int)e.code;
+        D = lcm_sat(lcm_sat(D, F.d), Bt.d);
+    }
+    first = __reduce_min_sync(0xffffffffu, first);
+    D = lcm_sat_warp(D);
+    const uint32_t code = first == 0x7fffffff ? ERR_NONE : (uint32_t)(first & 15);
+    if (lane == 0) {
+        qs.refined = 1;
+        qs.refine_iters = st[0];
+        qs.refine_evals = st[1];
+        qs.refine_moves = st[2];
+        qs.refine_exact = 0;
+        qs.refine_err = code;
+    }
+    if (code) return;
+    __syncwarp();
+    if (D) {
+        u128 part = 0;
+        for (int s = lane; s < N; s += 32) {
+            const Rat F = B.qF[o + s], Bt = B.qB[o + s];
+            part += (u128)((i128)F.n * (int64_t)udiv_exact64((uint64_t)D, (uint64_t)F.d));
+            part += (u128)((i128)Bt.n * (int64_t)udiv_exact64((uint64_t)D, (uint64_t)Bt.d));
+        }
+        for (int k = 16; k; k >>= 1) {
+            const uint64_t lo64 = __shfl_xor_sync(0xffffffffu, (uint64_t)part, k);
+            const uint64_t hi64 = __shfl_xor_sync(0xffffffffu, (uint64_t)(part >> 64), k);
+            part += ((u128)hi64 << 64) | lo64;
+        }
+        if (lane == 0) qs.sumFB_D = part >= ((u128)1 << 62) ? -1 : (int64_t)part;
+    }
+    if (lane == 0) {
+        qs.D = D;
+        Err ve{ERR_NONE};
+        int64_t where = 0;
+        Rat aux{0, 1};
+        qs.vcode = validate_frac(lo, hi, lead, trail, N, v.L, &where, &aux, ve);
+        qs.verr = ve.code;
+        qs.vwhere = where;
+        qs.vaux = aux;
+    }
+}
+
+__global__ void __launch_bounds__(32) k_refine_fast(BatchDev B, int mN, int mL, int mT) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    const FastLayout f = fast_layout(mN, mL, mT);
+    Rat* t = reinterpret_cast<Rat*>(fsm + f.t);
+    Rat* lead = reinterpret_cast<Rat*>(fsm + f.lead);
+    Rat* trail = reinterpret_cast<Rat*>(fsm + f.trail);
+    int32_t* lo = reinterpret_cast<int32_t*>(fsm + f.lo);
+    int32_t* hi = reinterpret_cast<int32_t*>(fsm + f.hi);
+    int32_t* type = reinterpret_cast<int32_t*>(fsm + f.type);
+    uint8_t* memo = fsm + f.memo;
+    int32_t* cost = reinterpret_cast<int32_t*>(fsm + f.cost);
+    int32_t* act = reinterpret_cast<int32_t*>(fsm + f.act);
+    const int lane = threadIdx.x;
+    const int count = B.rcount[0];
+    for (;;) {
+        int i = 0;
+        if (lane == 0) i = atomicAdd(&B.rcount[1], 1);
+        i = __shfl_sync(0xffffffffu, i, 0);
+        if (i >= count) break;
+        const int qi = B.rlist[i];
+        const QDesc Q = B.q[qi];
+        const NetView v = net_view(B.P, Q.net);
+        const ChainView c = chain_view(B.P, Q.cl, Q.N);
+        const int N = Q.N;
+        const int L = (int)v.L, T = v.T;
+        int bad = (v.L > mL || T > mT || N > mN) ? 1 : 0;
+        if (!bad) {
+            for (int k = lane; k < T * L; k += 32) {
+                const int64_t x = v.fp[k] + v.bp[k];
+                if (x < 0 || x >= (1 << 19)) bad = 1;
+                cost[k] = (int32_t)x;
+            }
+            for (int j = lane; j < L; j += 32) {
+                const int64_t a = v.a[j];
+                if (a < 0 || a > INT32_MAX) bad = 1;
+                act[j] = (int32_t)a;
+            }
+            const int64_t o = Q.qstage_off;
+            for (int s = lane; s < N; s += 32) {
+                const int32_t l = B.qlo[o + s], h = B.qhi[o + s], ty = c.type[s];
+                lo[s] = l;
+                hi[s] = h;
+                type[s] = ty;
+                lead[s] = R(1);
+                trail[s] = R(1);
+                const int64_t x = stage_sum_whole(l, h, v.Pfp + (int64_t)ty * (v.L + 1)) +
+                                  stage_sum_whole(l, h, v.Pbp + (int64_t)ty * (v.L + 1));
+                if (x < 0 || x >= (1 << 20)) bad = 1;
+                t[s] = R(x);
+            }
+        }
+        bad = __any_sync(0xffffffffu, bad);
+        __syncwarp();
+        int64_t st[3] = {0, 0, 0};
+        int r = RF_BAIL;
+        if (!bad && lane == 0) {
+            FastRefine q{cost, act, type, L, N, lo, hi, lead, trail, t, memo};
+            r = refine_fast_walk(q, st);
+        }
+        r = __shfl_sync(0xffffffffu, r, 0);
+        if (r == RF_BAIL) {
+            if (lane == 0) B.rlist[B.nq + atomicAdd(&B.rcount[2], 1)] = qi;
+            __syncwarp();
+            continue;
+        }
+        __syncwarp();
+        refine_tail_warp(B, qi, lo, hi, lead, trail, st);
+        if (lane == 0) {
+            atomicAdd(&B.work[WORK_REFINE], (unsigned long long)st[1]);
+            atomicMax(&B.work[WORK_REFINE_MAX], (unsigned long long)st[1]);
+            atomicAdd(&B.work[WORK_REFINE_MOVES], (unsigned long long)st[2]);
+        }
+        __syncwarp();
     }
 }
 
@@ -404,22 +585,26 @@ __device__ __forceinline__ uint32_t est_slot(const BatchDev& B, uint64_t h) {
     return (uint32_t)(h ^ (h >> 32)) & (uint32_t)B.pmask;
 }
 
-// packed (capacity score, -index): the largest wins, ties to the smallest index
+// packed (capacity score, -index): the largest wins, ties to the smallest
+// index.  The score is the chain's smallest capacity in MiB, saturated at
+// 2^32 - 1 (any member may represent the class: the first estimate does not
+// depend on capacities; the score only makes a feasible representative
+// likely); candidate indices are < 2^31 (bp_batch_prepare).
 __device__ uint64_t est_score(const BatchDev& B, int64_t ci) {
     const QDesc Q = B.q[B.cq[ci]];
     const ChainView c = chain_view(B.P, Q.cl, Q.N);
     int64_t mn = INT64_MAX;
     for (int s = 0; s < Q.N; ++s) mn = c.cap[s] < mn ? c.cap[s] : mn;
     uint64_t capk = (uint64_t)mn >> 20;
-    if (capk > ((1ull << 41) - 1)) capk = (1ull << 41) - 1;
-    return (capk << 22) | (uint64_t)((1u << 22) - 1 - (uint32_t)(ci & ((1 << 22) - 1)));
+    if (capk > 0xffffffffull) capk = 0xffffffffull;
+    return (capk << 32) | (uint64_t)(0xffffffffu - (uint32_t)ci);
 }
 
 __device__ int64_t est_rep(const BatchDev& B, uint64_t h) {
     uint32_t slot = est_slot(B, h);
     for (uint32_t n = 0; B.pkey[slot] != h; slot = (slot + 1) & (uint32_t)B.pmask)
         if (++n > (uint32_t)B.pmask) __trap();   // key never inserted: a bug, fail loudly
-    return (int64_t)((1u << 22) - 1) - (int64_t)(B.pbest[slot] & ((1ull << 22) - 1));
+    return (int64_t)(0xffffffffu - (uint32_t)(B.pbest[slot] & 0xffffffffull));
 }
 
 // 1: the candidate's plan is the refined plan (it must wait for refine); 0:
@@ -717,7 +902,13 @@ size_t refine_region_bytes(int max_N) {
     return r;
 }
 
-void launch_refine(const BatchDev& B, int sms, cudaStream_t st) {
+size_t refine_fast_bytes(int max_N, int max_L, int max_T) { return fast_layout(max_N, max_L, max_T).bytes; }
+
+// slim kernel first (refine_fast.cuh), the general one on the queries it
+// hands back (rlist[nq ...], rcount[2]); fast_grid / fast_bytes: 0 = no slim
+// kernel (tables too large for shared memory)
+void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes, int max_L, int max_T,
+                   cudaStream_t st) {
     if (!B.nq) return;
     const size_t bytes = refine_region_bytes(B.max_N);
     // very long chains, or no dedup (tens of thousands of queries to refine:
@@ -726,14 +917,34 @@ void launch_refine(const BatchDev& B, int sms, cudaStream_t st) {
         k_refine<<<blocks(B.nq, 64), 64, 0, st>>>(B);
         return;
     }
-    static size_t attr = 0;
-    if (bytes > attr) {
-        cudaFuncSetAttribute(k_refine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        attr = bytes;
-    }
-    cudaMemsetAsync(B.rcount, 0, 2 * sizeof(int32_t), st);
+    cudaMemsetAsync(B.rcount, 0, 4 * sizeof(int32_t), st);
     k_refine_list<<<blocks(B.nq, 128), 128, 0, st>>>(B);
-    k_refine_smem<<<sms * 32, 32, bytes, st>>>(B, B.max_N);
+    if (fast_grid > 0) {
+        k_refine_fast<<<fast_grid, 32, fast_bytes, st>>>(B, B.max_N, max_L, max_T);
+        k_refine_smem<<<sms * 8, 32, bytes, st>>>(B, B.max_N, B.rlist + B.nq, B.rcount + 2);
+    } else {
+        k_refine_smem<<<sms * 32, 32, bytes, st>>>(B, B.max_N, B.rlist, B.rcount);
+    }
+}
+
+// per-device launch attributes (dynamic shared memory above 48 KB is a
+// per-device function attribute); called once per context
+int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes) {
+    const size_t bytes = refine_region_bytes(max_N);
+    if (bytes <= 200 * 1024)
+        cudaFuncSetAttribute(k_refine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    const size_t fb = refine_fast_bytes(max_N, max_L, max_T);
+    *fast_bytes = 0;
+    if (fb > 96 * 1024) return 0;
+    if (cudaFuncSetAttribute(k_refine_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb) != cudaSuccess)
+        return 0;
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_fast, 32, fb);
+    if (per_sm <= 0) return 0;
+    *fast_bytes = fb;
+    return sms * per_sm;
 }
 void launch_prune_reset(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.pkey, 0, ((size_t)B.pmask + 1) * sizeof(unsigned long long), st);
@@ -744,13 +955,18 @@ void launch_prune_reset(const BatchDev& B, cudaStream_t st) {
 // refined-path candidates only (both after one launch_prune_reset)
 void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part) {
     if (!B.ncand) return;
-    static int grid = 0;
-    if (!grid) {   // persistent: fill every SM to its register-limited occupancy
-        int dev = 0, sms = 0, per_sm = 0;
-        cudaGetDevice(&dev);
+    // persistent: fill every SM to its register-limited occupancy (per
+    // device: contexts on several devices may launch concurrently)
+    static std::atomic<int> grids[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int grid = dev < 64 ? grids[dev].load(std::memory_order_relaxed) : 0;
+    if (!grid) {
+        int sms = 0, per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_prune, 32, 0);
         grid = sms * (per_sm > 0 ? per_sm : 1);
+        if (dev < 64) grids[dev].store(grid, std::memory_order_relaxed);
     }
     if (part & 1) {
         k_prune_key<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);

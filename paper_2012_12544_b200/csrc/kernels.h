@@ -20,7 +20,10 @@ void launch_dedup(const BatchDev& B, cudaStream_t st);
 void launch_coarse_copy(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
-void launch_refine(const BatchDev& B, int sms, cudaStream_t st);
+void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes, int max_L, int max_T,
+                   cudaStream_t st);
+int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes);
+size_t refine_region_bytes(int max_N);
 // part: bit 0 = keys + work list, bit 1 = representatives, bit 2 = members (copy
 // the shared estimate, or list), bit 3 = the listed members
 void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part = 15);

@@ -693,6 +693,11 @@ BPK_HD void stage_times(const NetView& v, const ChainView& c, int s, const int32
     B = stage_sum_frac(lo[s], hi[s], lead[s], trail[s], v.Pbp + (int64_t)t * (v.L + 1), e);
 }
 
+#ifdef BPK_REFINE_TRACE
+void bpk_refine_trace(Rat t_hi, Rat t_lo, int64_t c_from, int64_t c_to, Rat avail, Rat x, Rat nh, Rat nl,
+                      Rat lead, Rat trail);
+#endif
+
 // One boundary step of intra_layer_refine (partition.hpp:302-327) decided on
 // scaled integers.  With D = lcm(den t_hi, den t_lo), every Rat the reference
 // forms in the step (t_hi - t_lo, x, x*1024, the quantization scores, t -
@@ -969,6 +974,9 @@ BPK_HD void refine_body(const NetView& v, const ChainView& c, int32_t* lo, int32
                     if (st.fs == FS_NOMOVE) continue;
                 }
                 const Rat x = st.x, nh = st.nh, nl = st.nl;
+#ifdef BPK_REFINE_TRACE
+                bpk_refine_trace(t_hi, t_lo, c_from, c_to, avail, x, nh, nl, lead[from], trail[from]);
+#endif
                 // apply_move (269-292)
                 int a = n0, b = n0 + 1;
                 if (dir > 0) {

@@ -140,6 +140,9 @@ BPK_HD bool refine_wanted(const BatchDev& B, int qi) {
     return Q.schema_ok && need && !qs.dp_shape && Q.N >= 2;
 }
 
+BPK_HD void refine_commit(const BatchDev& B, int qi, const NetView& v, const ChainView& c, const int32_t* lo,
+                          const int32_t* hi, const Rat* lead, const Rat* trail, const int64_t* rs, bool copy, Err e);
+
 // vo (nullable): the query's network view with its tables staged elsewhere
 // (shared memory in k_refine_smem)
 BPK_HDNI void refine_query_at(const BatchDev& B, int qi, const RefineScratch* sc, const NetView* vo = nullptr) {
@@ -162,7 +165,19 @@ BPK_HDNI void refine_query_at(const BatchDev& B, int qi, const RefineScratch* sc
     int64_t rs[4];
     if (sc) refine(v, c, lo, hi, lead, trail, sc->tF, sc->tB, sc->tT, sc->dirty, rs, e);
     else refine(v, c, lo, hi, lead, trail, B.qF + o, B.qB + o, B.qT + o, B.qdirty + o, rs, e);
-    if (sc) {
+    refine_commit(B, qi, v, c, lo, hi, lead, trail, rs, sc != nullptr, e);
+}
+
+// The refined plan (lo/hi/lead/trail, wherever the walk kept it) into the
+// query's arrays, with the walk's stats and its error, then the plan's stage
+// sums, simulator scale and validate_plan outcome.  Also the host emulation's
+// tail after refine_fast_walk (tests/emu); k_refine_fast has a warp version.
+BPK_HD void refine_commit(const BatchDev& B, int qi, const NetView& v, const ChainView& c, const int32_t* lo,
+                          const int32_t* hi, const Rat* lead, const Rat* trail, const int64_t* rs, bool copy, Err e) {
+    const QDesc Q = B.q[qi];
+    QState& qs = B.qs[qi];
+    const int64_t o = Q.qstage_off;
+    if (copy) {
         for (int s = 0; s < Q.N; ++s) {
             B.qlo[o + s] = lo[s];
             B.qhi[o + s] = hi[s];

@@ -250,6 +250,21 @@ def config_c5(models=128, shard=0, n_shards=1, model_base=0) -> Problem:
     return p
 
 
+def subset(p: Problem, idx) -> Problem:
+    """The queries `idx` of `p` as their own batch: same network and cluster
+    tables, queries in the given order, dense offsets re-laid out.  Global
+    query ids carry over (`query_ids`)."""
+    idx = np.asarray(idx, dtype=np.int64)
+    s = Problem(networks=p.networks, clusters=p.clusters, name=f"{p.name} [{idx.size} queries]")
+    q = np.ascontiguousarray(p.queries[idx])
+    s.m_lists = p.m_lists          # explicit M lists stay alive (pointers are copied)
+    s.queries = q
+    s.layout()
+    ids = getattr(p, "query_ids", None)
+    s.query_ids = (np.arange(p.queries.size, dtype=np.int64) if ids is None else ids)[idx]
+    return s
+
+
 def query_cost(L, N):
     """Estimated relative work of one query (DP rows x windows + simulation)."""
     L = np.asarray(L, dtype=np.float64)

@@ -12,6 +12,7 @@
 
 #include "../../paper_2012_12544_b200/csrc/host_prep.hpp"
 #include "../../paper_2012_12544_b200/csrc/phases.cuh"
+#include "../../paper_2012_12544_b200/csrc/refine_fast.cuh"
 #include "../../paper_2012_12544_b200/csrc/timeline.cuh"
 
 using namespace bpk;
@@ -23,6 +24,81 @@ unsigned long long bpk::bpk_opstats[16];
 namespace {
 
 const int64_t INF = INT64_MAX / 4;
+
+// Mirror of k_refine_fast (csrc/kernels.cu): the slim walk in its regime,
+// else the general refine (k_refine_smem).  BPEMU_NOFAST=1: general only;
+// BPEMU_FAST_CHECK=1: run both and abort on any difference.  Returns 1 when
+// the slim walk finished the query.
+int emu_refine(const BatchDev& B, int qi) {
+    if (!refine_wanted(B, qi)) return 0;
+    static const bool nofast = getenv("BPEMU_NOFAST") && atoi(getenv("BPEMU_NOFAST"));
+    static const bool check = getenv("BPEMU_FAST_CHECK") && atoi(getenv("BPEMU_FAST_CHECK"));
+    if (nofast) { refine_query(B, qi); return 0; }
+    const QDesc Q = B.q[qi];
+    const NetView v = net_view(B.P, Q.net);
+    const ChainView c = chain_view(B.P, Q.cl, Q.N);
+    const int N = Q.N, L = (int)v.L, T = v.T;
+    const int64_t o = Q.qstage_off;
+    std::vector<int32_t> cost((size_t)T * L), act(L), type(N), lo(N), hi(N);
+    std::vector<Rat> lead(N, R(1)), trail(N, R(1)), t(N);
+    std::vector<uint8_t> memo(N);
+    bool bad = false;
+    for (int k = 0; k < T * L; ++k) {
+        const int64_t x = v.fp[k] + v.bp[k];
+        bad |= x < 0 || x >= (1 << 19);
+        cost[k] = (int32_t)x;
+    }
+    for (int j = 0; j < L; ++j) {
+        bad |= v.a[j] < 0 || v.a[j] > INT32_MAX;
+        act[j] = (int32_t)v.a[j];
+    }
+    for (int s = 0; s < N; ++s) {
+        lo[s] = B.qlo[o + s];
+        hi[s] = B.qhi[o + s];
+        type[s] = c.type[s];
+        const int64_t x = stage_sum_whole(lo[s], hi[s], v.Pfp + (int64_t)type[s] * (v.L + 1)) +
+                          stage_sum_whole(lo[s], hi[s], v.Pbp + (int64_t)type[s] * (v.L + 1));
+        bad |= x < 0 || x >= (1 << 20);
+        t[s] = R(x);
+    }
+    if (getenv("BPEMU_DUMP_REFINE") && atoi(getenv("BPEMU_DUMP_REFINE")) == qi) {
+        // the slim walk's inputs of one query (tests/cpp/refine_walk_bench.cu)
+        FILE* f = fopen(getenv("BPEMU_DUMP_FILE") ? getenv("BPEMU_DUMP_FILE") : "/tmp/refine_query.bin", "wb");
+        int32_t hdr[3] = {L, T, N};
+        fwrite(hdr, 4, 3, f);
+        fwrite(cost.data(), 4, cost.size(), f);
+        fwrite(act.data(), 4, act.size(), f);
+        fwrite(type.data(), 4, N, f);
+        fwrite(lo.data(), 4, N, f);
+        fwrite(hi.data(), 4, N, f);
+        fwrite(t.data(), sizeof(Rat), N, f);
+        fclose(f);
+    }
+    int64_t st[4] = {0, 0, 0, 0};
+    int r = RF_BAIL;
+    if (!bad) {
+        FastRefine f{cost.data(), act.data(), type.data(), L, N, lo.data(), hi.data(), lead.data(), trail.data(),
+                     t.data(), memo.data()};
+        r = refine_fast_walk(f, st);
+    }
+    if (r == RF_BAIL) { refine_query(B, qi); return 0; }
+    if (check) {
+        refine_query(B, qi);
+        const QState& qs = B.qs[qi];
+        bool same = qs.refine_iters == st[0] && qs.refine_evals == st[1] && qs.refine_moves == st[2];
+        for (int s = 0; s < N; ++s)
+            same = same && B.qlo[o + s] == lo[s] && B.qhi[o + s] == hi[s] && B.qlead[o + s].n == lead[s].n &&
+                   B.qlead[o + s].d == lead[s].d && B.qtrail[o + s].n == trail[s].n && B.qtrail[o + s].d == trail[s].d;
+        if (!same) {
+            fprintf(stderr, "emu: slim refine differs from the general refine on query %d (N %d L %d)\n", qi, N, L);
+            abort();
+        }
+        // the general walk already committed; restore the DP plan is not needed
+        return 1;
+    }
+    refine_commit(B, qi, v, c, lo.data(), hi.data(), lead.data(), trail.data(), st, true, Err{ERR_NONE});
+    return 1;
+}
 
 // Sequential mirror of k_partition (csrc/dp.cu): same windows, same order.
 void host_partition(const BatchDev& B, const DPItem& item, uint64_t& work) {
@@ -362,9 +438,9 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
     for (int i = 0; i < nq; ++i)
         for (int m = 0; m < HB.q[i].nbase; ++m)
             if (bottleneck_slot(B, i, m)) host_partition(B, DPItem{i, m, B.ms[HB.q[i].mslot_off + m].a_th}, work);
-    int64_t r_it = 0, r_ev = 0, r_mv = 0, r_ex = 0, r_q = 0, r_max = 0;
+    int64_t r_it = 0, r_ev = 0, r_mv = 0, r_ex = 0, r_q = 0, r_max = 0, r_fast = 0;
     for (int i = 0; i < nq; ++i) {
-        refine_query(B, i);
+        r_fast += emu_refine(B, i);
         if (B.qs[i].refined) {
             ++r_q;
             r_it += B.qs[i].refine_iters;
@@ -375,8 +451,9 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
         }
     }
     if (getenv("BPEMU_STATS"))
-        fprintf(stderr, "emu refine: queries %lld iterations %lld evaluated steps %lld (max %lld) moves %lld exact %lld\n",
-                (long long)r_q, (long long)r_it, (long long)r_ev, (long long)r_max, (long long)r_mv, (long long)r_ex);
+        fprintf(stderr, "emu refine: queries %lld (slim %lld) iterations %lld evaluated steps %lld (max %lld) moves %lld exact %lld\n",
+                (long long)r_q, (long long)r_fast, (long long)r_it, (long long)r_ev, (long long)r_max, (long long)r_mv,
+                (long long)r_ex);
 #ifdef BPK_OPSTATS
     if (getenv("BPEMU_STATS")) {
         fprintf(stderr, "opstats");
