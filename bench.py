@@ -4,10 +4,12 @@
 Workload (BASELINE.json configs[4]): the sweep of 128
 synthetic models x 64 cluster mixes x 8 stage counts x 8 micro-batch counts x
 2 schedule kinds = 2^20 candidates (65,536 explore() queries).  A step is one
-pass of the explore() path over that batch.  Scaling is weak: rank r sweeps
-its own 2^20 candidates (models 128r..128r+127), so the whole job processes
-N * 2^20 candidates per step; the per-rank best records are exchanged with
-one NCCL allgather and reduced with the deterministic argmin.
+pass of the explore() path over that batch.  Scaling is strong by default
+(north_star: one 10^6-candidate sweep sharded over the GPUs): rank r runs the
+queries of its shard of the ONE sweep -- whole batch-dedup classes assigned
+by estimated cost (workloads.shard_classes) -- and the per-rank best records
+are exchanged with one NCCL allgather and reduced with the deterministic
+argmin.  --scaling weak gives every rank its own 2^20-candidate sweep.
 
   value   candidates/s with inputs resident in HBM (bp_batch_run), device
           time from CUDA events on the launching stream, max over ranks
@@ -37,7 +39,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 from paper_2012_12544_b200 import workloads as W  # noqa: E402
-from paper_2012_12544_b200.problem import BEST_DTYPE, Problem  # noqa: E402
+from paper_2012_12544_b200.problem import BEST_DTYPE  # noqa: E402
 
 METRIC = "partition candidates evaluated/sec (C5 sweep)"
 UNIT = "candidates/s"
@@ -53,6 +55,7 @@ def parse():
     ap.add_argument("--models", type=int, default=128, help="models per rank (128 = full 2^20 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-stride", type=int, default=127)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     return ap.parse_args()
 
 
@@ -186,17 +189,33 @@ def rooflines(stats, steps, clocks, problem, step_ms):
         ms = v["ms"] / max(1, v["launches"])
         e = {"ms_per_step": v["ms"] / steps, "launches": v["launches"], "work_per_launch": v["work"]}
         ops = kernel_work_ops(k, v["work"])
-        if ops is not None and ms > 0:
+        if ops is not None and ms > 0 and not k.startswith("sim_"):
             e["achieved_gops"] = ops / (ms * 1e6)
             e["frac"] = e["achieved_gops"] / issue_peak
+        elif k.startswith("sim_"):
+            # the simulator classes run concurrently on two streams: a
+            # kernel's event-timed span includes the other stream's work, so
+            # rates are quoted on the phase (phases_ms_per_step), not here
+            e["note"] = "overlapped on two streams; see phases_ms_per_step"
         kern[k] = e
     crit = stats.pop("refine_critical_path", None)
     kern.pop("refine_critical_path", None)
     kern["counters"] = counters
     kern["phases_ms_per_step"] = phases
-    dom = max(stats, key=lambda k: stats[k]["ms"])
+    # the simulator classes overlap on two streams: as a group they are one
+    # "kernel" (the phase span, all simulated events)
+    sims = [k for k in stats if k.startswith("sim_") and k not in ("sim_prep", "sim_share")]
+    if sims and "phase_sims" in phases:
+        ev = sum(stats[k]["work"] for k in sims)
+        kern["simulate"] = {"ms_per_step": phases["phase_sims"], "launches": steps, "work_per_launch": ev,
+                            "achieved_gops": ev * OPS_PER_EVENT / (phases["phase_sims"] * 1e6),
+                            "note": "all simulator kernels of the step (both streams): phase span, all events"}
+        kern["simulate"]["frac"] = kern["simulate"]["achieved_gops"] / issue_peak
+    cands = {k: kern[k]["ms_per_step"] for k in kern if isinstance(kern[k], dict) and "ms_per_step" in kern[k]
+             and not k.startswith("sim_")}
+    dom = max(cands, key=cands.get)
     d = kern[dom]
-    u = work_unit(dom)
+    u = ("simulated events", OPS_PER_EVENT) if dom == "simulate" else work_unit(dom)
     roof = {"kernel": dom, "bound": "issue", "unit": "Gop/s", "peak": issue_peak,
             "achieved": d.get("achieved_gops"), "frac": d.get("frac"),
             "traffic": traffic.get(dom),
@@ -204,14 +223,17 @@ def rooflines(stats, steps, clocks, problem, step_ms):
                      is not None else f"{dom}: no work count"),
             "peak_source": f"{SMS} SMs x {LANES} lanes x {f_max / 1e6:.0f} MHz (sm_max_mhz, {peak_kind} "
                            f"MEASURED_PEAKS.json); HBM {peaks.get('hbm_gbs')} GB/s"}
-    if dom == "refine" and crit and crit["work"] > 0:
+    refine_lat = None
+    if crit and crit["work"] > 0 and "refine" in kern:
         # refine is a serial recurrence per query: its time is the longest
         # query's walk, so the meaningful bound is per-step latency on that path
-        ms_launch = d["ms_per_step"]
-        roof["critical_path"] = {"boundary_steps": crit["work"], "us_per_step": 1e3 * ms_launch / crit["work"],
-                                 "cycles_per_step": ms_launch * 1e-3 * f_max / crit["work"],
-                                 "note": "one query's intra_layer_refine walk is serial (each boundary step "
-                                         "reads the stage times the previous step wrote)"}
+        ms_launch = kern["refine"]["ms_per_step"]
+        refine_lat = {"longest_walk_steps": crit["work"], "refine_ms_per_step": ms_launch,
+                      "us_per_step_in_sweep": 1e3 * ms_launch / crit["work"],
+                      "cycles_per_step_in_sweep": ms_launch * 1e-3 * f_max / crit["work"],
+                      "note": "one query's intra_layer_refine walk is serial (each boundary step reads the stage "
+                              "times the previous step wrote): the refine launch cannot end before its longest "
+                              "walk, so its bound is that walk's latency alone on an idle GPU (walk_alone)"}
     # sweep bound: t_roof = sum B_cost / BW + (X_dp * c_dp + X_sim * c_sim) / issue
     q = problem.queries
     U = np.array([problem.networks[i].L for i in q["network"]], dtype=np.float64)
@@ -225,34 +247,56 @@ def rooflines(stats, steps, clocks, problem, step_ms):
     hbm = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
     t_ref = b_cost / hbm + (x_dp_ref * OPS_PER_TRANSITION + x_sim * OPS_PER_EVENT) / (issue_peak * 1e9)
     t_own = b_cost / hbm + (x_dp * OPS_PER_TRANSITION + x_sim * OPS_PER_EVENT) / (issue_peak * 1e9)
-    sweep = {"t_roof_ms_reference_dp": 1e3 * t_ref, "t_roof_ms_banded_dp": 1e3 * t_own, "t_measured_ms": step_ms,
-             "frac": 1e3 * t_ref / step_ms,
-             "x_dp_reference": x_dp_ref, "x_dp_performed": x_dp, "x_sim_events": x_sim, "b_cost_bytes": b_cost,
-             "formula": "t_roof = B_cost/HBM + (X_dp*3 + X_sim*3)/(148*128*f_max); frac = t_roof(reference X_dp) / "
-                        "t_measured (SURVEY.md 8d)"}
-    return roof, kern, sweep
+    # a cheaper DP must charge the work it performs, so the
+    # fraction is t_roof(performed X_dp, simulated events) / t_measured.  The
+    # reference's X_dp at the same pace is a work-equivalence figure only.
+    sweep = {"t_roof_ms": 1e3 * t_own, "t_measured_ms": step_ms, "frac": 1e3 * t_own / step_ms,
+             "x_dp_performed": x_dp, "x_sim_events": x_sim, "b_cost_bytes": b_cost,
+             "formula": "t_roof = B_cost/HBM + (X_dp*3 + X_sim*3)/(148*128*f_max) over the work performed; "
+                        "frac = t_roof / t_measured (SURVEY.md 8d)",
+             "work_equivalence": {"x_dp_reference": x_dp_ref, "t_roof_ms_reference_dp": 1e3 * t_ref,
+                                  "ratio": 1e3 * t_ref / step_ms,
+                                  "note": "the reference's own DP transitions (3L^2-class loops) at roofline pace "
+                                          "against our measured step: how much reference work one step replaces, "
+                                          "not a roofline fraction"}}
+    return roof, kern, sweep, refine_lat
 
 
 def cpu_baseline(problem, stride, threads):
-    """The reference's own explore() (oracle/_ref) on a bounded C5 sample."""
+    """The reference's own explore() (oracle/_ref) on a bounded C5 sample:
+    the -O3 -march=native timing build, and the bounds-checking parity build
+    beside it."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import PortOracle, RefOracle, ref_available
-    oracle = RefOracle() if ref_available() else PortOracle()
     idx = np.arange(0, problem.queries.size, stride)
-    sub = Problem(networks=problem.networks, clusters=problem.clusters)
-    q = problem.queries[idx]
-    sub.set_queries(q["network"], q["cluster"], q["n_stages"], q["mini_batch"])
-    t = time.perf_counter()
-    if oracle.kind == "reference":
-        res = oracle.explore_timed(sub, threads=threads)
-    else:
-        res, _, _ = oracle.explore(sub, details=False)
-        threads = 1
-    dt = time.perf_counter() - t
-    return {"value": sub.total_candidates / dt, "unit": UNIT, "cores": threads, "kind": oracle.kind,
-            "sample": f"C5 1/{stride} query stride ({sub.queries.size} queries, {sub.total_candidates} "
-                      f"candidates), explore() per query on {threads} host threads, {dt:.1f} s",
-            "status_hist": np.bincount(res["status"], minlength=7).tolist()}
+    sub = W.subset(problem, idx)
+
+    def timed(oracle):
+        t = time.perf_counter()
+        if oracle.kind == "reference":
+            res = oracle.explore_timed(sub, threads=threads)
+            n = threads
+        else:
+            res, _, _ = oracle.explore(sub, details=False)
+            n = 1
+        return time.perf_counter() - t, res, n
+
+    if not ref_available():
+        oracle = PortOracle()
+        dt, res, n = timed(oracle)
+        return {"value": sub.total_candidates / dt, "unit": UNIT, "cores": n, "kind": "port",
+                "sample": f"C5 1/{stride} query stride ({sub.total_candidates} candidates), {dt:.1f} s"}
+    fast = RefOracle(fast=True)
+    dt, res, n = timed(fast)
+    out = {"value": sub.total_candidates / dt, "unit": UNIT, "cores": n, "kind": "reference", "build": fast.build,
+           "sample": f"C5 1/{stride} query stride ({sub.queries.size} queries, {sub.total_candidates} "
+                     f"candidates), explore() per query on {n} host threads, {dt:.1f} s",
+           "status_hist": np.bincount(res["status"], minlength=7).tolist()}
+    checked = RefOracle()
+    if checked.build != fast.build:
+        dt2, _, _ = timed(checked)
+        out["checking_build"] = {"value": sub.total_candidates / dt2, "build": checked.build, "seconds": dt2}
+    return out
 
 
 def run_reference(args):
@@ -263,14 +307,12 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import PortOracle, RefOracle, ref_available
-    oracle = RefOracle() if ref_available() else PortOracle()
+    oracle = RefOracle(fast=True) if ref_available() else PortOracle()
     stride = 257    # prime: 255-256 queries (~4,096 candidates) per step, rotating offsets
     times, cands = [], []
     for step in range(args.warmup + args.steps):
         idx = np.arange(step % stride, p.queries.size, stride)
-        sub = Problem(networks=p.networks, clusters=p.clusters)
-        q = p.queries[idx]
-        sub.set_queries(q["network"], q["cluster"], q["n_stages"], q["mini_batch"])
+        sub = W.subset(p, idx)
         t = time.perf_counter()
         if oracle.kind == "reference":
             oracle.explore_timed(sub, threads=threads)
@@ -283,14 +325,36 @@ def run_reference(args):
     value = sum(cands) / sum(times)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64/exact-rational",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "int64/exact-rational",
             "data": "synthetic (C5 generator, mt19937_64 seeds of SURVEY.md 8d)",
             "config": {"workload": "C5 sweep sample: 1/257 query stride per step (~256 queries, ~4,096 candidates), "
                                    "rotating offsets", "models": args.models},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads if oracle.kind == "reference" else 1,
-                             "kind": oracle.kind, "sample": "1/257 query stride of C5 per step, offset = step index"},
+                             "kind": oracle.kind, "build": getattr(oracle, "build", "port"),
+                             "sample": "1/257 query stride of C5 per step, offset = step index"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+LONGEST_WALK_QUERY = 18895     # C5's longest refine walk (N = 64, L = 128, 3,255 boundary steps)
+
+
+def walk_alone(ex, full, sp):
+    """The refine launch of a batch holding only C5's longest-walk query:
+    its walk's latency on an otherwise idle GPU (the refine phase's floor)."""
+    one = W.subset(full, [LONGEST_WALK_QUERY])
+    b = ex.prepare(one, details=False, stream=sp)
+    ex.run(b, stream=sp)
+    ex.profiling(True)
+    for _ in range(3):
+        ex.run(b, stream=sp)
+    ex.fetch(b, one, stream=sp)
+    st = ex.kernel_stats()
+    ex.profiling(False)
+    ex.free(b)
+    r = st.get("refine", {})
+    return {"query": LONGEST_WALK_QUERY, "steps": st.get("refine_critical_path", {}).get("work", 0),
+            "ms": r.get("ms", 0) / max(1, r.get("launches", 1))}
 
 
 def run_b200(args):
@@ -305,7 +369,16 @@ def run_b200(args):
     stream = torch.cuda.Stream()
     sp = stream.cuda_stream
 
-    p = W.config_c5(models=args.models, model_base=rank * args.models)
+    if args.scaling == "strong":
+        # ONE sweep, sharded: whole dedup classes per rank, balanced by cost
+        full = W.config_c5(models=args.models)
+        p = W.subset(full, W.shard_classes(full, world)[rank]) if world > 1 else full
+        cands_per_step = full.total_candidates
+    else:
+        full = W.config_c5(models=args.models, model_base=rank * args.models)
+        p = full
+        cands_per_step = p.total_candidates * world
+    qids = getattr(p, "query_ids", np.arange(p.queries.size, dtype=np.int64))
     p.pin()
     ex = Explorer(local)
     ex.load(p)
@@ -316,6 +389,15 @@ def run_b200(args):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x, [x]
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        torch.distributed.all_gather(allt, t)
+        v = [float(a.item()) for a in allt]
+        return max(v), v
 
     # ---- device-resident steps (value)
     with torch.cuda.stream(stream):
@@ -339,12 +421,7 @@ def run_b200(args):
     stats = ex.kernel_stats()
     ex.profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-    cands_per_step = p.total_candidates * world
+    total_ms, rank_ms = max_over_ranks(sum(step_ms))
     value = cands_per_step * args.steps / (total_ms / 1e3)
 
     # ---- the same steps with the batch dedup off (BP_OPT_DEDUP = 0: every
@@ -362,17 +439,17 @@ def run_b200(args):
             nd_evs[i][1].record(stream)
     barrier()
     ex.dedup(True)
-    nd_ms = sum(a.elapsed_time(b) for a, b in nd_evs)
-    if world > 1:
-        t = torch.tensor([nd_ms], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        nd_ms = float(t.item())
+    nd_ms, _ = max_over_ranks(sum(a.elapsed_time(b) for a, b in nd_evs))
     value_nodedup = cands_per_step * args.steps / (nd_ms / 1e3)
 
     # ---- global best: per-rank record -> one allgather -> deterministic argmin
     rec = torch.zeros(BEST_DTYPE.itemsize, dtype=torch.uint8, device="cuda")
-    ex.best(batch, rec.data_ptr(), query_base=rank * p.queries.size, stream=sp)
+    ex.best(batch, rec.data_ptr(), query_base=0, stream=sp)
     torch.cuda.synchronize()
+    r0 = rec.cpu().numpy().view(BEST_DTYPE).copy()
+    if r0[0]["valid"]:
+        r0[0]["query_id"] = int(qids[int(r0[0]["query_id"])])   # shard-local -> global query id
+    rec.copy_(torch.from_numpy(r0.view(np.uint8)).to(rec.device))
     if world > 1:
         allrec = [torch.zeros_like(rec) for _ in range(world)]
         torch.distributed.all_gather(allrec, rec)
@@ -402,14 +479,11 @@ def run_b200(args):
         e2e_ms.append(1e3 * (time.perf_counter() - t))
     barrier()
     h2, d2 = ex.transfers()
-    e2e_total = sum(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_total = float(t.item())
+    e2e_total, _ = max_over_ranks(sum(e2e_ms))
     e2e_value = cands_per_step * args.steps / (e2e_total / 1e3)
     assert r2.tobytes() == res.tobytes(), "e2e results differ from the device-resident run"
 
+    alone = walk_alone(ex, full, sp) if (rank == 0 and args.models == 128 and args.scaling == "strong") else None
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
@@ -417,32 +491,44 @@ def run_b200(args):
 
     # ---- roofline of the dominant kernel
     clocks = clk.summary()
-    roof, kern, sweep = rooflines(stats, args.steps, clocks, p, total_ms / args.steps)
-
+    roof, kern, sweep, refine_lat = rooflines(stats, args.steps, clocks, p, total_ms / args.steps)
+    if refine_lat is not None and alone is not None and alone["ms"] > 0:
+        refine_lat["walk_alone"] = alone
+        refine_lat["latency_bound_frac"] = alone["ms"] / refine_lat["refine_ms_per_step"]
+    mean_ms = sum(rank_ms) / len(rank_ms)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64/exact-rational",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64/exact-rational",
             "data": "synthetic (C5 generator, mt19937_64 seeds of SURVEY.md 8d; random-init layer tables)",
             "config": {"workload": "C5 sweep: 128 models x 64 cluster mixes x 8 stage counts x 8 M x 2 kinds "
-                                   "= 2^20 candidates per GPU",
-                       "queries_per_gpu": int(p.queries.size), "candidates_per_gpu": int(p.total_candidates),
-                       "parallelism": f"weak x{world} (query shards per GPU, NCCL allgather of best records)",
+                                   "= 2^20 candidates" + (" in total, sharded over the GPUs" if args.scaling == "strong"
+                                                          else " per GPU"),
+                       "queries": int(full.queries.size) if args.scaling == "strong" else int(p.queries.size) * world,
+                       "candidates_per_step": int(cands_per_step),
+                       "parallelism": (f"strong x{world} (whole dedup classes per GPU, cost-balanced; NCCL allgather "
+                                       f"of one best record per rank)" if args.scaling == "strong" else
+                                       f"weak x{world} (a 2^20-candidate sweep per GPU; NCCL allgather of best "
+                                       f"records)"),
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_total / args.steps,
                     "h2d_bytes_per_step": (h2 - h1) // args.steps, "d2h_bytes_per_step": (d2 - d1) // args.steps},
             "no_dedup": {"value": value_nodedup, "unit": UNIT, "ms_per_step": nd_ms / args.steps,
                          "note": "same steps with BP_OPT_DEDUP=0: identical subproblems of the batch not shared"},
+            "ranks": {"ms_per_step": [x / args.steps for x in rank_ms],
+                      "imbalance_max_over_mean": max(rank_ms) / mean_ms if mean_ms > 0 else None,
+                      "queries_rank0": int(p.queries.size)},
             "gpu_launches": launches,
             "clocks": clocks,
             "roofline": roof,
             "sweep_roofline": sweep,
+            "refine_latency": refine_lat,
             "kernels": kern,
             "best": {"makespan": f"{int(best['makespan']['num'])}/{int(best['makespan']['den'])}",
                      "M": int(best["M"]), "kind": int(best["kind"]), "query_id": int(best["query_id"])},
             "query_status_hist": np.bincount(res["status"], minlength=7).tolist()}
     if not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(p, args.cpu_sample_stride, os.cpu_count() or 1)
+            line["cpu_baseline"] = cpu_baseline(full, args.cpu_sample_stride, os.cpu_count() or 1)
         except Exception as e:   # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)}
     print(json.dumps(line), flush=True)

@@ -20,6 +20,7 @@ from paper_2012_12544_b200.problem import Problem, ptr
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libbapipe_ref.so")
+REF_FAST_SO = os.path.join(HERE, "_ref", "libbapipe_ref_fast.so")   # -O3 -march=native, timing only
 PORT_SO = os.path.join(HERE, "_build", "libbapipe_oracle.so")
 
 
@@ -47,10 +48,14 @@ class _Base:
 class RefOracle(_Base):
     kind = "reference"
 
-    def __init__(self):
-        if not os.path.exists(REF_SO):
-            raise RuntimeError(f"{REF_SO} not built (make -C oracle ref)")
-        self.lib = C.CDLL(REF_SO)
+    def __init__(self, fast=False):
+        """fast: the timing build (no bounds checks, so no REF_UB detection);
+        falls back to the checking build when it is absent."""
+        so = REF_FAST_SO if fast and os.path.exists(REF_FAST_SO) else REF_SO
+        if not os.path.exists(so):
+            raise RuntimeError(f"{so} not built (make -C oracle ref)")
+        self.lib = C.CDLL(so)
+        self.build = "-O3 -march=native" if so == REF_FAST_SO else "-O3 -D_GLIBCXX_ASSERTIONS"
         vp = C.c_void_p
         self.lib.bpref_explore_batch.restype = C.c_int
         self.lib.bpref_explore_batch.argtypes = [vp, C.c_int, vp, C.c_int, vp, C.c_int, vp, vp, vp, C.c_int]

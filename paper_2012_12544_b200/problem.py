@@ -234,6 +234,9 @@ class Problem:
         return self
 
     def alloc_outputs(self, details=True, pinned=False):
+        """details: True = query, candidate and stage records; "candidates" =
+        query and candidate records (no per-stage plans); False = query
+        records only."""
         if pinned:
             import torch
             r = torch.empty(self.queries.size * RESULT_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
@@ -242,7 +245,7 @@ class Problem:
             return res, None, None
         res = np.zeros(self.queries.size, dtype=RESULT_DTYPE)
         cand = np.zeros(self.total_candidates, dtype=CAND_DTYPE) if details else None
-        st = np.zeros(self.total_stages, dtype=STAGE_DTYPE) if details else None
+        st = np.zeros(self.total_stages, dtype=STAGE_DTYPE) if details and details != "candidates" else None
         return res, cand, st
 
 

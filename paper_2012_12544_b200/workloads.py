@@ -265,6 +265,62 @@ def subset(p: Problem, idx) -> Problem:
     return s
 
 
+def query_classes(p: Problem):
+    """Batch-dedup class of every query: (network, stage count, accelerator
+    type chain of the used prefix) -- the key under which the engine shares
+    the whole-layer DP and refine (kernels.cu k_dedup_*).  Returns the class
+    index per query (classes numbered in first-appearance order)."""
+    q = p.queries
+    keys = {}
+    out = np.empty(q.size, dtype=np.int64)
+    for i in range(q.size):
+        cl = p.clusters[int(q["cluster"][i])]
+        n = int(q["n_stages"][i]) or cl.N
+        k = (int(q["network"][i]), n, cl.types[:n].tobytes())
+        out[i] = keys.setdefault(k, len(keys))
+    return out
+
+
+def class_cost(p: Problem, cls):
+    """Estimated cost of each dedup class: one DP fill (~U^2 transitions after
+    the banded DP's early exits) and one refine walk (~N x U boundary-step
+    units) per class, plus the class's simulated events (2NM, +2(N-1)M sync,
+    per query and M).  Relative units; used only to balance shards."""
+    q = p.queries
+    ncls = int(cls.max()) + 1 if cls.size else 0
+    cost = np.zeros(ncls)
+    seen = np.zeros(ncls, dtype=bool)
+    Ms = np.array([1, 2, 4, 8, 16, 32, 64, 128], dtype=np.float64)
+    for i in range(q.size):
+        c = int(cls[i])
+        L = float(p.networks[int(q["network"][i])].L)
+        n = float(int(q["n_stages"][i]) or p.clusters[int(q["cluster"][i])].N)
+        sync = p.clusters[int(q["cluster"][i])].mode == MODE_SYNC
+        if not seen[c]:
+            seen[c] = True
+            cost[c] += L * L + 40.0 * n * L
+        ev = 2 * n * Ms + (2 * (n - 1) * Ms if sync else 0)
+        cost[c] += 2.0 * float(ev.sum())
+    return cost
+
+
+def shard_classes(p: Problem, n_shards: int):
+    """Strong-scaling shards of one sweep: whole dedup classes (so no rank
+    re-solves another's DP / refine), assigned heaviest-first to the least
+    loaded rank (LPT) by class_cost.  Returns the sorted query indices of each
+    shard."""
+    cls = query_classes(p)
+    cost = class_cost(p, cls)
+    owner = np.empty(cost.size, dtype=np.int64)
+    load = np.zeros(n_shards)
+    for c in np.argsort(-cost, kind="stable"):
+        r = int(np.argmin(load))
+        owner[c] = r
+        load[r] += cost[c]
+    qo = owner[cls]
+    return [np.nonzero(qo == r)[0] for r in range(n_shards)]
+
+
 def query_cost(L, N):
     """Estimated relative work of one query (DP rows x windows + simulation)."""
     L = np.asarray(L, dtype=np.float64)
