@@ -489,7 +489,25 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
     for (int64_t c = 0; c < HB.ncand; ++c) {
         int cls = sim_classify(B, c);
         if (cls < 0) continue;
+#ifdef BPK_OPSTATS
+        unsigned long long before[16];
+        for (int k = 0; k < 16; ++k) before[k] = bpk_opstats[k];
+#endif
         sim_exact(B, c, S);
+        if (getenv("BPEMU_DUMP_SIM") && cls >= SIM_EXACT) {
+            // the exact simulator's inputs (stage F / B, link SR) of exact-class candidates
+            static FILE* df = fopen(getenv("BPEMU_DUMP_SIM"), "w");
+            const bp_candidate& cd = B.cand[c];
+            fprintf(df, "C %lld %d %lld %d %d", (long long)c, cd.n_stages, (long long)cd.M, cd.kind, cd.status);
+            for (int s = 0; s < cd.n_stages; ++s)
+                fprintf(df, " %lld %lld %lld %lld %lld", (long long)S.dF(s).n, (long long)S.dF(s).d,
+                        (long long)S.dB(s).n, (long long)S.dB(s).d, (long long)S.sr(s));
+            fprintf(df, "\n");
+        }
+#ifdef BPK_OPSTATS
+        if (cls < SIM_EXACT)   // count the exact-class candidates' Rat work only
+            for (int k = 0; k < 16; ++k) bpk_opstats[k] = before[k];
+#endif
         if (cls == SIM_EXACT) {
             ++exact_n;
             exact_ovf += B.cand[c].status == BP_C_ERR_OVERFLOW;
@@ -503,6 +521,13 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
     if (getenv("BPEMU_STATS"))
         fprintf(stderr, "emu sim: fast %lld exact %lld (overflow %lld)\n", (long long)fast_n, (long long)exact_n,
                 (long long)exact_ovf);
+#ifdef BPK_OPSTATS
+    if (getenv("BPEMU_STATS")) {
+        fprintf(stderr, "opstats after sims");
+        for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", bpk_opstats[k]);
+        fprintf(stderr, "\n");
+    }
+#endif
     for (int i = 0; i < nq; ++i) rank_query(B, i);
     std::memcpy(res, B.res, sizeof(bp_query_result) * (size_t)nq);
     if (cand) std::memcpy(cand, B.cand, sizeof(bp_candidate) * (size_t)HB.ncand);
