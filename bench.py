@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--models", type=int, default=128, help="models per rank (128 = full 2^20 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-per-call", action="store_true")
     ap.add_argument("--cpu-sample-stride", type=int, default=127)
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     return ap.parse_args()
@@ -299,6 +300,50 @@ def cpu_baseline(problem, stride, threads):
     return out
 
 
+def per_call(reps_small=20, reps_c4=3):
+    """explore() on single queries, one call at a time (BASELINE.md's CPU
+    plan: C1-C3 >= 20 repetitions, C4 in its variants): the drop-in's
+    explore() (include/bapipe_b200/explorer.hpp, host structs in, result out,
+    every candidate on the GPU) against the reference's own explore() on one
+    host core (-O3 -march=native) and, as aggregate calls/s, on every core."""
+    import tempfile
+    prod = os.path.join(ROOT, "paper_2012_12544_b200", "bin", "percall")
+    ref = os.path.join(ROOT, "oracle", "_ref", "percall_ref")
+    if not os.path.exists(prod):
+        return {"error": "paper_2012_12544_b200/bin/percall not built"}
+    out = {"cases": [], "note": "wall ms per explore() call; product: first call of a context excluded (2 warm-up "
+                                "calls per case)"}
+    with tempfile.TemporaryDirectory() as d:
+        groups = {"small": [], "c4": []}
+        for name, p, types in W.single_query_configs():
+            q = p.queries[0]
+            nf, cf = os.path.join(d, f"{len(out['cases'])}_net.json"), os.path.join(d, f"{len(out['cases'])}_cl.json")
+            with open(nf, "w") as f:
+                json.dump(W.network_json(p.networks[0], types), f)
+            with open(cf, "w") as f:
+                json.dump(W.cluster_json(p.clusters[0], types), f)
+            groups["c4" if name.startswith("C4") else "small"].append((name, str(int(q["mini_batch"])), nf, cf))
+            out["cases"].append(name)
+
+        def run(exe, reps, cases, threads=0):
+            cmd = [exe] + (["--threads", str(threads)] if threads else []) + [str(reps)]
+            for _, mb, nf, cf in cases:
+                cmd += [mb, nf, cf]
+            r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+            return [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+
+        res = {}
+        for who, exe, threads in (("b200", prod, 0), ("reference", ref, os.cpu_count() or 1)):
+            if not os.path.exists(exe):
+                res[who] = None
+                continue
+            rows = run(exe, reps_small, groups["small"], threads) + run(exe, reps_c4, groups["c4"], 0)
+            res[who] = {name: {k: v for k, v in r.items() if k != "ms" and k != "case"}
+                        for name, r in zip([c[0] for c in groups["small"] + groups["c4"]], rows)}
+        out.update(res)
+    return out
+
+
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -531,6 +576,12 @@ def run_b200(args):
             line["cpu_baseline"] = cpu_baseline(full, args.cpu_sample_stride, os.cpu_count() or 1)
         except Exception as e:   # the baseline is reported, never required
             line["cpu_baseline"] = {"value": None, "error": str(e)}
+    if not args.no_per_call:
+        ex.close()
+        try:
+            line["per_call"] = per_call()
+        except Exception as e:
+            line["per_call"] = {"error": str(e)}
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -87,12 +87,31 @@ def build_cli(force=False):
     return CLI
 
 
+PERCALL = os.path.join(HERE, "bin", "percall")
+
+
+def build_percall(force=False):
+    """bench.py's per-call latency tool (cli/percall.cpp) on the drop-in
+    explore(); oracle/Makefile builds the same source against the reference."""
+    if not os.path.exists(os.path.join(JSON_DIR, "json.hpp")):
+        return None
+    src = os.path.join(HERE, "cli", "percall.cpp")
+    deps = [src, SO] + [os.path.join(ROOT, "include", "bapipe_b200", f) for f in ("explorer.hpp", "io.hpp")]
+    if not force and not _stale(PERCALL, deps):
+        return PERCALL
+    os.makedirs(os.path.dirname(PERCALL), exist_ok=True)
+    subprocess.run([_host_cxx(), "-std=c++17", "-O2", "-pthread", "-I" + os.path.join(ROOT, "include"),
+                    "-I" + JSON_DIR, "-o", PERCALL, src, "-L" + HERE, "-lbapipe_b200", "-Wl,-rpath,$ORIGIN/.."],
+                   check=True)
+    return PERCALL
+
+
 def build_oracles():
     """Test-only checkers: the C restatement always, oracle/_ref when the
     reference sources are present (dev container only)."""
     targets = ["oracle"]
     if os.path.isdir("/root/reference/proj/include"):
-        targets += ["ref", "dropin", "cli"]
+        targets += ["ref", "dropin", "cli", "percall"]
     subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle")] + targets, check=True)
     emu = os.path.join(ROOT, "tests", "emu")
     if os.path.isdir(emu):
@@ -105,5 +124,6 @@ def build_oracles():
 if __name__ == "__main__":
     build_product(force="--force" in sys.argv, verbose="-v" in sys.argv)
     build_cli(force="--force" in sys.argv)
+    build_percall(force="--force" in sys.argv)
     build_oracles()
     print(SO)

@@ -250,6 +250,45 @@ def config_c5(models=128, shard=0, n_shards=1, model_base=0) -> Problem:
     return p
 
 
+KINDS = ("1f1b-as", "fbp-as", "1f1b-sno", "1f1b-so")
+
+
+def network_json(net: Network, type_names, name="net") -> dict:
+    """NetworkProfile in the reference's JSON schema (profiles.hpp:194-217,
+    274-290); type_names maps type ids to accelerator type strings."""
+    layers = []
+    for j in range(net.L):
+        fp = {type_names[t]: int(net.fp[t, j]) for t in range(net.T) if net.fp[t, j] > 0}
+        bp = {type_names[t]: int(net.bp[t, j]) for t in range(net.T) if net.bp[t, j] > 0}
+        layers.append({"name": f"l{j}", "fp_us": fp, "bp_us": bp, "weight_bytes": int(net.w[j]),
+                       "out_activation_bytes": int(net.a[j])})
+    return {"name": name, "layers": layers}
+
+
+def cluster_json(cl: Cluster, type_names, n=None) -> dict:
+    """ClusterSpec in the reference's JSON schema (profiles.hpp:219-261,
+    292-303), the first n accelerators."""
+    n = cl.N if n is None else n
+    accels = []
+    for i in range(n):
+        a = {"id": f"acc{i}", "type": type_names[int(cl.types[i])], "mem_capacity_bytes": int(cl.cap[i])}
+        mm = {KINDS[k]: int(cl.min_micro[i, k]) for k in range(4) if cl.min_micro[i, k] != 1}
+        if mm:
+            a["min_micro_batch"] = mm
+        accels.append(a)
+    return {"execution_mode": "async" if cl.mode == MODE_ASYNC else "sync", "accelerators": accels,
+            "link_bandwidth_bytes_per_us": [int(b) for b in cl.bw[:n - 1]]}
+
+
+def single_query_configs():
+    """(name, Problem, type names) of the one-query configs C1-C4 (SURVEY.md
+    8d) -- the reference's own per-call use of explore()."""
+    return [("C1", config_c1(), ["v100"]), ("C2", config_c2(), ["v100"]), ("C3", config_c3(), ["v100", "p100"]),
+            ("C4 onchip", config_c4("onchip"), ["vcu118", "vcu129"]),
+            ("C4 offchip", config_c4("offchip"), ["vcu118", "vcu129"]),
+            ("C4 homogeneous", config_c4("homogeneous"), ["vcu118", "vcu129"])]
+
+
 def subset(p: Problem, idx) -> Problem:
     """The queries `idx` of `p` as their own batch: same network and cluster
     tables, queries in the given order, dense offsets re-laid out.  Global
