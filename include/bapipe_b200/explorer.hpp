@@ -426,6 +426,35 @@ inline std::string invalid_plan_message(const bp_candidate& c) {
     }
 }
 
+// The accelerator-type lookups of stage_fp_time / stage_bp_time (plan.hpp:
+// 90-108) in stage_costs / chain_instance order (cost_models.hpp:103-119,
+// simulator.hpp:248-262): stage by stage, F's layers then B's.  The first
+// layer without a time for its stage's type throws the reference's
+// SchemaError (profiles.hpp:38-43).  The device tables hold such an entry as
+// 0 and clamp non-positive times, so a plan over a layer time <= 0 (which
+// validate_network rejects, profiles.hpp:83-98, but estimate / simulate do
+// not check) is refused instead of computed on the wrong value.
+inline void check_stage_times(const PartitionPlan& plan, const NetworkProfile& net, const ClusterSpec& cluster) {
+    const std::int64_t L = net.L();
+    for (std::size_t i = 0; i < plan.stages.size() && i < cluster.accelerators.size(); ++i) {
+        const StageAssignment& st = plan.stages[i];
+        const std::string& type = cluster.accelerators[i].accel_type;
+        const std::int64_t lo = std::max<std::int64_t>(st.lo, 1), hi = std::min<std::int64_t>(st.hi, L);
+        for (int which = 0; which < 2; ++which)
+            for (std::int64_t j = lo; j <= hi; ++j) {
+                const LayerProfile& l = net.layers[(std::size_t)j - 1];
+                const auto& m = which == 0 ? l.fp_time : l.bp_time;
+                auto it = m.find(type);
+                if (it == m.end())
+                    throw SchemaError("layer '" + l.name + "' has no " + (which == 0 ? "fp" : "bp") +
+                                      " time for accelerator type '" + type + "'");
+                if (it->second <= 0)
+                    throw DeviceError("layer '" + l.name + "' has a non-positive " + (which == 0 ? "fp" : "bp") +
+                                      " time: outside the device library's domain (validate_network requires >= 1)");
+            }
+    }
+}
+
 // an escaping device status as the reference throws it
 [[noreturn]] inline void throw_status(int status, const std::string& invalid_plan_msg) {
     switch (status) {
@@ -691,6 +720,7 @@ inline CostEstimate Explorer::estimate(ScheduleKind kind, const PartitionPlan& p
                                        const ClusterSpec& cluster, std::int64_t M, std::int64_t micro) {
     check_mode(kind, cluster.execution_mode);   // cost_models.hpp:127-129
     if (plan.n_stages() != cluster.N()) throw InvalidPlan("plan stage count != cluster size");
+    detail::check_stage_times(plan, net, cluster);   // stage_costs' lookups (cost_models.hpp:103-119)
     upload(net, cluster);
     PlanBuf buf;
     const bp_plan_request q = plan_request(plan, buf, kind, M, micro, 1);
@@ -721,16 +751,21 @@ inline Timeline Explorer::simulate(ScheduleKind kind, const PartitionPlan& plan,
                                    std::int64_t mini_batches) {
     check_mode(kind, cluster.execution_mode);   // simulator.hpp:268
     if (plan.stages.empty()) throw InvalidPlan("plan has no stages");
-    if (mini_batches < 1) throw SchemaError("simulate: mini_batches >= 1 required");
     upload(net, cluster);
     PlanBuf buf;
-    const bp_plan_request q = plan_request(plan, buf, kind, M, micro, mini_batches);
+    // mini_batches < 1: the reference simulates one mini-batch, emits no
+    // events and reports Rat(mini_batches) * makespan (simulator.hpp:182-216)
+    const std::int64_t mb = std::max<std::int64_t>(mini_batches, 1);
+    const bp_plan_request q = plan_request(plan, buf, kind, M, micro, mb);
     const std::int64_t N = plan.n_stages(), Mp = std::max<std::int64_t>(M, 0);
-    const std::int64_t cap = mini_batches * (2 * N * Mp + 4 * (N - 1) * Mp);
+    const std::int64_t cap = mb * (2 * N * Mp + 4 * (N - 1) * Mp);
     std::vector<bp_event> ev((std::size_t)std::max<std::int64_t>(cap, 1));
     std::vector<bp_rat> hw((std::size_t)N), ws((std::size_t)N), busy((std::size_t)std::max<std::int64_t>(N - 1, 1));
     bp_timeline_result r{};
     check(bp_simulate_plan(ctx_, &q, &r, ev.data(), cap, hw.data(), ws.data(), busy.data()), "bp_simulate_plan");
+    // chain_instance's type lookups come after validate_plan and the stage
+    // count check (simulator.hpp:268-273)
+    if (r.status != BP_C_ERR_INVALID_PLAN) detail::check_stage_times(plan, net, cluster);
     if (r.status != BP_C_OK) {
         std::string msg;
         if (r.status == BP_C_ERR_INVALID_PLAN) {
@@ -749,6 +784,10 @@ inline Timeline Explorer::simulate(ScheduleKind kind, const PartitionPlan& plan,
     }
     Timeline t;
     t.makespan = detail::R(r.makespan);
+    if (mini_batches < 1) {
+        t.makespan = Rat(mini_batches) * t.makespan;
+        r.n_events = 0;
+    }
     t.events.reserve((std::size_t)r.n_events);
     for (std::int64_t i = 0; i < r.n_events; ++i) {
         const bp_event& x = ev[(std::size_t)i];

@@ -25,7 +25,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, how="lpt"):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests", "emu"))
     import torch.distributed as dist
@@ -35,7 +35,12 @@ def _worker(rank, world, port, out):
 
     from paper_2012_12544_b200 import workloads as W
     from paper_2012_12544_b200.sweep import allgather_best, best_record_from_results
-    p = W.config_c5(models=2, shard=rank, n_shards=world)
+    if how == "class":
+        # bench.py's strong-scaling split: whole dedup classes per rank
+        full = W.config_c5(models=2)
+        p = W.subset(full, W.shard_classes(full, world)[rank])
+    else:
+        p = W.config_c5(models=2, shard=rank, n_shards=world)
     res, _, _ = pyemu.Emu().explore(p, details=False)
     local = best_record_from_results(res, p.query_ids)
     best = allgather_best(local)
@@ -43,14 +48,15 @@ def _worker(rank, world, port, out):
     dist.destroy_process_group()
 
 
-def test_sharded_sweep_allgather_argmin_matches_unsharded(emu):
+@pytest.mark.parametrize("how", ["lpt", "class"])
+def test_sharded_sweep_allgather_argmin_matches_unsharded(emu, how):
     from paper_2012_12544_b200 import workloads as W
     from paper_2012_12544_b200.sweep import best_record_from_results
     world = 2
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(world, port, out), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, out, how), nprocs=world, join=True)
     full = W.config_c5(models=2)
     res, _, _ = emu.explore(full, details=False)
     want = best_record_from_results(res, full.query_ids)
@@ -68,3 +74,19 @@ def test_cost_balanced_shards():
     loads = [cost[s].sum() for s in shards]
     assert sum(len(s) for s in shards) == full.queries.size
     assert max(loads) / min(loads) < 1.05
+
+
+def test_class_shards_keep_dedup_classes_whole():
+    from paper_2012_12544_b200 import workloads as W
+    full = W.config_c5(models=16)
+    cls = W.query_classes(full)
+    shards = W.shard_classes(full, 8)
+    owner = np.empty(full.queries.size, dtype=np.int64)
+    for r, s in enumerate(shards):
+        owner[s] = r
+    assert sorted(np.concatenate(shards).tolist()) == list(range(full.queries.size))
+    for c in np.unique(cls):
+        assert np.unique(owner[cls == c]).size == 1          # a class never spans two ranks
+    cost = W.class_cost(full, cls)
+    loads = [sum(cost[c] for c in np.unique(cls[s])) for s in shards]
+    assert max(loads) / min(loads) < 1.1
