@@ -110,6 +110,7 @@ struct bp_ctx {
     HostPinned stage_tables;   // pinned staging of the network / cluster tables
     Pools P{};
     int max_T = 1;
+    size_t smem_optin = 227 * 1024;   // cudaDeviceProp::sharedMemPerBlockOptin
     bool prof = false;
     bool dedup = true;       // BP_OPT_DEDUP
     bool plan_only = false;  // BP_OPT_PLAN_ONLY
@@ -444,7 +445,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     // DP launch geometry: blocks resident per SM bounded by shared memory
     int max_units = std::max(1, c->hn.max_L);
     size_t smem = partition_smem_bytes(max_units, std::max(1, hb.max_N), c->max_T);
-    if (smem > 227 * 1024)
+    if (smem > c->smem_optin)
         return fail(c, BP_BAD_INPUT, "network too large for the shared-memory DP (L=" + std::to_string(max_units) + ")");
     int per_sm = (int)std::max<size_t>(1, (size_t)(200 * 1024) / (smem + 1024));
     if (per_sm > 8) per_sm = 8;
@@ -614,10 +615,18 @@ bp_ctx* bp_create(int device) {
                 std::to_string(prop.minor);
         return nullptr;
     }
+    // the kernels with large dynamic shared memory may use up to the opt-in
+    // limit on this device (a per-device function attribute, set once here:
+    // lowering it per batch would race with other contexts' launches)
+    if (const cudaError_t ke = kernel_attributes_init((int)prop.sharedMemPerBlockOptin); ke != cudaSuccess) {
+        g_err = std::string("cannot set kernel attributes: ") + cudaGetErrorString(ke);
+        return nullptr;
+    }
     bp_ctx* c = new (std::nothrow) bp_ctx();
     if (!c) return nullptr;
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    c->smem_optin = (size_t)prop.sharedMemPerBlockOptin;
     return c;
 }
 

@@ -357,8 +357,15 @@ __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which,
 void launch_partition(const BatchDev& B, int which, int grid, int max_units, int max_N, int T_slots,
                       cudaStream_t st) {
     size_t bytes = partition_smem_bytes(max_units, max_N, T_slots);
-    cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     k_partition<<<grid, DP_THREADS, bytes, st>>>(B, which, max_units, max_N, T_slots);
+}
+
+cudaError_t partition_attributes_init(int optin_bytes) {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, k_partition);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_partition, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin_bytes - (int)a.sharedSizeBytes);
 }
 
 // Layout of k_partition's dynamic shared memory (must match DPSmem above).

@@ -927,17 +927,13 @@ void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes,
     }
 }
 
-// per-device launch attributes (dynamic shared memory above 48 KB is a
-// per-device function attribute); called once per context
+// launch geometry of the slim refine kernel for a batch (0: not used, its
+// tables do not fit in shared memory); the dynamic shared memory attribute is
+// set once per device (kernel_attributes_init)
 int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes) {
-    const size_t bytes = refine_region_bytes(max_N);
-    if (bytes <= 200 * 1024)
-        cudaFuncSetAttribute(k_refine_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     const size_t fb = refine_fast_bytes(max_N, max_L, max_T);
     *fast_bytes = 0;
     if (fb > 96 * 1024) return 0;
-    if (cudaFuncSetAttribute(k_refine_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb) != cudaSuccess)
-        return 0;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -945,6 +941,25 @@ int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes) {
     if (per_sm <= 0) return 0;
     *fast_bytes = fb;
     return sms * per_sm;
+}
+
+// The kernels with more than 48 KB of dynamic shared memory, allowed up to
+// the device's opt-in limit once per device (bp_create); each launch then
+// passes its own size.
+template <class K>
+cudaError_t allow_dynamic_smem(K* kernel, int optin_bytes) {
+    cudaFuncAttributes a;
+    cudaError_t e = cudaFuncGetAttributes(&a, kernel);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                optin_bytes - (int)a.sharedSizeBytes);
+}
+
+cudaError_t kernel_attributes_init(int optin_bytes) {
+    cudaError_t e = allow_dynamic_smem(k_refine_smem, optin_bytes);
+    if (e == cudaSuccess) e = allow_dynamic_smem(k_refine_fast, optin_bytes);
+    if (e == cudaSuccess) e = partition_attributes_init(optin_bytes);
+    return e;
 }
 void launch_prune_reset(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.pkey, 0, ((size_t)B.pmask + 1) * sizeof(unsigned long long), st);

@@ -23,6 +23,8 @@ void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
 void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes, int max_L, int max_T,
                    cudaStream_t st);
 int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes);
+cudaError_t kernel_attributes_init(int optin_bytes);
+cudaError_t partition_attributes_init(int optin_bytes);
 size_t refine_region_bytes(int max_N);
 // part: bit 0 = keys + work list, bit 1 = representatives, bit 2 = members (copy
 // the shared estimate, or list), bit 3 = the listed members

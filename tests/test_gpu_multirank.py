@@ -84,3 +84,34 @@ def test_two_ranks_class_shards_match_unsharded():
         ids = np.array(out[r][1])
         got[ids] = np.frombuffer(out[r][2], dtype=RESULT_DTYPE)
     assert got.tobytes() == res.tobytes()
+
+
+def test_two_contexts_concurrent_batches():
+    """Two contexts on one device, each with a batch of a different stage
+    count range (different dynamic shared memory sizes), run concurrently on
+    two streams: each equals the same queries run alone (the kernels' shared
+    memory attributes are per device and set once, bp_create)."""
+    import torch
+
+    from paper_2012_12544_b200 import workloads as W
+    from paper_2012_12544_b200.runtime import Explorer
+    full = W.config_c5(models=16)
+    n = full.queries["n_stages"]
+    subs = [W.subset(full, np.nonzero(n >= 32)[0]), W.subset(full, np.nonzero(n < 32)[0])]
+    alone = []
+    for s in subs:
+        ex = Explorer(0)
+        alone.append(ex.explore(s, details=True))
+        ex.close()
+    exs = [Explorer(0), Explorer(0)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    bs = [e.prepare(s, details=True, stream=st.cuda_stream) for e, s, st in zip(exs, subs, streams)]
+    for e, b, st in zip(exs, bs, streams):
+        e.run(b, stream=st.cuda_stream)
+    torch.cuda.synchronize()
+    for e, b, s, st, want in zip(exs, bs, subs, streams, alone):
+        got = e.fetch(b, s, details=True, stream=st.cuda_stream)
+        for g, w in zip(got, want):
+            assert g.tobytes() == w.tobytes()
+        e.free(b)
+        e.close()
