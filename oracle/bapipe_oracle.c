@@ -11,7 +11,7 @@
  * E_UB at the exact read the reference performs.
  *
  * Pinning: tests/test_oracle.py checks this file against (a) the reference's
- * own golden vectors (tests/golden/reference_unit_vectors.json, restated from
+ * own golden vectors (restated inline in tests/test_oracle.py from
  * proj/tests/test_*.cpp) and (b) the compiled reference (oracle/_ref) on thousands
  * of seeded random queries and the BASELINE configs.
  */
