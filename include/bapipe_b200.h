@@ -124,7 +124,10 @@ enum {
     BP_C_ERR_OVERFLOW = 7,         /* overflow_error escapes explore() */
     BP_C_ERR_INVALID_PLAN = 8,     /* InvalidPlan escapes; detail = BP_IP_* code, detail2 = stage/layer */
     BP_C_ERR_DOMAIN = 9,           /* domain_error escapes */
-    BP_C_REF_UB = 10               /* reference undefined behaviour (out-of-bounds layer read) */
+    BP_C_REF_UB = 10,              /* reference undefined behaviour (out-of-bounds layer read) */
+    BP_C_PRUNED_LB = 11            /* BP_OPT_PRUNE_LB only: feasible and ranked, but not simulated --
+                                      its makespan lower bound exceeds its query's best
+                                      (SPEC.md:320); makespan {0, 0}, rank -1 */
 };
 
 /* InvalidPlan message codes (plan.hpp:42-83). */
@@ -252,12 +255,21 @@ int bp_set_profiling(bp_ctx* ctx, int enable);
  *   comm-coarsened DP per (that, a_th), simulations per identical inputs --
  *   and share the results; 0 evaluates every query and candidate
  *   independently. */
-enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2 };
+enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2, BP_OPT_PRUNE_LB = 3 };
 /*   BP_OPT_PLAN_ONLY (default 0): each candidate stops after balance_partition,
  *   its estimate and the memory check -- the reference's `bapipe plan`
  *   (tools/bapipe.cpp:152-170), which calls balance_partition for one
  *   (kind, M) with no min-micro filter and no simulation.  Feasible candidates
  *   get BP_C_OK with makespan 0/1; want_details gives their plans. */
+/*   BP_OPT_PRUNE_LB (default 0): estimate-based pruning, the reference's
+ *   SPEC.md:320 promise (its explore() simulates every candidate).  A
+ *   candidate whose simulation provably cannot raise (the scaled-integer
+ *   simulator class) is simulated only if its makespan lower bound
+ *   max_b [sum_{s<b} (F_s + B_s + 2 SR_s [sync]) + M (F_b + B_b)] does not
+ *   exceed its query's best simulated makespan; the others get
+ *   BP_C_PRUNED_LB.  Every bp_query_result is byte-identical to the
+ *   unpruned run (status, n_ranked, best, first_error and the best's
+ *   values); only per-candidate records of pruned candidates differ. */
 int bp_set_option(bp_ctx* ctx, int option, int64_t value);
 
 /* ---- one plan: full-timeline simulate and estimate ----------------------

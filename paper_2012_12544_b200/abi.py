@@ -123,6 +123,8 @@ PRODUCT_SYMBOLS = (
 )
 BP_OPT_DEDUP = 1
 BP_OPT_PLAN_ONLY = 2
+BP_OPT_PRUNE_LB = 3
+BP_C_PRUNED_LB = 11
 
 
 def _sig(lib, name, res, args):

@@ -114,6 +114,7 @@ struct bp_ctx {
     bool prof = false;
     bool dedup = true;       // BP_OPT_DEDUP
     bool plan_only = false;  // BP_OPT_PLAN_ONLY
+    bool prune_lb = false;   // BP_OPT_PRUNE_LB
     std::map<std::string, KStat> stats;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -351,6 +352,7 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
     size_t o_rlist = L.take<int32_t>(2 * nqs), o_rcount = L.take<int32_t>(4);
     size_t o_plist = L.take<int32_t>(nc), o_pctr = L.take<int32_t>(2);
+    size_t o_qseed = L.take<unsigned long long>(nqs), o_qinc = L.take<bp_rat>(nqs);
     size_t o_pkey = L.take<unsigned long long>((size_t)stab), o_pbest = L.take<unsigned long long>((size_t)stab);
     int32_t ctab = 1;
     while (ctab < 2 * std::max<int64_t>(1, (int64_t)nms)) ctab <<= 1;
@@ -424,6 +426,8 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     D.rlist = dptr<int32_t>(b, o_rlist);
     D.rcount = dptr<int32_t>(b, o_rcount);
     D.plist = dptr<int32_t>(b, o_plist);
+    D.qseed = dptr<unsigned long long>(b, o_qseed);
+    D.qinc = dptr<bp_rat>(b, o_qinc);
     D.pctr = dptr<int32_t>(b, o_pctr);
     D.pkey = dptr<unsigned long long>(b, o_pkey);
     D.pbest = dptr<unsigned long long>(b, o_pbest);
@@ -467,6 +471,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     const HostBatch& hb = B->hb;
     D.dedup = c->dedup ? 1 : 0;
     D.plan_only = c->plan_only ? 1 : 0;
+    D.prune_lb = c->prune_lb && !c->plan_only ? 1 : 0;
     cudaError_t e;
     e = cudaMemsetAsync(D.cand, 0, (size_t)hb.ncand * sizeof(bp_candidate), st);
     if (e == cudaSuccess && D.stages) e = cudaMemsetAsync(D.stages, 0, (size_t)hb.nstage * sizeof(bp_stage), st);
@@ -528,6 +533,12 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     phase_end(c, "phase_prune", st, ph);
     ph = phase_begin(c, st);
     timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
+    if (D.prune_lb) {   // BP_OPT_PRUNE_LB round 1: bounds, one seed per query
+        timed(c, "lb_prune", st, [&] {
+            launch_lb_bound(D, st);
+            launch_lb_round1(D, st);
+        }, 2);
+    }
     static const char* fast_names[8] = {"sim_fast_g2", "sim_fast_g4", "sim_fast_g8", "sim_fast_g16",
                                         "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4", "sim_fast_g32s8"};
     // the simulator classes are independent: the two exact ones on the side
@@ -542,6 +553,11 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "sim_flow32", st, [&] { launch_sim_flow(D, 0, c->sm_count, st); });
     cudaStreamWaitEvent(st, c->join, 0);
     timed(c, "sim_share", st, [&] { launch_sim_share(D, st); });
+    if (D.prune_lb) {   // round 2: the candidates whose bound does not exceed their query's best
+        timed(c, "lb_prune", st, [&] { launch_lb_round2(D, st); }, 2);
+        for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
+        timed(c, "lb_prune", st, [&] { launch_lb_finish(D, st); });
+    }
     phase_end(c, "phase_sims", st, ph);
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();
@@ -809,6 +825,7 @@ int bp_set_option(bp_ctx* c, int option, int64_t value) {
     switch (option) {
         case BP_OPT_DEDUP: c->dedup = value != 0; return BP_OK;
         case BP_OPT_PLAN_ONLY: c->plan_only = value != 0; return BP_OK;
+        case BP_OPT_PRUNE_LB: c->prune_lb = value != 0; return BP_OK;
         default: return fail(c, BP_BAD_INPUT, "unknown option " + std::to_string(option));
     }
 }

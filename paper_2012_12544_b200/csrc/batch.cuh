@@ -86,7 +86,15 @@ struct CState {
     int32_t ft_trials;     // prune: memory_fine_tune trial moves (instrumentation)
     int32_t mem0_from;     // prune member: representative whose first-estimate memory it starts from, -1 = none
     int32_t mem0_buf;      // 0: that memory is in sMem (estimate was feasible), 1: in sMem0
+    int64_t lb;            // BP_OPT_PRUNE_LB: makespan lower bound * D (scaled-integer class), -1 = none
+    int32_t lbstate;       // LB_* below
+    int32_t pad;
 };
+
+// BP_OPT_PRUNE_LB states of a simulation representative: simulated normally,
+// deferred (not simulated yet), simulated in round 1 (its query's seed) or
+// round 2 (its bound did not exceed a best)
+enum { LB_NONE = 0, LB_DEFERRED = 1, LB_ROUND1 = 2, LB_ROUND2 = 3 };
 
 // DP work item: a (query, a_th) pair; a_th < 0 = whole-layer partition.
 struct DPItem {
@@ -152,6 +160,9 @@ struct BatchDev {
     int32_t cmask;
     int32_t dedup;            // BP_OPT_DEDUP: share identical subproblems
     int32_t plan_only;        // BP_OPT_PLAN_ONLY: stop after balance_partition + estimate
+    int32_t prune_lb;         // BP_OPT_PRUNE_LB: simulate dominated scaled-integer candidates only if needed
+    unsigned long long* qseed;// [nq] BP_OPT_PRUNE_LB: packed (lower bound, local index) minimum per query
+    bp_rat* qinc;             // [nq] BP_OPT_PRUNE_LB: best simulated makespan per query ({0,0}: none)
     int32_t* rlist;           // [nq] queries to refine this run (compacted)
     int32_t* rcount;          // [2] list length, next entry
     int32_t* plist;           // [ncand] candidates to prune this run (compacted)

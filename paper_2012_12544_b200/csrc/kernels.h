@@ -31,6 +31,10 @@ size_t refine_region_bytes(int max_N);
 void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part = 15);
 void launch_prune_reset(const BatchDev& B, cudaStream_t st);
 void launch_sim_prep(const BatchDev& B, cudaStream_t st);
+void launch_lb_bound(const BatchDev& B, cudaStream_t st);
+void launch_lb_round1(const BatchDev& B, cudaStream_t st);
+void launch_lb_round2(const BatchDev& B, cudaStream_t st);
+void launch_lb_finish(const BatchDev& B, cudaStream_t st);
 void launch_sim_share(const BatchDev& B, cudaStream_t st);
 void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st);
 void launch_sim_exact(const BatchDev& B, int sms, cudaStream_t st);

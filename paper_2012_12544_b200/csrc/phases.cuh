@@ -629,8 +629,14 @@ BPK_HDNI void rank_query(const BatchDev& B, int qi) {
     const int nc = 2 * Q.nbase;
     bp_candidate* cand = B.cand + Q.cand_off;
     int nr = 0;
+    int npruned = 0;
     for (int i = 0; i < nc; ++i) {
         int st = cand[i].status;
+        if (st == BP_C_PRUNED_LB) {   // BP_OPT_PRUNE_LB: ranked, never first (its bound exceeds the best)
+            cand[i].rank = -1;
+            ++npruned;
+            continue;
+        }
         if (st != BP_C_OK) {
             // a candidate that failed after its estimate (simulate) carries
             // no values, like the reference's rejected/aborted candidates
@@ -660,7 +666,7 @@ BPK_HDNI void rank_query(const BatchDev& B, int qi) {
     for (int i = 0; i < nr; ++i) cand[order[i]].rank = i;
     const bp_candidate& b = cand[order[0]];
     r.status = BP_Q_OK;
-    r.n_ranked = nr;
+    r.n_ranked = nr + npruned;
     r.best = order[0];
     r.best_kind = b.kind;
     r.best_M = b.M;

@@ -114,6 +114,7 @@ __global__ void k_sim_share(BatchDev B) {
     if (ci >= B.ncand) return;
     const int32_t r = B.cs[ci].sim_rep;
     if (r < 0) return;
+    if (B.prune_lb && B.cs[r].lbstate == LB_DEFERRED) return;   // not simulated (yet)
     bp_candidate& cd = B.cand[ci];
     cd.status = B.cand[r].status;
     cd.makespan = B.cand[r].makespan;
@@ -136,6 +137,9 @@ __global__ void k_sim_prep(BatchDev B) {
                 cls = -1;
             }
         }
+        // BP_OPT_PRUNE_LB: scaled-integer representatives wait for their
+        // query's best (k_lb_round1 / k_lb_decide list them)
+        if (cls >= 0 && cls < SIM_EXACT && B.prune_lb) cls = -1;
         if (cls >= 0) {
             int pos = atomicAdd(&B.sim_count[cls], 1);
             B.sim_list[(int64_t)cls * B.ncand + pos] = (int32_t)ci;
@@ -467,6 +471,147 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
     }  // persistent loop
 }
 
+// ---- BP_OPT_PRUNE_LB: estimate-based pruning (the reference's
+// explore() simulates every candidate, explorer.hpp:96-132).
+//
+// Only the scaled-integer class is ever skipped: its simulation provably
+// cannot raise (k_sim_prep's bound), so skipping it cannot change a query's
+// outcome, and a skipped candidate is feasible, hence ranked, either way.  It
+// is skipped when its makespan lower bound exceeds its query's best
+// simulated makespan, so it cannot be ranked first: the query's best record
+// is unchanged.  Every stage runs its M F and M B ops one after another, and
+// before the first of them micro-batch 1 must cross the stages before it,
+// after the last of them micro-batch M must cross them back (sync transfers
+// on both paths, simulator.hpp:134-171):
+//   makespan >= max_b [ sum_{s<b} (F_s + B_s + 2 SR_s [sync]) + M (F_b + B_b) ].
+// Scaled by the candidate's D this is an integer below the class's 2^61
+// bound.
+__device__ int64_t sim_lower_bound_scaled(const BatchDev& B, int64_t ci) {
+    const bp_candidate& cd = B.cand[ci];
+    const CState& cs = B.cs[ci];
+    const int qi = B.cq[ci];
+    const QDesc Q = B.q[qi];
+    const int N = Q.N;
+    const int64_t M = cd.M, micro = cd.micro, D = cs.D;
+    const bool sync = !kind_async(cd.kind);
+    const NetView v = net_view(B.P, Q.net);
+    const ChainView c = chain_view(B.P, Q.cl, N);
+    const int64_t slot = Q.stage_off + (ci - Q.cand_off) * N, qo = Q.qstage_off;
+    const bool refined = cs.plan_kind == PLAN_REFINED;
+    const int32_t* hi = refined ? B.qhi + qo : B.chi + slot;
+    const int32_t* lo = refined ? B.qlo + qo : B.clo + slot;
+    int64_t prefix = 0, best = 0;
+    for (int s = 0; s < N; ++s) {
+        int64_t F, Bt;
+        if (refined) {
+            const Rat f = B.qF[qo + s], b = B.qB[qo + s];
+            F = f.n * (D / f.d);
+            Bt = b.n * (D / b.d);
+        } else {
+            const int32_t t = c.type[s];
+            F = stage_sum_whole(lo[s], hi[s], v.Pfp + (int64_t)t * (v.L + 1));
+            Bt = stage_sum_whole(lo[s], hi[s], v.Pbp + (int64_t)t * (v.L + 1));
+        }
+        const int64_t here = prefix + M * (F + Bt);
+        best = here > best ? here : best;
+        int64_t sr = 0;
+        if (sync && s + 1 < N) {
+            const int64_t a = v.a[hi[s] - 1] * micro;
+            sr = (a == 0 ? 0 : ceil_div64(a, c.bw[s])) * D;
+        }
+        prefix += F + Bt + 2 * sr;
+    }
+    return best;
+}
+
+__device__ __forceinline__ bool lb_class(int cls) { return cls >= 0 && cls < SIM_EXACT; }
+
+// bound of every scaled-integer candidate; per query, the smallest bound's
+// candidate (the seed, simulated first)
+__global__ void k_lb_bound(BatchDev B) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= B.ncand) return;
+    CState& cs = B.cs[ci];
+    cs.lb = -1;
+    cs.lbstate = LB_NONE;
+    if (!lb_class(cs.sim_cls)) return;
+    const int64_t lb = sim_lower_bound_scaled(B, ci);
+    cs.lb = lb;
+    cs.lbstate = LB_DEFERRED;
+    const int qi = B.cq[ci];
+    const float key = (float)lb / (float)cs.D;
+    atomicMin(&B.qseed[qi], ((unsigned long long)__float_as_uint(key) << 32) |
+                                (unsigned long long)(uint32_t)(ci - B.q[qi].cand_off));
+}
+
+__device__ void lb_list(const BatchDev& B, int64_t r) {
+    const int cls = B.cs[r].sim_cls;
+    const int pos = atomicAdd(&B.sim_count[cls], 1);
+    B.sim_list[(int64_t)cls * B.ncand + pos] = (int32_t)r;
+    const bp_candidate& c = B.cand[r];
+    const uint64_t N = (uint64_t)c.n_stages, M = (uint64_t)c.M;
+    atomicAdd(&B.work[WORK_SIM_EVENTS + cls], (unsigned long long)(2 * N * M + (c.kind >= 2 ? 2 * (N - 1) * M : 0)));
+}
+
+// round 1: each query's seed (its simulation representative) is simulated
+// with the exact classes
+__global__ void k_lb_round1(BatchDev B) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= B.ncand || !lb_class(B.cs[ci].sim_cls)) return;
+    const int qi = B.cq[ci];
+    if ((uint32_t)(B.qseed[qi] & 0xffffffffull) != (uint32_t)(ci - B.q[qi].cand_off)) return;
+    const int64_t r = B.cs[ci].sim_rep >= 0 ? B.cs[ci].sim_rep : ci;
+    if (atomicCAS(&B.cs[r].lbstate, LB_DEFERRED, LB_ROUND1) == LB_DEFERRED) lb_list(B, r);
+}
+
+// each query's best simulated makespan so far (thread per query)
+__global__ void k_lb_incumbent(BatchDev B) {
+    const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    const QDesc Q = B.q[qi];
+    bp_rat inc{0, 0};
+    for (int i = 0; i < 2 * Q.nbase; ++i) {
+        const bp_candidate& c = B.cand[Q.cand_off + i];
+        if (c.status != BP_C_OK) continue;
+        const Rat m{c.makespan.num, c.makespan.den};
+        if (inc.den == 0 || rat_lt(m, Rat{inc.num, inc.den})) inc = c.makespan;
+    }
+    B.qinc[qi] = inc;
+}
+
+// round 2: the deferred representatives some member of which has a bound
+// not above its query's best
+__global__ void k_lb_decide(BatchDev B) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= B.ncand) return;
+    const CState cs = B.cs[ci];
+    if (!lb_class(cs.sim_cls)) return;
+    const int64_t r = cs.sim_rep >= 0 ? cs.sim_rep : ci;
+    if (B.cs[r].lbstate != LB_DEFERRED) return;
+    const bp_rat inc = B.qinc[B.cq[ci]];
+    // lb / D <= inc.num / inc.den, exactly
+    const bool need = inc.den == 0 || (i128)cs.lb * inc.den <= (i128)inc.num * cs.D;
+    if (need && atomicCAS(&B.cs[r].lbstate, LB_DEFERRED, LB_ROUND2) == LB_DEFERRED) lb_list(B, r);
+}
+
+// the skipped candidates' records; members of round-2 representatives copy
+// their outcome
+__global__ void k_lb_finish(BatchDev B) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= B.ncand) return;
+    const CState cs = B.cs[ci];
+    if (!lb_class(cs.sim_cls)) return;
+    const int64_t r = cs.sim_rep >= 0 ? cs.sim_rep : ci;
+    bp_candidate& cd = B.cand[ci];
+    if (B.cs[r].lbstate == LB_DEFERRED) {
+        cd.status = BP_C_PRUNED_LB;
+        cd.makespan = bp_rat{0, 0};
+    } else if (cs.sim_rep >= 0 && cd.status == C_PENDING) {
+        cd.status = B.cand[r].status;
+        cd.makespan = B.cand[r].makespan;
+    }
+}
+
 static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
@@ -481,6 +626,27 @@ void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
 
 void launch_sim_share(const BatchDev& B, cudaStream_t st) {
     if (B.ncand) k_sim_share<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+}
+
+void launch_lb_bound(const BatchDev& B, cudaStream_t st) {
+    if (!B.ncand) return;
+    cudaMemsetAsync(B.qseed, 0xff, (size_t)B.nq * sizeof(unsigned long long), st);
+    k_lb_bound<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+}
+void launch_lb_round1(const BatchDev& B, cudaStream_t st) {
+    if (B.ncand) k_lb_round1<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+}
+// after round 1 (and its k_sim_share): the round-2 lists of the scaled-integer
+// classes, replacing their round-1 lists
+void launch_lb_round2(const BatchDev& B, cudaStream_t st) {
+    if (!B.ncand) return;
+    cudaMemsetAsync(B.sim_count, 0, SIM_EXACT * sizeof(int32_t), st);
+    cudaMemsetAsync(B.sim_count + SIM_CLASSES, 0, SIM_EXACT * sizeof(int32_t), st);
+    k_lb_incumbent<<<blocks_for(B.nq, 128), 128, 0, st>>>(B);
+    k_lb_decide<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+}
+void launch_lb_finish(const BatchDev& B, cudaStream_t st) {
+    if (B.ncand) k_lb_finish<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
 }
 
 void launch_sim_fast(const BatchDev& B, int cls, int sms, cudaStream_t st) {

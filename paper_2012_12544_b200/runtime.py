@@ -104,6 +104,14 @@ class Explorer:
         if rc != 0:
             raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
 
+    def prune_lb(self, on=True):
+        """BP_OPT_PRUNE_LB: skip simulating scaled-integer candidates whose
+        makespan lower bound exceeds their query's best (per-query results
+        identical; skipped candidates get BP_C_PRUNED_LB)."""
+        rc = self.lib.bp_set_option(self.ctx, abi.BP_OPT_PRUNE_LB, 1 if on else 0)
+        if rc != 0:
+            raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
+
     def plan_call(self, req, which, cap=0):
         """bp_simulate_plan (which='simulate') or bp_estimate_plan on a
         bp_plan_request for this context's loaded problem.  Returns the raw

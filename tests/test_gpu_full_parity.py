@@ -105,3 +105,30 @@ def test_c5_five_copies_in_one_batch(ex, c5):
                               one_cand.view(np.uint8).reshape(c.size, -1)).any(axis=1))[0]
             raise AssertionError(f"copy {k}: {bad.size} candidate records differ from the 1x batch, "
                                  f"first {bad[:5].tolist()}")
+
+
+def test_c5_lower_bound_pruning_keeps_every_query_result(ex, c5, gold):
+    """BP_OPT_PRUNE_LB: the full sweep's per-query records are
+    the reference's; every skipped candidate is feasible in the unpruned run
+    with a makespan above its query's best."""
+    from fractions import Fraction as Fr
+
+    from paper_2012_12544_b200.abi import BP_C_PRUNED_LB
+    ex.prune_lb(True)
+    try:
+        res, cand, _ = ex.explore(c5, details="candidates")
+    finally:
+        ex.prune_lb(False)
+    assert res.tobytes() == gold["res"].tobytes()
+    pruned = np.nonzero(cand["status"] == BP_C_PRUNED_LB)[0]
+    assert pruned.size > 0
+    _, full, _ = ex.explore(c5, details="candidates")
+    keep = cand["status"] != BP_C_PRUNED_LB
+    assert cand[keep]["status"].tobytes() == full[keep]["status"].tobytes()
+    assert cand[keep]["makespan"].tobytes() == full[keep]["makespan"].tobytes()
+    assert np.all(full["status"][pruned] == 0)
+    qi = np.searchsorted(c5.queries["cand_offset"], pruned, side="right") - 1
+    for i, q in zip(pruned[:: max(1, pruned.size // 4000)], qi[:: max(1, pruned.size // 4000)]):
+        b = res[q]["best_makespan"]
+        m = full[i]["makespan"]
+        assert Fr(int(m["num"]), int(m["den"])) > Fr(int(b["num"]), int(b["den"]))
