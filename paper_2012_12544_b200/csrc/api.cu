@@ -297,11 +297,19 @@ int upload_clusters(bp_ctx* c) {
 int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cudaStream_t st) {
     if (!c->have_nets || !c->have_cls) return fail(c, BP_BAD_INPUT, "networks/clusters not set");
     std::string err;
+    static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
+    const auto t0 = std::chrono::steady_clock::now();
     if (!build_batch(q, nq, c->hn, c->hc, B->hb, err)) return fail(c, BP_BAD_INPUT, err);
+    const auto t1 = std::chrono::steady_clock::now();
     const HostBatch& hb = B->hb;
     for (int i = 0; i < nq; ++i)
         if (q[i].cand_offset != hb.q[i].cand_off || q[i].stage_offset != hb.q[i].stage_off)
             return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
+    const auto t2 = std::chrono::steady_clock::now();
+    if (timing)
+        fprintf(stderr, "prepare: build_batch %.2f ms, offset check %.2f ms\n",
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(t2 - t1).count());
     // candidate and stage-slot indices are int32 in the kernels' work lists
     if (hb.ncand >= INT32_MAX || hb.nstage >= ((int64_t)1 << 40))
         return fail(c, BP_BAD_INPUT, "batch too large (" + std::to_string(hb.ncand) +
@@ -358,7 +366,13 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
     while (ctab < 2 * std::max<int64_t>(1, (int64_t)nms)) ctab <<= 1;
     size_t o_ckey = L.take<unsigned long long>((size_t)ctab), o_crep = L.take<int32_t>((size_t)ctab);
     size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(2 * SIM_CLASSES);   // counts, then hand-out counters
+    const auto t3 = std::chrono::steady_clock::now();
     if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
+    if (timing)
+        fprintf(stderr, "prepare: layout %.2f ms, device arena %.2f ms (%zu MB)\n",
+                std::chrono::duration<double, std::milli>(t3 - t2).count(),
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t3).count(),
+                L.off >> 20);
     void* b = B->mem.p;
     // stage the inputs in pinned memory and copy once
     if (!B->stage_in.ensure(in_end)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc");

@@ -35,6 +35,7 @@ struct HostNets {
 struct HostCls {
     std::vector<ClDesc> desc;
     std::vector<int32_t> ctype;
+    std::vector<int32_t> pmax;   // host only: prefix maximum of ctype per cluster (build_batch's type check)
     std::vector<int64_t> cap, minm, bw;
     int max_N = 0;
 };
@@ -212,6 +213,7 @@ inline bool build_clusters(const bp_cluster* cls, int n, HostCls& H, std::string
         d.first_bad_link = c.n_accels - 1;
         for (int k = 0; k < c.n_accels; ++k) {
             H.ctype.push_back(c.type_id[k]);
+            H.pmax.push_back(k == 0 ? c.type_id[k] : std::max(H.pmax.back(), c.type_id[k]));
             H.cap.push_back(c.mem_capacity[k]);
             bool bad = c.mem_capacity[k] <= 0 || c.type_id[k] < 0;
             for (int q = 0; q < 4; ++q) {
@@ -249,6 +251,15 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
     HB.ncand = HB.nstage = HB.nqstage = HB.nmslot = 0;
     HB.max_units = HB.max_N = HB.max_nbase = 0;
     std::unordered_map<int64_t, std::pair<int64_t, int>> divisors;   // mini -> (offset, count)
+    // per network, the smallest type id without a profile: a chain prefix
+    // whose largest type id is below it passes validate_pair's type check
+    // at once (otherwise the per-accelerator loop decides)
+    std::vector<int32_t> first_bad_type(HN.desc.size());
+    for (size_t n = 0; n < HN.desc.size(); ++n) {
+        int32_t t = 0;
+        while (t < HN.desc[n].T && HN.type_ok[HN.desc[n].off_tflag + t]) ++t;
+        first_bad_type[n] = t;
+    }
     for (int i = 0; i < nq; ++i) {
         const bp_query& b = qs[i];
         if (b.network < 0 || b.network >= (int)HN.desc.size() || b.cluster < 0 || b.cluster >= (int)HC.desc.size()) {
@@ -269,7 +280,8 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
         Q.N = N;
         Q.mini = b.mini_batch;
         bool ok = nd.valid && N <= cd.first_bad_acc && N - 1 <= cd.first_bad_link && b.mini_batch >= 1;
-        for (int k = 0; k < N && ok; ++k) {
+        const bool types_ok = N < 1 || HC.pmax[cd.off_acc + N - 1] < first_bad_type[b.network];
+        for (int k = 0; k < N && ok && !types_ok; ++k) {
             int32_t t = HC.ctype[cd.off_acc + k];
             if (t >= nd.T || !HN.type_ok[nd.off_tflag + t]) ok = false;
         }
