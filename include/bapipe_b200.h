@@ -255,7 +255,7 @@ int bp_set_profiling(bp_ctx* ctx, int enable);
  *   comm-coarsened DP per (that, a_th), simulations per identical inputs --
  *   and share the results; 0 evaluates every query and candidate
  *   independently. */
-enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2, BP_OPT_PRUNE_LB = 3 };
+enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2, BP_OPT_PRUNE_LB = 3, BP_OPT_SPLIT = 4 };
 /*   BP_OPT_PLAN_ONLY (default 0): each candidate stops after balance_partition,
  *   its estimate and the memory check -- the reference's `bapipe plan`
  *   (tools/bapipe.cpp:152-170), which calls balance_partition for one
@@ -270,6 +270,10 @@ enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2, BP_OPT_PRUNE_LB = 3 };
  *   BP_C_PRUNED_LB.  Every bp_query_result is byte-identical to the
  *   unpruned run (status, n_ranked, best, first_error and the best's
  *   values); only per-candidate records of pruned candidates differ. */
+/*   BP_OPT_SPLIT (default 1): a batch of at least 4096 queries runs as two
+ *   concurrent parts -- the queries with the batch's largest stage count
+ *   (the longest refine walks) and the rest -- on two streams.  Results are
+ *   identical either way. */
 int bp_set_option(bp_ctx* ctx, int option, int64_t value);
 
 /* ---- one plan: full-timeline simulate and estimate ----------------------

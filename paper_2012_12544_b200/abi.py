@@ -124,6 +124,7 @@ PRODUCT_SYMBOLS = (
 BP_OPT_DEDUP = 1
 BP_OPT_PLAN_ONLY = 2
 BP_OPT_PRUNE_LB = 3
+BP_OPT_SPLIT = 4
 BP_C_PRUNED_LB = 11
 
 

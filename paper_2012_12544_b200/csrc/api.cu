@@ -94,6 +94,16 @@ struct bp_batch {
     int refine_grid = 0;       // slim refine kernel: persistent grid, 0 = not used
     size_t refine_bytes = 0;   // its dynamic shared memory
     uint64_t gen = 0;          // bp_ctx::gen at prepare: the device tables it points at
+    // this batch's own side stream and fork / join events (concurrent batches
+    // of one context must not share them)
+    cudaStream_t side = nullptr, lane = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr, done = nullptr;
+    // BP_OPT_SPLIT: the batch runs as two parts on two streams (see split_prepare)
+    std::vector<bp_batch*> parts;
+    std::vector<std::vector<int32_t>> part_q;      // parent query index of each part query
+    DevBuf part_ids;                               // device: parent query index per part query (parts concatenated)
+    DevBuf part_best;                              // device: one bp_best_record per part
+    std::vector<int64_t> part_ids_host;
 };
 
 struct bp_ctx {
@@ -115,14 +125,12 @@ struct bp_ctx {
     bool dedup = true;       // BP_OPT_DEDUP
     bool plan_only = false;  // BP_OPT_PLAN_ONLY
     bool prune_lb = false;   // BP_OPT_PRUNE_LB
+    bool split = true;       // BP_OPT_SPLIT
     std::map<std::string, KStat> stats;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
     bp_batch* cached = nullptr;
-    // side stream + fork/join events: the comm-coarsened DP runs concurrently
-    // with the (latency-bound, low-occupancy) refine kernel
-    cudaStream_t side = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr;
+    bool stats_accumulate = false;   // fetching the parts of a split batch: work counters add up
 };
 
 namespace {
@@ -294,6 +302,8 @@ int upload_clusters(bp_ctx* c) {
 }
 
 // Host prep + device layout + H2D of the batch's inputs (on stream st).
+int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t st);
+
 int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cudaStream_t st) {
     if (!c->have_nets || !c->have_cls) return fail(c, BP_BAD_INPUT, "networks/clusters not set");
     std::string err;
@@ -310,6 +320,15 @@ int prepare(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cuda
         fprintf(stderr, "prepare: build_batch %.2f ms, offset check %.2f ms\n",
                 std::chrono::duration<double, std::milli>(t1 - t0).count(),
                 std::chrono::duration<double, std::milli>(t2 - t1).count());
+    return prepare_built(c, B, nq, details, st);
+}
+
+// The device layout, arena and pinned staging of a batch whose host build
+// (B->hb) is done.
+int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
+    static const bool timing = getenv("BP_HOST_TIMING") != nullptr;
+    const HostBatch& hb = B->hb;
+    const auto t2 = std::chrono::steady_clock::now();
     // candidate and stage-slot indices are int32 in the kernels' work lists
     if (hb.ncand >= INT32_MAX || hb.nstage >= ((int64_t)1 << 40))
         return fail(c, BP_BAD_INPUT, "batch too large (" + std::to_string(hb.ncand) +
@@ -508,27 +527,27 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "bottleneck", st, [&] { launch_bottleneck(D, st); }, 2);
     // fork: coarse DPs (side stream) || refine (main stream); both only read
     // the whole-layer DP results and write disjoint state
-    if (!c->side) {
-        cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming);
+    if (!B->side) {
+        cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking);
+        cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&B->join, cudaEventDisableTiming);
     }
     launch_prune_reset(D, st);
     cudaEvent_t ph = phase_begin(c, st);
-    cudaEventRecord(c->fork, st);
-    cudaStreamWaitEvent(c->side, c->fork, 0);
+    cudaEventRecord(B->fork, st);
+    cudaStreamWaitEvent(B->side, B->fork, 0);
     if (hb.nmslot > 0) {
-        timed(c, "minmax_dp_coarse", c->side,
-              [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, c->side); });
-        timed(c, "dedup_copy", c->side, [&] { launch_coarse_copy(D, c->side); });
+        timed(c, "minmax_dp_coarse", B->side,
+              [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, B->side); });
+        timed(c, "dedup_copy", B->side, [&] { launch_coarse_copy(D, B->side); });
     }
-    cudaEventRecord(c->join, c->side);
+    cudaEventRecord(B->join, B->side);
     const int refine_launches = (refine_region_bytes(maxN) > 200 * 1024 || !D.dedup) ? 1 : B->refine_grid ? 3 : 2;
     timed(c, "refine", st, [&] {
         launch_refine(D, c->sm_count, B->refine_grid, B->refine_bytes, B->dp_max_units, T, st);
     }, refine_launches);
     timed(c, "dedup_copy", st, [&] { launch_dedup_copy_refine(D, st); });
-    cudaStreamWaitEvent(st, c->join, 0);
+    cudaStreamWaitEvent(st, B->join, 0);
     // (pruning the coarse-path candidates on the side stream while refine runs,
     // launch_prune(D, 0, side), was measured no faster overall: refine's
     // single-lane walks slow down by as much as the overlap saves)
@@ -558,14 +577,14 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     // the simulator classes are independent: the two exact ones on the side
     // stream overlap the fast classes and the N <= 32 dataflow kernel, so
     // their latency tails overlap instead of adding up
-    cudaEventRecord(c->fork, st);
-    cudaStreamWaitEvent(c->side, c->fork, 0);
-    timed(c, "sim_flow64", c->side, [&] { launch_sim_flow(D, 1, c->sm_count, c->side); });
-    timed(c, "sim_exact", c->side, [&] { launch_sim_exact(D, c->sm_count, c->side); }, 4);
-    cudaEventRecord(c->join, c->side);
+    cudaEventRecord(B->fork, st);
+    cudaStreamWaitEvent(B->side, B->fork, 0);
+    timed(c, "sim_flow64", B->side, [&] { launch_sim_flow(D, 1, c->sm_count, B->side); });
+    timed(c, "sim_exact", B->side, [&] { launch_sim_exact(D, c->sm_count, B->side); }, 4);
+    cudaEventRecord(B->join, B->side);
     for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
     timed(c, "sim_flow32", st, [&] { launch_sim_flow(D, 0, c->sm_count, st); });
-    cudaStreamWaitEvent(st, c->join, 0);
+    cudaStreamWaitEvent(st, B->join, 0);
     timed(c, "sim_share", st, [&] { launch_sim_share(D, st); });
     if (D.prune_lb) {   // round 2: the candidates whose bound does not exceed their query's best
         timed(c, "lb_prune", st, [&] { launch_lb_round2(D, st); }, 2);
@@ -600,20 +619,212 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
                                                  "sim_fast_g32", "sim_fast_g32s2", "sim_fast_g32s4",
                                                  "sim_fast_g32s8", "sim_exact", "sim_flow32", "sim_flow64"};
         if (cudaMemcpy(work, B->dev.work, sizeof(work), cudaMemcpyDeviceToHost) == cudaSuccess) {
-            c->stats["minmax_dp"].work = (double)work[WORK_DP_WHOLE];
-            c->stats["minmax_dp_coarse"].work = (double)work[WORK_DP_COARSE];
-            c->stats["refine"].work = (double)work[WORK_REFINE];
-            c->stats["refine_critical_path"].work = (double)work[WORK_REFINE_MAX];
-            c->stats["prune"].work = (double)work[WORK_PRUNE];
-            c->stats["refine_moves"].work = (double)work[WORK_REFINE_MOVES];
-            c->stats["refine_exact_steps"].work = (double)work[WORK_REFINE_EXACT];
-            c->stats["prune_trials"].work = (double)work[WORK_PRUNE_TRIALS];
-            c->stats["prune_critical_path"].work = (double)work[WORK_PRUNE_MAX];
-            for (int k = 0; k < SIM_CLASSES; ++k) c->stats[names[k]].work = (double)work[WORK_SIM_EVENTS + k];
+            // a split batch's parts add up (the critical paths take the maximum)
+            auto put = [&](const char* k, unsigned long long v, bool is_max = false) {
+                double& w = c->stats[k].work;
+                w = !c->stats_accumulate ? (double)v : is_max ? std::max(w, (double)v) : w + (double)v;
+            };
+            put("minmax_dp", work[WORK_DP_WHOLE]);
+            put("minmax_dp_coarse", work[WORK_DP_COARSE]);
+            put("refine", work[WORK_REFINE]);
+            put("refine_critical_path", work[WORK_REFINE_MAX], true);
+            put("prune", work[WORK_PRUNE]);
+            put("refine_moves", work[WORK_REFINE_MOVES]);
+            put("refine_exact_steps", work[WORK_REFINE_EXACT]);
+            put("prune_trials", work[WORK_PRUNE_TRIALS]);
+            put("prune_critical_path", work[WORK_PRUNE_MAX], true);
+            for (int k = 0; k < SIM_CLASSES; ++k) put(names[k], work[WORK_SIM_EVENTS + k]);
         }
         collect(c);
     }
     return BP_OK;
+}
+
+
+// ---- BP_OPT_SPLIT: a large batch runs as two parts, concurrently.
+// The queries with the batch's largest stage count carry the longest
+// intra_layer_refine walks (a serial chain per query: the refine launch lasts
+// as long as its longest walk, with most SMs idle) and the largest
+// simulations; run as their own batch on a second stream, the other queries'
+// refine, prune and simulate phases overlap that walk.  Each part is a
+// complete batch (its own dedup tables, lists and arena); results are
+// identical to one batch (no result depends on the sharing, see
+// BP_OPT_DEDUP), and the parts' outputs are scattered back into the caller's
+// layout at fetch.
+constexpr int SPLIT_MIN_QUERIES = 4096, SPLIT_MIN_PART = 512;
+
+bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<int32_t>& a, std::vector<int32_t>& b) {
+    if (!c->split || c->plan_only || nq < SPLIT_MIN_QUERIES) return false;
+    std::vector<int32_t> n(nq);
+    int maxN = 0;
+    for (int i = 0; i < nq; ++i) {
+        if (q[i].cluster < 0 || q[i].cluster >= (int)c->hc.desc.size()) return false;   // prepare reports it
+        n[i] = q[i].n_stages > 0 ? q[i].n_stages : c->hc.desc[q[i].cluster].N;
+        maxN = std::max(maxN, n[i]);
+    }
+    a.clear();
+    b.clear();
+    for (int i = 0; i < nq; ++i) (n[i] == maxN ? a : b).push_back(i);
+    return (int)a.size() >= SPLIT_MIN_PART && (int)b.size() >= SPLIT_MIN_PART;
+}
+
+// eager (bp_explore_batch): each part is uploaded and launched on its own
+// stream as soon as it is prepared, so the first part's kernels run while the
+// host prepares the second.  *ran tells the caller that the batch ran.
+int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cudaStream_t st,
+                bool eager = false, bool* ran = nullptr) {
+    if (ran) *ran = false;
+    std::vector<int32_t> ga, gb;
+    if (!split_groups(c, q, nq, ga, gb)) {
+        for (bp_batch* p : B->parts) bp_batch_free(c, p);
+        B->parts.clear();
+        return prepare(c, B, q, nq, details, st);
+    }
+    // the whole batch's validation and layout (the caller's offsets, and the
+    // scatter targets at fetch)
+    std::string err;
+    if (!build_batch(q, nq, c->hn, c->hc, B->hb, err)) return fail(c, BP_BAD_INPUT, err);
+    const HostBatch& hb = B->hb;
+    for (int i = 0; i < nq; ++i)
+        if (q[i].cand_offset != hb.q[i].cand_off || q[i].stage_offset != hb.q[i].stage_off)
+            return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
+    B->nq = nq;
+    B->gen = c->gen;
+    B->details = details != 0;
+    while (B->parts.size() < 2) B->parts.push_back(new bp_batch());
+    B->part_q = {std::move(ga), std::move(gb)};
+    B->part_ids_host.clear();
+    if (eager) {
+        if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
+        cudaEventRecord(B->fork, st);
+    }
+    for (int k = 0; k < 2; ++k) {
+        // the part's host build is the whole build's restricted to its
+        // queries, with its own dense offsets (what bp_layout would give)
+        HostBatch& ph = B->parts[k]->hb;
+        const std::vector<int32_t>& idx = B->part_q[k];
+        ph.q.resize(idx.size());
+        ph.Mpool = hb.Mpool;
+        ph.whole_items.clear();
+        ph.ncand = ph.nstage = ph.nqstage = ph.nmslot = 0;
+        ph.max_units = ph.max_N = ph.max_nbase = 0;
+        for (size_t j = 0; j < idx.size(); ++j) {
+            QDesc d = hb.q[idx[j]];
+            d.cand_off = ph.ncand;
+            d.stage_off = ph.nstage;
+            d.qstage_off = ph.nqstage;
+            d.mslot_off = ph.nmslot;
+            ph.ncand += 2 * (int64_t)d.nbase;
+            ph.nstage += 2 * (int64_t)d.nbase * d.N;
+            ph.nqstage += d.N;
+            ph.nmslot += d.nbase;
+            ph.max_N = std::max(ph.max_N, d.N);
+            ph.max_nbase = std::max(ph.max_nbase, d.nbase);
+            if (d.schema_ok && d.N >= 2) {
+                ph.whole_items.push_back(DPItem{(int32_t)j, -1, -1});
+                ph.max_units = std::max(ph.max_units, c->hn.desc[d.net].L);
+            }
+            ph.q[j] = d;
+        }
+        int rc = prepare_built(c, B->parts[k], (int)idx.size(), details, st);
+        if (rc != BP_OK) return rc;
+        for (int32_t i : idx) B->part_ids_host.push_back(i);
+        if (eager) {
+            bp_batch* p = B->parts[k];
+            if (!p->lane) {
+                cudaStreamCreateWithFlags(&p->lane, cudaStreamNonBlocking);
+                cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming);
+            }
+            cudaStreamWaitEvent(p->lane, B->fork, 0);
+            if ((rc = upload_inputs(c, p, p->lane)) != BP_OK || (rc = run(c, p, p->lane)) != BP_OK) return rc;
+            cudaEventRecord(p->done, p->lane);
+            cudaStreamWaitEvent(st, p->done, 0);
+        }
+    }
+    const size_t idb = B->part_ids_host.size() * sizeof(int64_t);
+    if (!B->part_ids.ensure(idb) || !B->part_best.ensure(2 * sizeof(bp_best_record)) || !B->stage_in.ensure(idb))
+        return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(split)");
+    std::memcpy(B->stage_in.p, B->part_ids_host.data(), idb);
+    B->in_bytes = idb;   // upload_any copies them with the parts' inputs
+    if (eager) {
+        const cudaError_t e = cudaMemcpyAsync(B->part_ids.p, B->stage_in.p, idb, cudaMemcpyHostToDevice, st);
+        c->h2d += (int64_t)idb;
+        if (e != cudaSuccess) return cuda_fail(c, e, "H2D split ids");
+        if (ran) *ran = true;
+    }
+    return BP_OK;
+}
+
+int upload_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
+    if (B->parts.empty()) return upload_inputs(c, B, st);
+    const cudaError_t e = cudaMemcpyAsync(B->part_ids.p, B->stage_in.p, B->in_bytes, cudaMemcpyHostToDevice, st);
+    c->h2d += (int64_t)B->in_bytes;
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D split ids");
+    for (bp_batch* p : B->parts)
+        if (const int rc = upload_inputs(c, p, st); rc != BP_OK) return rc;
+    return BP_OK;
+}
+
+int run_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
+    if (B->parts.empty()) return run(c, B, st);
+    if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
+    cudaEventRecord(B->fork, st);
+    for (bp_batch* p : B->parts) {
+        if (!p->lane) {
+            cudaStreamCreateWithFlags(&p->lane, cudaStreamNonBlocking);
+            cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming);
+        }
+        cudaStreamWaitEvent(p->lane, B->fork, 0);
+        if (const int rc = run(c, p, p->lane); rc != BP_OK) return rc;
+        cudaEventRecord(p->done, p->lane);
+        cudaStreamWaitEvent(st, p->done, 0);
+    }
+    return BP_OK;
+}
+
+int fetch_any(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_stage* stages, cudaStream_t st) {
+    if (B->parts.empty()) return fetch(c, B, res, cand, stages, st);
+    c->stats_accumulate = false;
+    for (size_t k = 0; k < B->parts.size(); ++k) {
+        bp_batch* p = B->parts[k];
+        const HostBatch& ph = p->hb;
+        std::vector<bp_query_result> r(res ? (size_t)p->nq : 0);
+        std::vector<bp_candidate> cd(cand ? (size_t)ph.ncand : 0);
+        std::vector<bp_stage> sg(stages && p->details ? (size_t)ph.nstage : 0);
+        const int rc = fetch(c, p, res ? r.data() : nullptr, cand ? cd.data() : nullptr,
+                             sg.empty() ? nullptr : sg.data(), st);
+        c->stats_accumulate = true;
+        if (rc != BP_OK) { c->stats_accumulate = false; return rc; }
+        for (int j = 0; j < p->nq; ++j) {
+            const QDesc& pd = ph.q[j];
+            const QDesc& wd = B->hb.q[B->part_q[k][j]];
+            if (res) res[B->part_q[k][j]] = r[j];
+            const int64_t nc = 2 * (int64_t)pd.nbase;
+            if (cand) std::memcpy(cand + wd.cand_off, cd.data() + pd.cand_off, (size_t)nc * sizeof(bp_candidate));
+            if (!sg.empty())
+                std::memcpy(stages + wd.stage_off, sg.data() + pd.stage_off, (size_t)(nc * pd.N) * sizeof(bp_stage));
+        }
+    }
+    c->stats_accumulate = false;
+    return BP_OK;
+}
+
+int best_any(bp_ctx* c, bp_batch* B, void* dev_out, int64_t query_base, cudaStream_t st) {
+    if (B->parts.empty()) {
+        timed(c, "best", st, [&] { launch_best(B->dev, (bp_best_record*)dev_out, query_base, nullptr, st); });
+    } else {
+        const int64_t* ids = (const int64_t*)B->part_ids.p;
+        bp_best_record* recs = (bp_best_record*)B->part_best.p;
+        timed(c, "best", st, [&] {
+            for (size_t k = 0; k < B->parts.size(); ++k) {
+                launch_best(B->parts[k]->dev, recs + k, query_base, ids, st);
+                ids += B->part_q[k].size();
+            }
+            launch_best_merge(recs, (int)B->parts.size(), (bp_best_record*)dev_out, st);
+        }, (int)B->parts.size() + 1);
+    }
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BP_OK : cuda_fail(c, e, "best");
 }
 
 }  // namespace
@@ -669,9 +880,6 @@ void bp_destroy(bp_ctx* c) {
     c->cls_mem.release();
     c->stage_tables.release();
     for (auto e : c->event_pool) cudaEventDestroy(e);
-    if (c->side) cudaStreamDestroy(c->side);
-    if (c->fork) cudaEventDestroy(c->fork);
-    if (c->join) cudaEventDestroy(c->join);
     delete c;
 }
 
@@ -745,7 +953,7 @@ bp_batch* bp_batch_prepare(bp_ctx* c, const bp_query* q, int nq, int want_detail
         cudaSetDevice(c->device);
         bp_batch* B = new bp_batch();
         cudaStream_t st = (cudaStream_t)stream;
-        if (prepare(c, B, q, nq, want_details, st) != BP_OK || upload_inputs(c, B, st) != BP_OK) {
+        if (prepare_any(c, B, q, nq, want_details, st) != BP_OK || upload_any(c, B, st) != BP_OK) {
             bp_batch_free(c, B);
             return nullptr;
         }
@@ -768,7 +976,7 @@ int bp_batch_run(bp_ctx* c, bp_batch* B, void* stream) {
     if (!c || !B) return fail(c, BP_BAD_INPUT, "bad arguments");
     if (stale(c, B)) return fail(c, BP_BAD_INPUT, STALE);
     cudaSetDevice(c->device);
-    return run(c, B, (cudaStream_t)stream);
+    return run_any(c, B, (cudaStream_t)stream);
 }
 
 int bp_batch_fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_stage* stages,
@@ -776,24 +984,28 @@ int bp_batch_fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* c
     if (!c || !B) return fail(c, BP_BAD_INPUT, "bad arguments");
     if (stale(c, B)) return fail(c, BP_BAD_INPUT, STALE);
     cudaSetDevice(c->device);
-    return fetch(c, B, res, cand, stages, (cudaStream_t)stream);
+    return fetch_any(c, B, res, cand, stages, (cudaStream_t)stream);
 }
 
 int bp_batch_best(bp_ctx* c, bp_batch* B, void* dev_out, int64_t query_base, void* stream) {
     if (!c || !B || !dev_out) return fail(c, BP_BAD_INPUT, "bad arguments");
     if (stale(c, B)) return fail(c, BP_BAD_INPUT, STALE);
     cudaSetDevice(c->device);
-    cudaStream_t st = (cudaStream_t)stream;
-    timed(c, "best", st, [&] { launch_best(B->dev, (bp_best_record*)dev_out, query_base, nullptr, st); });
-    cudaError_t e = cudaGetLastError();
-    return e == cudaSuccess ? BP_OK : cuda_fail(c, e, "best");
+    return best_any(c, B, dev_out, query_base, (cudaStream_t)stream);
 }
 
 void bp_batch_free(bp_ctx* c, bp_batch* B) {
     if (!B) return;
     if (c) cudaSetDevice(c->device);
+    for (bp_batch* p : B->parts) bp_batch_free(c, p);
     B->mem.release();
     B->stage_in.release();
+    B->part_ids.release();
+    B->part_best.release();
+    if (B->side) cudaStreamDestroy(B->side);
+    if (B->lane) cudaStreamDestroy(B->lane);
+    for (cudaEvent_t ev : {B->fork, B->join, B->done})
+        if (ev) cudaEventDestroy(ev);
     delete B;
 }
 
@@ -808,12 +1020,13 @@ int bp_explore_batch(bp_ctx* c, const bp_query* q, int nq, bp_query_result* res,
         static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
         auto now = [] { return std::chrono::steady_clock::now(); };
         const auto t0 = now();
-        int rc = prepare(c, B, q, nq, stages != nullptr, st);
+        bool ran = false;
+        int rc = prepare_any(c, B, q, nq, stages != nullptr, st, true, &ran);
         const auto t1 = now();
-        if (rc == BP_OK) rc = upload_inputs(c, B, st);
-        if (rc == BP_OK) rc = run(c, B, st);
+        if (rc == BP_OK && !ran) rc = upload_any(c, B, st);
+        if (rc == BP_OK && !ran) rc = run_any(c, B, st);
         const auto t2 = now();
-        if (rc == BP_OK) rc = fetch(c, B, res, cand, stages, st);
+        if (rc == BP_OK) rc = fetch_any(c, B, res, cand, stages, st);
         if (timing) {
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
             fprintf(stderr, "bp_explore_batch: prepare %.2f ms, launch %.2f ms, wait+fetch %.2f ms\n", ms(t0, t1),
@@ -840,6 +1053,7 @@ int bp_set_option(bp_ctx* c, int option, int64_t value) {
         case BP_OPT_DEDUP: c->dedup = value != 0; return BP_OK;
         case BP_OPT_PLAN_ONLY: c->plan_only = value != 0; return BP_OK;
         case BP_OPT_PRUNE_LB: c->prune_lb = value != 0; return BP_OK;
+        case BP_OPT_SPLIT: c->split = value != 0; return BP_OK;
         default: return fail(c, BP_BAD_INPUT, "unknown option " + std::to_string(option));
     }
 }

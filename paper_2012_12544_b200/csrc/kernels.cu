@@ -781,7 +781,7 @@ __global__ void __launch_bounds__(BEST_THREADS) k_best(BatchDev B, bp_best_recor
         const bp_query_result& r = B.res[qi];
         bp_best_record x{};
         x.valid = r.status == BP_Q_OK ? 1 : 0;
-        x.query_id = query_ids ? query_ids[qi] : query_base + qi;
+        x.query_id = (query_ids ? query_ids[qi] : qi) + query_base;
         if (x.valid) {
             x.makespan = r.best_makespan;
             x.peak_memory = r.best_peak_memory;
@@ -1001,6 +1001,17 @@ void launch_plan_finish(const BatchDev& B, cudaStream_t st) {
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);
 }
+__global__ void k_best_merge(const bp_best_record* recs, int n, bp_best_record* out) {
+    bp_best_record b = recs[0];
+    for (int k = 1; k < n; ++k)
+        if (best_less(recs[k], b)) b = recs[k];
+    *out = b;
+}
+
+void launch_best_merge(const bp_best_record* recs, int n, bp_best_record* out, cudaStream_t st) {
+    k_best_merge<<<1, 1, 0, st>>>(recs, n, out);
+}
+
 void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,
                  cudaStream_t st) {
     k_best<<<1, BEST_THREADS, 0, st>>>(B, out, query_base, query_ids);

@@ -48,6 +48,7 @@ cudaError_t timeline_simulate(const Pools& P, int clusterN, const bp_plan_reques
                               int64_t* h2d, int64_t* d2h);
 cudaError_t timeline_estimate(const Pools& P, int clusterN, const bp_plan_request& q, bp_estimate_result* res,
                               bp_stage* stages, int32_t* infeasible, int64_t* h2d, int64_t* d2h);
+void launch_best_merge(const bp_best_record* recs, int n, bp_best_record* out, cudaStream_t st);
 void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,
                  cudaStream_t st);
 

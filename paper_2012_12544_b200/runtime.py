@@ -112,6 +112,13 @@ class Explorer:
         if rc != 0:
             raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
 
+    def split(self, on=True):
+        """BP_OPT_SPLIT: run large batches as two concurrent parts (default
+        on; results are identical either way)."""
+        rc = self.lib.bp_set_option(self.ctx, abi.BP_OPT_SPLIT, 1 if on else 0)
+        if rc != 0:
+            raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
+
     def plan_call(self, req, which, cap=0):
         """bp_simulate_plan (which='simulate') or bp_estimate_plan on a
         bp_plan_request for this context's loaded problem.  Returns the raw

@@ -31,7 +31,8 @@ for rep in range(4):
     t5 = time.perf_counter()
     print(f"load {1e3*(t1-t0):.1f} ms  prepare {1e3*(t2-t1):.1f} ms  run {1e3*(t3-t2):.1f} ms  "
           f"fetch {1e3*(t4-t3):.1f} ms  free {1e3*(t5-t4):.1f} ms  total {1e3*(t5-t0):.1f} ms")
-t = time.perf_counter()
-ex.load(p, force=True)
-r = ex.explore(p, details=False)
-print(f"explore() e2e {1e3*(time.perf_counter()-t):.1f} ms")
+for rep in range(4):   # the public call, as bench.py's e2e leg makes it (its batch arena is reused)
+    t = time.perf_counter()
+    ex.load(p, force=True)
+    r = ex.explore(p, details=False)
+    print(f"explore() e2e {1e3*(time.perf_counter()-t):.1f} ms")

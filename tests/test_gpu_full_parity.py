@@ -67,13 +67,18 @@ def global_candidates(p, idx):
     return np.concatenate([np.arange(q["cand_offset"][i], q["cand_offset"][i] + p.n_candidates[i]) for i in idx])
 
 
-@pytest.mark.parametrize("dedup", [True, False], ids=["dedup", "no_dedup"])
-def test_c5_every_candidate_matches_reference(ex, c5, gold, dedup):
+@pytest.mark.parametrize("dedup,split", [(True, True), (False, True), (True, False)],
+                         ids=["dedup_split", "no_dedup", "one_batch"])
+def test_c5_every_candidate_matches_reference(ex, c5, gold, dedup, split):
+    """BP_OPT_SPLIT on (the default: the N = 64 queries and the rest run as two
+    concurrent parts) and off, batch dedup on and off."""
     ex.dedup(dedup)
+    ex.split(split)
     try:
         res, cand, st = ex.explore(c5, details=True)
     finally:
         ex.dedup(True)
+        ex.split(True)
     assert res.tobytes() == gold["res"].tobytes(), "per-query records differ"
     check(candidate_digests(c5, cand, st), gold["digest"], gold["status"], "C5 one batch")
 
