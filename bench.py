@@ -449,7 +449,6 @@ def run_b200(args):
         for _ in range(args.warmup):
             ex.run(batch, stream=sp)
     torch.cuda.synchronize()
-    ex.profiling(True)
     l0 = ex.launches()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier()
@@ -463,9 +462,32 @@ def run_b200(args):
         barrier()
     launches = ex.launches() - l0
     res, _, _ = ex.fetch(batch, p, details=False, stream=sp)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+
+    # ---- per-kernel breakdown (CUDA events around every launch), on the same
+    # steps run as ONE batch (BP_OPT_SPLIT off): with the split, two parts run
+    # concurrently and their kernel spans would overlap
+    ex.split(False)
+    kb = ex.prepare(p, details=False, stream=sp)
+    with torch.cuda.stream(stream):
+        ex.run(kb, stream=sp)
+    torch.cuda.synchronize()
+    ex.profiling(True)
+    kb_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with torch.cuda.stream(stream):
+        for i in range(args.steps):
+            flush.zero_()
+            kb_evs[i][0].record(stream)
+            ex.run(kb, stream=sp)
+            kb_evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    res_kb, _, _ = ex.fetch(kb, p, details=False, stream=sp)
     stats = ex.kernel_stats()
     ex.profiling(False)
-    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ex.free(kb)
+    ex.split(True)
+    assert res_kb.tobytes() == res.tobytes(), "one-batch and split runs differ"
+    kb_ms = sum(a.elapsed_time(b) for a, b in kb_evs) / args.steps
     total_ms, rank_ms = max_over_ranks(sum(step_ms))
     value = cands_per_step * args.steps / (total_ms / 1e3)
 
@@ -594,6 +616,8 @@ def run_b200(args):
             "sweep_roofline": sweep,
             "refine_latency": refine_lat,
             "kernels": kern,
+            "kernels_note": (f"per-kernel CUDA-event spans of the same steps run as one batch (BP_OPT_SPLIT off: "
+                             f"{kb_ms:.2f} ms per step); the headline runs the batch as two concurrent parts"),
             "best": {"makespan": f"{int(best['makespan']['num'])}/{int(best['makespan']['den'])}",
                      "M": int(best["M"]), "kind": int(best["kind"]), "query_id": int(best["query_id"])},
             "query_status_hist": np.bincount(res["status"], minlength=7).tolist()}
