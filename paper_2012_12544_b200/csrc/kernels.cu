@@ -108,9 +108,11 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_cost_prefix(const NetDesc* net
     }
 }
 
+// a warp per query: the lanes write its candidate records (coalesced)
 __global__ void k_setup(BatchDev B) {
-    int qi = blockIdx.x * blockDim.x + threadIdx.x;
-    if (qi < B.nq) setup_query(B, qi);
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int qi = (int)(t >> 5);
+    if (qi < B.nq) setup_query(B, qi, (int)(t & 31), 32);
 }
 
 __device__ __forceinline__ uint64_t coarse_hash(int32_t cls, int64_t a_th) {
@@ -168,8 +170,10 @@ __global__ void k_coarse_queue(BatchDev B) {
 }
 
 // shared coarse plans: both kinds' candidate slots of the M slot
+// A warp per query: the lanes copy the (M slot, kind, stage) entries.
 __global__ void k_coarse_copy(BatchDev B) {
-    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int qi = (int)(t >> 5), lane = (int)(t & 31);
     if (qi >= B.nq) return;
     const QDesc Q = B.q[qi];
     for (int m = 0; m < Q.nbase; ++m) {
@@ -178,14 +182,13 @@ __global__ void k_coarse_copy(BatchDev B) {
         const MState& rm = B.ms[ms.crep];
         const QDesc R = B.q[rm.q];
         const int rmm = (int)(ms.crep - R.mslot_off);
-        ms.coarse_ok = rm.coarse_ok;
-        for (int k = 0; k < 2; ++k) {
+        if (lane == 0) ms.coarse_ok = rm.coarse_ok;
+        for (int e = lane; e < 2 * Q.N; e += 32) {
+            const int k = e / Q.N, s = e - k * Q.N;
             const int64_t o = Q.stage_off + ((int64_t)k * Q.nbase + m) * Q.N;
             const int64_t ro = R.stage_off + ((int64_t)k * R.nbase + rmm) * R.N;
-            for (int s = 0; s < Q.N; ++s) {
-                B.clo[o + s] = B.clo[ro + s];
-                B.chi[o + s] = B.chi[ro + s];
-            }
+            B.clo[o + s] = B.clo[ro + s];
+            B.chi[o + s] = B.chi[ro + s];
         }
     }
 }
@@ -251,31 +254,38 @@ __global__ void k_dedup_resolve(BatchDev B) {
     B.qrep[qi] = rep;
 }
 
-// whole-layer DP results: plan ranges, max stage time, InfeasibleShape flag
+// whole-layer DP results: plan ranges, max stage time, InfeasibleShape flag.
+// A warp per query: the lanes copy the stages (coalesced).
 __global__ void k_dedup_copy_dp(BatchDev B) {
-    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int qi = (int)(t >> 5), lane = (int)(t & 31);
     if (qi >= B.nq) return;
     const int r = B.qrep[qi];
     if (r == qi) return;
-    const QState& s = B.qs[r];
-    QState& d = B.qs[qi];
-    d.dp_shape = s.dp_shape;
-    d.target = s.target;
+    if (lane == 0) {
+        const QState& s = B.qs[r];
+        QState& d = B.qs[qi];
+        d.dp_shape = s.dp_shape;
+        d.target = s.target;
+    }
     const int64_t o = B.q[qi].qstage_off, os = B.q[r].qstage_off;
-    for (int k = 0; k < B.q[qi].N; ++k) {
+    for (int k = lane; k < B.q[qi].N; k += 32) {
         B.qlo[o + k] = B.qlo[os + k];
         B.qhi[o + k] = B.qhi[os + k];
     }
 }
 
-// refined plan, its stage sums and validate_plan outcome, simulator scale
+// refined plan, its stage sums and validate_plan outcome, simulator scale.
+// A warp per query: the lanes copy the stages (coalesced).
 __global__ void k_dedup_copy_refine(BatchDev B) {
-    int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int qi = (int)(t >> 5), lane = (int)(t & 31);
     if (qi >= B.nq) return;
     const int r = B.qrep[qi];
     if (r == qi || !B.qs[qi].need_refine) return;
     const QState& s = B.qs[r];
     QState& d = B.qs[qi];
+    if (lane == 0) {
     d.refine_err = s.refine_err;
     d.refined = s.refined;
     d.refine_iters = s.refine_iters;
@@ -288,8 +298,9 @@ __global__ void k_dedup_copy_refine(BatchDev B) {
     d.vaux = s.vaux;
     d.D = s.D;
     d.sumFB_D = s.sumFB_D;
+    }
     const int64_t o = B.q[qi].qstage_off, os = B.q[r].qstage_off;
-    for (int k = 0; k < B.q[qi].N; ++k) {
+    for (int k = lane; k < B.q[qi].N; k += 32) {
         B.qlo[o + k] = B.qlo[os + k];
         B.qhi[o + k] = B.qhi[os + k];
         B.qlead[o + k] = B.qlead[os + k];
@@ -809,7 +820,7 @@ void launch_cost_prefix(const NetDesc* nets, int n_nets, const int64_t* fp, cons
 }
 
 void launch_setup(const BatchDev& B, cudaStream_t st) {
-    if (B.nq) k_setup<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    if (B.nq) k_setup<<<blocks((int64_t)B.nq * 32, 256), 256, 0, st>>>(B);
 }
 
 // ---- scheduling orders on the device: a radix sort of one packed key per
@@ -879,10 +890,10 @@ void launch_dedup(const BatchDev& B, cudaStream_t st) {
     }
 }
 void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st) {
-    if (B.nq) k_dedup_copy_dp<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    if (B.nq) k_dedup_copy_dp<<<blocks((int64_t)B.nq * 32, 256), 256, 0, st>>>(B);
 }
 void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st) {
-    if (B.nq) k_dedup_copy_refine<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    if (B.nq) k_dedup_copy_refine<<<blocks((int64_t)B.nq * 32, 256), 256, 0, st>>>(B);
 }
 void launch_bottleneck(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.ckey, 0, ((size_t)B.cmask + 1) * sizeof(unsigned long long), st);
@@ -893,7 +904,7 @@ void launch_bottleneck(const BatchDev& B, cudaStream_t st) {
     }
 }
 void launch_coarse_copy(const BatchDev& B, cudaStream_t st) {
-    if (B.nq) k_coarse_copy<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    if (B.nq) k_coarse_copy<<<blocks((int64_t)B.nq * 32, 256), 256, 0, st>>>(B);
 }
 size_t refine_region_bytes(int max_N) {
     size_t r = (size_t)max_N * (5 * sizeof(Rat) + 2 * sizeof(int32_t) + 1);

@@ -25,44 +25,43 @@ BPK_HD int kind_of_slot(int mode, int k) {   // feasible_kinds, explorer.hpp:17-
 BPK_HD int status_of_err(uint32_t code) { return (int)code; }   // ERR_* == BP_C_*
 
 // ---------------------------------------------------------------- K0
-BPK_HDNI void setup_query(const BatchDev& B, int qi) {
+// lane / nlanes: the candidates of the query are shared among nlanes
+// cooperating threads (a warp on the device, 1 in the host emulation)
+BPK_HDNI void setup_query(const BatchDev& B, int qi, int lane = 0, int nlanes = 1) {
     const QDesc Q = B.q[qi];
-    QState& qs = B.qs[qi];
-    qs = QState{};
-    bp_query_result& r = B.res[qi];
-    r = bp_query_result{};
-    r.best = -1;
-    r.first_error = -1;
-    if (!Q.schema_ok) {
-        r.status = BP_Q_SCHEMA;
-        return;
+    if (lane == 0) {
+        B.qs[qi] = QState{};
+        bp_query_result r = bp_query_result{};
+        r.best = -1;
+        r.first_error = -1;
+        r.status = Q.schema_ok ? 0 : BP_Q_SCHEMA;
+        r.n_candidates = Q.schema_ok ? 2 * Q.nbase : 0;
+        B.res[qi] = r;
     }
+    if (!Q.schema_ok) return;
     ChainView c = chain_view(B.P, Q.cl, Q.N);
-    r.n_candidates = 2 * Q.nbase;
-    for (int k = 0; k < 2; ++k) {
-        int kind = kind_of_slot(c.mode, k);
+    for (int64_t local = lane; local < 2 * (int64_t)Q.nbase; local += nlanes) {
+        const int k = (int)(local / Q.nbase), m = (int)(local - (int64_t)k * Q.nbase);
+        const int kind = kind_of_slot(c.mode, k);
         int64_t min_micro = 1;   // candidate_Ms, explorer.hpp:42-47
         for (int a = 0; a < Q.N; ++a) {
             int64_t mm = c.minm[4 * a + kind];
             if (mm > min_micro) min_micro = mm;
         }
-        for (int m = 0; m < Q.nbase; ++m) {
-            int64_t local = (int64_t)k * Q.nbase + m;
-            int64_t ci = Q.cand_off + local;
-            bp_candidate cd = bp_candidate{};
-            cd.kind = kind;
-            cd.M = B.Mpool[Q.m_off + m];
-            cd.micro = Q.mini / cd.M;
-            cd.rank = -1;
-            cd.n_stages = Q.N;
-            // (`bapipe plan` calls balance_partition with no min-micro filter)
-            cd.status = (B.plan_only || Q.mini / cd.M >= min_micro) ? C_PENDING : BP_C_REJ_MIN_MICRO;
-            B.cand[ci] = cd;
-            B.cs[ci] = CState{};
-            B.cq[ci] = qi;
-        }
+        const int64_t ci = Q.cand_off + local;
+        bp_candidate cd = bp_candidate{};
+        cd.kind = kind;
+        cd.M = B.Mpool[Q.m_off + m];
+        cd.micro = Q.mini / cd.M;
+        cd.rank = -1;
+        cd.n_stages = Q.N;
+        // (`bapipe plan` calls balance_partition with no min-micro filter)
+        cd.status = (B.plan_only || Q.mini / cd.M >= min_micro) ? C_PENDING : BP_C_REJ_MIN_MICRO;
+        B.cand[ci] = cd;
+        B.cs[ci] = CState{};
+        B.cq[ci] = qi;
     }
-    for (int m = 0; m < Q.nbase; ++m) B.ms[Q.mslot_off + m] = MState{};
+    for (int m = lane; m < Q.nbase; m += nlanes) B.ms[Q.mslot_off + m] = MState{};
 }
 
 // ---------------------------------------------------------------- K1b
