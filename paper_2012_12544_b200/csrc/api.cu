@@ -658,7 +658,12 @@ bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<int32_
     std::vector<int32_t> n(nq);
     int maxN = 0;
     for (int i = 0; i < nq; ++i) {
-        if (q[i].cluster < 0 || q[i].cluster >= (int)c->hc.desc.size()) return false;   // prepare reports it
+        // a query the host build would reject: no split, so that the one-batch
+        // path reports it with its own index
+        if (q[i].cluster < 0 || q[i].cluster >= (int)c->hc.desc.size() || q[i].network < 0 ||
+            q[i].network >= (int)c->hn.desc.size() || q[i].n_stages < 0 ||
+            q[i].n_stages > c->hc.desc[q[i].cluster].N || (q[i].n_m > 0 && !q[i].m_list))
+            return false;
         n[i] = q[i].n_stages > 0 ? q[i].n_stages : c->hc.desc[q[i].cluster].N;
         maxN = std::max(maxN, n[i]);
     }
@@ -669,8 +674,9 @@ bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<int32_
 }
 
 // eager (bp_explore_batch): each part is uploaded and launched on its own
-// stream as soon as it is prepared, so the first part's kernels run while the
-// host prepares the second.  *ran tells the caller that the batch ran.
+// stream as soon as its host build is done, so the first part's kernels (the
+// long refine walks) run while the host builds the second.  *ran tells the
+// caller that the batch ran.
 int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cudaStream_t st,
                 bool eager = false, bool* ran = nullptr) {
     if (ran) *ran = false;
@@ -680,14 +686,7 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         B->parts.clear();
         return prepare(c, B, q, nq, details, st);
     }
-    // the whole batch's validation and layout (the caller's offsets, and the
-    // scatter targets at fetch)
-    std::string err;
-    if (!build_batch(q, nq, c->hn, c->hc, B->hb, err)) return fail(c, BP_BAD_INPUT, err);
-    const HostBatch& hb = B->hb;
-    for (int i = 0; i < nq; ++i)
-        if (q[i].cand_offset != hb.q[i].cand_off || q[i].stage_offset != hb.q[i].stage_off)
-            return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
+    if (!c->have_nets || !c->have_cls) return fail(c, BP_BAD_INPUT, "networks/clusters not set");
     B->nq = nq;
     B->gen = c->gen;
     B->details = details != 0;
@@ -698,39 +697,24 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
         cudaEventRecord(B->fork, st);
     }
+    std::string err;
+    std::vector<bp_query> in;
+    static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
+    const auto t0 = std::chrono::steady_clock::now();
+    auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
     for (int k = 0; k < 2; ++k) {
-        // the part's host build is the whole build's restricted to its
-        // queries, with its own dense offsets (what bp_layout would give)
-        HostBatch& ph = B->parts[k]->hb;
+        // the part's host build, on its own queries (its own dense layout)
         const std::vector<int32_t>& idx = B->part_q[k];
-        ph.q.resize(idx.size());
-        ph.Mpool = hb.Mpool;
-        ph.whole_items.clear();
-        ph.ncand = ph.nstage = ph.nqstage = ph.nmslot = 0;
-        ph.max_units = ph.max_N = ph.max_nbase = 0;
-        for (size_t j = 0; j < idx.size(); ++j) {
-            QDesc d = hb.q[idx[j]];
-            d.cand_off = ph.ncand;
-            d.stage_off = ph.nstage;
-            d.qstage_off = ph.nqstage;
-            d.mslot_off = ph.nmslot;
-            ph.ncand += 2 * (int64_t)d.nbase;
-            ph.nstage += 2 * (int64_t)d.nbase * d.N;
-            ph.nqstage += d.N;
-            ph.nmslot += d.nbase;
-            ph.max_N = std::max(ph.max_N, d.N);
-            ph.max_nbase = std::max(ph.max_nbase, d.nbase);
-            if (d.schema_ok && d.N >= 2) {
-                ph.whole_items.push_back(DPItem{(int32_t)j, -1, -1});
-                ph.max_units = std::max(ph.max_units, c->hn.desc[d.net].L);
-            }
-            ph.q[j] = d;
-        }
-        int rc = prepare_built(c, B->parts[k], (int)idx.size(), details, st);
+        in.resize(idx.size());
+        for (size_t j = 0; j < idx.size(); ++j) in[j] = q[idx[j]];
+        bp_batch* p = B->parts[k];
+        if (!build_batch(in.data(), (int)in.size(), c->hn, c->hc, p->hb, err)) return fail(c, BP_BAD_INPUT, err);
+        const double tb = since();
+        int rc = prepare_built(c, p, (int)idx.size(), details, st);
         if (rc != BP_OK) return rc;
+        if (timing) fprintf(stderr, "split part %d (%zu queries): built %.2f ms, prepared %.2f ms\n", k, idx.size(), tb, since());
         for (int32_t i : idx) B->part_ids_host.push_back(i);
         if (eager) {
-            bp_batch* p = B->parts[k];
             if (!p->lane) {
                 cudaStreamCreateWithFlags(&p->lane, cudaStreamNonBlocking);
                 cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming);
@@ -739,7 +723,25 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
             if ((rc = upload_inputs(c, p, p->lane)) != BP_OK || (rc = run(c, p, p->lane)) != BP_OK) return rc;
             cudaEventRecord(p->done, p->lane);
             cudaStreamWaitEvent(st, p->done, 0);
+            if (timing) fprintf(stderr, "split part %d launched %.2f ms\n", k, since());
         }
+    }
+    // the whole batch's layout, in the caller's query order, from the parts'
+    // builds: the caller's offsets must be bp_layout's, and fetch scatters
+    // the parts' records to them
+    HostBatch& hb = B->hb;
+    hb.q.resize(nq);
+    for (int k = 0; k < 2; ++k)
+        for (size_t j = 0; j < B->part_q[k].size(); ++j) hb.q[B->part_q[k][j]] = B->parts[k]->hb.q[j];
+    hb.ncand = hb.nstage = 0;
+    for (int i = 0; i < nq; ++i) {
+        QDesc& d = hb.q[i];
+        d.cand_off = hb.ncand;
+        d.stage_off = hb.nstage;
+        hb.ncand += 2 * (int64_t)d.nbase;
+        hb.nstage += 2 * (int64_t)d.nbase * d.N;
+        if (q[i].cand_offset != d.cand_off || q[i].stage_offset != d.stage_off)
+            return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
     }
     const size_t idb = B->part_ids_host.size() * sizeof(int64_t);
     if (!B->part_ids.ensure(idb) || !B->part_best.ensure(2 * sizeof(bp_best_record)) || !B->stage_in.ensure(idb))

@@ -251,6 +251,8 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
     HB.ncand = HB.nstage = HB.nqstage = HB.nmslot = 0;
     HB.max_units = HB.max_N = HB.max_nbase = 0;
     std::unordered_map<int64_t, std::pair<int64_t, int>> divisors;   // mini -> (offset, count)
+    int64_t last_mini = -1;
+    std::pair<int64_t, int> last_div{0, 0};
     // per network, the smallest type id without a profile: a chain prefix
     // whose largest type id is below it passes validate_pair's type check
     // at once (otherwise the per-accelerator loop decides)
@@ -294,6 +296,9 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
                 if (m < 1 || (b.mini_batch >= 1 && b.mini_batch % m != 0)) ok = false;
                 HB.Mpool.push_back(m < 1 ? 1 : m);
             }
+        } else if (b.mini_batch >= 1 && b.mini_batch == last_mini) {   // sweeps repeat one mini-batch size
+            Q.m_off = last_div.first;
+            Q.nbase = last_div.second;
         } else if (b.mini_batch >= 1) {
             auto it = divisors.find(b.mini_batch);
             if (it == divisors.end()) {
@@ -310,6 +315,8 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
             }
             Q.m_off = it->second.first;
             Q.nbase = it->second.second;
+            last_mini = b.mini_batch;
+            last_div = it->second;
         }
         Q.schema_ok = ok ? 1 : 0;   // nbase kept: the output layout counts the slots
         Q.cand_off = HB.ncand;
