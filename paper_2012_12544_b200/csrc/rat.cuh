@@ -42,7 +42,7 @@ namespace bpk {
 
 // host-only operation counters for the test emulator (tests/emu, BPK_OPSTATS)
 #if defined(BPK_OPSTATS) && !defined(__CUDA_ARCH__)
-extern unsigned long long bpk_opstats[16];
+extern unsigned long long bpk_opstats[32];
 #define BPK_COUNT(i) (++bpk_opstats[i])
 #else
 #define BPK_COUNT(i) ((void)0)

@@ -138,10 +138,11 @@ BPK_HD Rat rf_add_p2(Rat a, int64_t bn, int m, int s) {
     const int l = ea < m ? ea : m;
     const int64_t ad = a.d >> l;
     const int64_t t = (a.n << (m - l)) + (s > 0 ? bn : -bn) * ad;
-    if (t == 0) return Rat{0, 1};
-    int z = rf_ctz64(uabs64(t));
+    // branch-free (the commit's four sums interleave): t == 0 gives 0/1
+    const uint64_t ut = uabs64(t);
+    int z = rf_ctz64(ut | ((uint64_t)1 << 62));
     z = z < l ? z : l;
-    return Rat{t >> z, ad << (m - z)};
+    return Rat{t >> z, t == 0 ? 1 : ad << (m - z)};
 }
 
 // x * c for x = xn / 2^m reduced (xn odd unless m = 0) and 0 < c < 2^19
@@ -287,6 +288,7 @@ BPK_HD int refine_fast_walk(const FastRefine& q, int64_t* stats, long long* prof
                 RF_MARK(7);
                 const Rat ta = q.t[n0], tb = q.t[n0 + 1];
                 const int32_t lo0 = q.lo[n0], hi0 = q.hi[n0], lo1 = q.lo[n0 + 1], hi1 = q.hi[n0 + 1];
+                const int32_t ty0 = q.type[n0], ty1 = q.type[n0 + 1];
                 // t_a vs t_b over the common scale D = lcm(d_a, d_b)
                 int64_t D, A, Bv;
                 uint32_t g;
@@ -298,6 +300,7 @@ BPK_HD int refine_fast_walk(const FastRefine& q, int64_t* stats, long long* prof
                     A = ga ? ta.n : ta.n << sh;
                     Bv = ga ? tb.n << sh : tb.n;
                 } else {
+                    BPK_COUNT(22);
                     const RfCmp r = rf_compare_general(ta, tb);
                     D = r.D;
                     A = r.A;
@@ -313,8 +316,8 @@ BPK_HD int refine_fast_walk(const FastRefine& q, int64_t* stats, long long* prof
                 const bool shared = hi0 == lo1;
                 if (j < 1 || j > q.L) return RF_BAIL;     // (the reference's UB case; the general kernel reports it)
                 if (dir < 0 && !shared && q.act[j - 1] > q.act[hi0 - 1]) continue;
-                const int64_t c_from = q.cost[q.type[from] * q.L + (j - 1)];
-                const int64_t c_to = q.cost[q.type[to] * q.L + (j - 1)];
+                const int64_t c_from = q.cost[(dir > 0 ? ty0 : ty1) * q.L + (j - 1)];
+                const int64_t c_to = q.cost[(dir > 0 ? ty1 : ty0) * q.L + (j - 1)];
                 const Rat t_hi = dir > 0 ? ta : tb, t_lo = dir > 0 ? tb : ta;
                 const int64_t Th = dir > 0 ? A : Bv, Tl = dir > 0 ? Bv : A;
                 // avail = owned_fraction(from, j) (plan.hpp:33-39)
@@ -328,8 +331,10 @@ BPK_HD int refine_fast_walk(const FastRefine& q, int64_t* stats, long long* prof
                 const int64_t Nd = Th - Tl;
                 Rat x{0, 1};
                 bool quant;
+                int eD = -1;                              // log2 D when x is x0 and D a power of two
                 int64_t qn = Nd, qd = D * cs;             // the value to quantize (need not be reduced)
                 if (!rf_lt(Rat{Nd, D * cs}, avail)) {
+                    BPK_COUNT(21);
                     // x = avail - 1/1024
                     x = rf_add_p2(avail, 1, 10, -1);
                     if (x.n <= 0) continue;
@@ -338,21 +343,30 @@ BPK_HD int refine_fast_walk(const FastRefine& q, int64_t* stats, long long* prof
                     qd = x.d;
                 } else {
                     // den(x0) = 2^E2 * O / gcd(Nd, O), O the odd part of D * cs
-                    const int eD = rf_ctz((uint32_t)D), ec = rf_ctz((uint32_t)cs);
+                    eD = rf_ctz((uint32_t)D);
+                    const int ec = rf_ctz((uint32_t)cs);
                     const int eN = rf_ctz64((uint64_t)Nd);
                     const int E2 = eD + ec - (eN < eD + ec ? eN : eD + ec);
                     const uint64_t O = (uint64_t)(D >> eD) * (uint64_t)(cs >> ec);
+                    BPK_COUNT(16);
                     if (E2 > 10) {
+                        BPK_COUNT(17);
                         quant = true;                     // den(x0) > 1024
                     } else if (O == 1) {
+                        BPK_COUNT(18);
                         quant = false;                    // den(x0) = 2^E2 <= 1024
                         x = Rat{Nd >> (eN < eD + ec ? eN : eD + ec), (int64_t)1 << E2};
                     } else if ((1024 >> E2) < 3) {
+                        BPK_COUNT(19);
                         // den(x0) <= 1024 only if O divides Nd
                         uint64_t qo;
-                        quant = !rf_divides((uint64_t)Nd, O, rf_inv64(O), &qo);
+                        // O is the odd part of cs (< 2^20) unless D has an odd factor:
+                        // the inverse mod 2^32 then one lift is half the work of mod 2^64
+                        const uint64_t inv = O >> 32 ? rf_inv64(O) : inv64_lift((uint32_t)O, inv32_odd((uint32_t)O));
+                        quant = !rf_divides((uint64_t)Nd, O, inv, &qo);
                         if (!quant) x = Rat{(int64_t)qo >> (eN < eD + ec ? eN : eD + ec), (int64_t)1 << E2};
                     } else {
+                        BPK_COUNT(20);
                         x = rf_x0_general(Nd, D, g, cs);
                         quant = x.d > 1024;
                     }
@@ -362,10 +376,17 @@ BPK_HD int refine_fast_walk(const FastRefine& q, int64_t* stats, long long* prof
                 if (quant) {
                     // k = floor(1024 x), kc = ceil(1024 x)
                     const int64_t num = qn * 1024, den = qd;
-                    k = rf_small_quot(num, den);
+                    if (eD >= 0 && qd == D * cs && rf_pow2((uint32_t)D)) {
+                        // x0 with D = 2^eD: floor(1024 Nd / D) is a shift, below 1024 cs < 2^30,
+                        // and k = that / cs a 32-bit division
+                        const uint32_t Y = (uint32_t)(eD >= 10 ? (Nd >> (eD - 10)) : (Nd << (10 - eD)));
+                        k = (int64_t)(Y / (uint32_t)cs);
+                    } else {
+                        k = rf_small_quot(num, den);
+                    }
                     kc = k + (k * den != num ? 1 : 0);
-                    const int zl = k ? (rf_ctz64((uint64_t)k) < 10 ? rf_ctz64((uint64_t)k) : 10) : 10;
-                    const int zh = rf_ctz64((uint64_t)kc) < 10 ? rf_ctz64((uint64_t)kc) : 10;
+                    const int zl = k ? (rf_ctz((uint32_t)k) < 10 ? rf_ctz((uint32_t)k) : 10) : 10;
+                    const int zh = rf_ctz((uint32_t)kc) < 10 ? rf_ctz((uint32_t)kc) : 10;
                     const Rat qlo = k ? Rat{k >> zl, (int64_t)1024 >> zl} : Rat{0, 1};
                     const Rat qhi = Rat{kc >> zh, (int64_t)1024 >> zh};
                     if (!rf_lt(qhi, avail)) {
@@ -402,6 +423,7 @@ BPK_HD int refine_fast_walk(const FastRefine& q, int64_t* stats, long long* prof
                         fb = dir > 0 ? x : Rat{x.d - x.n, x.d};
                     }
                 } else {
+                    BPK_COUNT(23);
                     const RfCommit o = rf_commit_general(t_hi, t_lo, x, c_from, c_to, trail_a, lead_b, dir, shared);
                     nh = o.nh;
                     nl = o.nl;

@@ -18,7 +18,7 @@
 using namespace bpk;
 
 #ifdef BPK_OPSTATS
-unsigned long long bpk::bpk_opstats[16];
+unsigned long long bpk::bpk_opstats[32];
 #endif
 
 namespace {
@@ -457,7 +457,7 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
 #ifdef BPK_OPSTATS
     if (getenv("BPEMU_STATS")) {
         fprintf(stderr, "opstats");
-        for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", bpk_opstats[k]);
+        for (int k = 0; k < 32; ++k) fprintf(stderr, " %llu", bpk_opstats[k]);
         fprintf(stderr, "\n");
     }
 #endif
@@ -490,8 +490,8 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
         int cls = sim_classify(B, c);
         if (cls < 0) continue;
 #ifdef BPK_OPSTATS
-        unsigned long long before[16];
-        for (int k = 0; k < 16; ++k) before[k] = bpk_opstats[k];
+        unsigned long long before[32];
+        for (int k = 0; k < 32; ++k) before[k] = bpk_opstats[k];
 #endif
         sim_exact(B, c, S);
         if (getenv("BPEMU_DUMP_SIM") && cls >= SIM_EXACT) {
@@ -506,7 +506,7 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
         }
 #ifdef BPK_OPSTATS
         if (cls < SIM_EXACT)   // count the exact-class candidates' Rat work only
-            for (int k = 0; k < 16; ++k) bpk_opstats[k] = before[k];
+            for (int k = 0; k < 32; ++k) bpk_opstats[k] = before[k];
 #endif
         if (cls == SIM_EXACT) {
             ++exact_n;
@@ -524,7 +524,7 @@ extern "C" int bpemu_explore_batch(const bp_network* nets, int n_nets, const bp_
 #ifdef BPK_OPSTATS
     if (getenv("BPEMU_STATS")) {
         fprintf(stderr, "opstats after sims");
-        for (int k = 0; k < 16; ++k) fprintf(stderr, " %llu", bpk_opstats[k]);
+        for (int k = 0; k < 32; ++k) fprintf(stderr, " %llu", bpk_opstats[k]);
         fprintf(stderr, "\n");
     }
 #endif
