@@ -385,6 +385,7 @@ int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
     while (ctab < 2 * std::max<int64_t>(1, (int64_t)nms)) ctab <<= 1;
     size_t o_ckey = L.take<unsigned long long>((size_t)ctab), o_crep = L.take<int32_t>((size_t)ctab);
     size_t o_slist = L.take<int32_t>((size_t)SIM_CLASSES * nc), o_scnt = L.take<int32_t>(2 * SIM_CLASSES);   // counts, then hand-out counters
+    size_t o_ftmp = L.take<int32_t>(nc);
     const auto t3 = std::chrono::steady_clock::now();
     if (!B->mem.ensure(L.off + 256)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(batch)");
     if (timing)
@@ -478,6 +479,7 @@ int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
     D.otemp_bytes = otemp_bytes;
     D.sim_list = dptr<int32_t>(b, o_slist);
     D.sim_count = dptr<int32_t>(b, o_scnt);
+    D.flow_tmp = dptr<int32_t>(b, o_ftmp);
     D.details = details ? 1 : 0;
     // DP launch geometry: blocks resident per SM bounded by shared memory
     int max_units = std::max(1, c->hn.max_L);
@@ -565,7 +567,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     }
     phase_end(c, "phase_prune", st, ph);
     ph = phase_begin(c, st);
-    timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 2);
+    timed(c, "sim_prep", st, [&] { launch_sim_prep(D, st); }, 4);
     if (D.prune_lb) {   // BP_OPT_PRUNE_LB round 1: bounds, one seed per query
         timed(c, "lb_prune", st, [&] {
             launch_lb_bound(D, st);

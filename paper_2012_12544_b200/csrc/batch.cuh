@@ -140,6 +140,7 @@ struct BatchDev {
     size_t otemp_bytes;
     int32_t* sim_list;        // [SIM_CLASSES][ncand] candidate lists per simulator class
     int32_t* sim_count;       // [2 * SIM_CLASSES]: list lengths, then hand-out counters (k_sim_flow)
+    int32_t* flow_tmp;        // [ncand] scratch of k_flow_sort
     // exact-simulator scheduling: counting sort of its list by (N, log2 M)
     int32_t* xkey;            // [ncand]
     int32_t* xsorted;         // [ncand]

@@ -612,6 +612,36 @@ __global__ void k_lb_finish(BatchDev B) {
     }
 }
 
+// The dataflow lists in decreasing op-DAG depth (2M + 2N rounds, 16 log2
+// buckets): their blocks take candidates from a counter in list order, so the
+// heaviest start first and the phase ends on light ones (LPT).
+__global__ void __launch_bounds__(1024) k_flow_sort(BatchDev B, int cls) {
+    __shared__ int cnt[16], off[16];
+    const int n = B.sim_count[cls];
+    int32_t* list = B.sim_list + (int64_t)cls * B.ncand;
+    if (threadIdx.x < 16) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    auto key = [&](int32_t ci) {
+        const bp_candidate& c = B.cand[ci];
+        const int64_t r = 2 * c.M + 2 * (int64_t)c.n_stages;
+        const int lg = 63 - __clzll((long long)r);
+        return 15 - (lg > 15 ? 15 : lg);
+    };
+    for (int i = threadIdx.x; i < n; i += blockDim.x) atomicAdd(&cnt[key(list[i])], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int k = 0; k < 16; ++k) { off[k] = a; a += cnt[k]; }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int32_t ci = list[i];
+        B.flow_tmp[atomicAdd(&off[key(ci)], 1)] = ci;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) list[i] = B.flow_tmp[i];
+}
+
 static inline int blocks_for(int64_t n, int t) { return (int)((n + t - 1) / t); }
 
 void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
@@ -621,6 +651,8 @@ void launch_sim_prep(const BatchDev& B, cudaStream_t st) {
     if (B.ncand) {
         k_sim_classify<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
         k_sim_prep<<<blocks_for(B.ncand, 128), 128, 0, st>>>(B);
+        k_flow_sort<<<1, 1024, 0, st>>>(B, SIM_FLOW);
+        k_flow_sort<<<1, 1024, 0, st>>>(B, SIM_FLOW + 1);
     }
 }
 
