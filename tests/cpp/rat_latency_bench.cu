@@ -109,6 +109,42 @@ __global__ void kbench(long long* out, int64_t seed) {
         out[k++] = (c1 - c0) / ITERS;
         out[16] += (long long)a;
     }
+    // 11: ctz via __ffs (BREV + FLO)
+    {
+        uint32_t a = 0x1000u | (uint32_t)(seed & 0);
+        c0 = clock64();
+        for (int i = 0; i < ITERS; ++i) { int z = __ffs(a) - 1; a = (1u << ((z + 1) & 15)) | 0x10000u; }
+        c1 = clock64();
+        out[11] = (c1 - c0) / ITERS;
+        out[16] += a;
+    }
+    // 12: ctz via __popc((x & -x) - 1)
+    {
+        uint32_t a = 0x1000u | (uint32_t)(seed & 0);
+        c0 = clock64();
+        for (int i = 0; i < ITERS; ++i) { int z = __popc((a & (0u - a)) - 1); a = (1u << ((z + 1) & 15)) | 0x10000u; }
+        c1 = clock64();
+        out[12] = (c1 - c0) / ITERS;
+        out[16] += a;
+    }
+    // 13: baseline of 11/12 (the same chain with a constant shift)
+    {
+        uint32_t a = 0x1000u | (uint32_t)(seed & 0);
+        c0 = clock64();
+        for (int i = 0; i < ITERS; ++i) { int z = (int)(a & 7); a = (1u << ((z + 1) & 15)) | 0x10000u; }
+        c1 = clock64();
+        out[13] = (c1 - c0) / ITERS;
+        out[16] += a;
+    }
+    // 14: float estimate of a small quotient (I2F.S64, MUFU.RCP, F2I.S64)
+    {
+        int64_t num = ((int64_t)1 << 50) + seed, den = ((int64_t)1 << 42) + 12345;
+        c0 = clock64();
+        for (int i = 0; i < ITERS; ++i) { int64_t k = (int64_t)((float)num * __frcp_rn((float)den)); num += k & 1; }
+        c1 = clock64();
+        out[14] = (c1 - c0) / ITERS;
+        out[16] += num;
+    }
     // 10: 32-bit add chain (loop overhead + 1 op)
     {
         uint32_t a = (uint32_t)seed;
@@ -129,7 +165,8 @@ int main() {
     cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
     const char* names[] = {"rf_add_small (pow2 b)", "rf_mul_int", "stage_time_safe", "gcd_u32 pow2",
                            "gcd_u32 2^9*odd", "gcd_mod odd m", "rf_div32 odd", "rf_lt", "umod_u64_u32",
-                           "64-bit mul chain", "32-bit mad chain"};
-    for (int k = 0; k < 11; ++k) printf("%-24s %6lld cycles\n", names[k], h[k]);
+                           "64-bit mul chain", "32-bit mad chain", "ctz via ffs", "ctz via popc",
+                           "(chain baseline)", "float quotient"};
+    for (int k = 0; k < 15; ++k) printf("%-24s %6lld cycles\n", names[k], h[k]);
     return 0;
 }

@@ -54,3 +54,23 @@ print(f"  one batch: {run([np.arange(shard.queries.size)]):.2f} ms")
 for k in (1, 2, 4):
     parts = [big[np.isin(cls[big], ucls[i::k])] for i in range(k)]
     print(f"  N = {n.max()} in {k} group(s) + the rest: {run(parts + [rest]):.2f} ms")
+
+# per-kernel profile of the two split parts of this shard, each alone
+if "--profile" in sys.argv:
+    for name, g in (("N = max", big), ("rest", rest)):
+        sub = W.subset(shard, g)
+        ex = Explorer(0)
+        ex.split(False)
+        b = ex.prepare(sub)
+        ex.run(b)
+        ex.profiling(True)
+        for _ in range(3):
+            ex.run(b)
+        ex.fetch(b, sub)
+        st = ex.kernel_stats()
+        print(f"  part {name}: {sub.queries.size} queries")
+        for k, v in sorted(st.items(), key=lambda kv: -kv[1]["ms"]):
+            if v["ms"] / 3 > 0.15:
+                print(f"    {k:24s} {v['ms'] / 3:8.3f} ms")
+        ex.free(b)
+        ex.close()
