@@ -33,9 +33,10 @@ namespace {
 constexpr int FLOW_Q = 4;
 
 // Block-wide sync and OR-reduction of per-thread flags.  One warp (NT = 32):
-// a warp reduction, no barrier.  Two warps: one barrier per round on a
-// shared word, three words in rotation so that resetting the next round's
-// word never races with a slow reader of the previous one.
+// a warp reduction, no barrier.  Two warps: each warp reduces its flags
+// (REDUX) and lane 0 stores the warp's word; one barrier per round; the words
+// rotate over three rounds so that a fast warp's next store never races with
+// a slow reader of the previous round.
 template <int NT>
 __device__ __forceinline__ void flow_sync() {
     if constexpr (NT == 32) __syncwarp();
@@ -43,13 +44,14 @@ __device__ __forceinline__ void flow_sync() {
 }
 template <int NT>
 __device__ __forceinline__ unsigned flow_or(unsigned f, unsigned* red, int round) {
+    const unsigned w = __reduce_or_sync(0xffffffffu, f);
     if constexpr (NT == 32) {
-        return __reduce_or_sync(0xffffffffu, f);
+        return w;
     } else {
-        if (threadIdx.x == 0) red[(round + 1) % 3] = 0;
-        if (f) atomicOr(&red[round % 3], f);
+        unsigned* slot = red + 2 * (round % 3);
+        if ((threadIdx.x & 31) == 0) slot[threadIdx.x >> 5] = w;
         __syncthreads();
-        return red[round % 3];
+        return slot[0] | slot[1];
     }
 }
 
@@ -60,7 +62,7 @@ struct FlowSmem {
     int prodF[NT], consF[NT];
     int prodB[NT], consB[NT];
     Rat fr[NT];
-    unsigned red[3];
+    unsigned red[6];        // flow_or: two warp words per round, three rounds
     int next;               // the block's next candidate (dynamic assignment)
 };
 
@@ -112,7 +114,6 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
             w = warmup_depth(kind, N, s + 1);
             if (w > M) w = M;
         }
-        if (s < 3) sm.red[s] = 0;
         flow_sync<NT>();
         int64_t p = 0;                 // this stage's next position
         bool done = s >= N;
