@@ -92,17 +92,22 @@ struct bp_batch {
     int nq = 0;
     int dp_grid = 0, dp_max_units = 0;
     int refine_grid = 0;       // slim refine kernel: persistent grid, 0 = not used
+    int refine_warps = 1;      // its walking warps per block
     size_t refine_bytes = 0;   // its dynamic shared memory
     uint64_t gen = 0;          // bp_ctx::gen at prepare: the device tables it points at
     // this batch's own side stream and fork / join events (concurrent batches
     // of one context must not share them)
     cudaStream_t side = nullptr, lane = nullptr;
-    cudaEvent_t fork = nullptr, join = nullptr, done = nullptr;
+    cudaStream_t rstream = nullptr;   // the refine walks, at the device's greatest priority
+    cudaEvent_t fork = nullptr, join = nullptr, done = nullptr, rjoin = nullptr;
+    int prio = 0;              // priority of this batch's own streams (split parts)
     // BP_OPT_SPLIT: the batch runs as two parts on two streams (see split_prepare)
     std::vector<bp_batch*> parts;
     std::vector<std::vector<int32_t>> part_q;      // parent query index of each part query
     DevBuf part_ids;                               // device: parent query index per part query (parts concatenated)
     DevBuf part_best;                              // device: one bp_best_record per part
+    DevBuf res_all;                                // device: the parts' query results in the caller's order
+    HostPinned out_stage;                          // pinned staging of a part's candidate / stage records
     std::vector<int64_t> part_ids_host;
 };
 
@@ -189,6 +194,25 @@ void phase_end(bp_ctx* c, const char* name, cudaStream_t st, cudaEvent_t a) {
 }
 
 void collect(bp_ctx* c) {
+    refine_trace_collect();
+    // BP_TIMELINE=<file>: append every span's start / end (ms from the first
+    // span's start) -- the launch timeline of a profiled run (tests/timeline_probe.py)
+    static const char* tl = getenv("BP_TIMELINE");
+    if (tl && !c->pending.empty()) {
+        if (FILE* f = fopen(tl, "a")) {
+            cudaEvent_t base = c->pending.front().second.first;
+            cudaEventSynchronize(c->pending.back().second.second);
+            for (auto& p : c->pending) {
+                float a = 0, b = 0;
+                cudaEventSynchronize(p.second.second);
+                cudaEventElapsedTime(&a, base, p.second.first);
+                cudaEventElapsedTime(&b, base, p.second.second);
+                fprintf(f, "%s %.4f %.4f\n", p.first.c_str(), a, b);
+            }
+            fprintf(f, "--\n");
+            fclose(f);
+        }
+    }
     for (auto& p : c->pending) {
         float ms = 0;
         cudaEventSynchronize(p.second.second);
@@ -490,7 +514,8 @@ int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
     if (per_sm > 8) per_sm = 8;
     B->dp_grid = c->sm_count * per_sm;
     B->dp_max_units = max_units;
-    B->refine_grid = refine_setup(std::max(1, hb.max_N), max_units, c->max_T, &B->refine_bytes);
+    B->refine_grid = refine_setup(std::max(1, hb.max_N), max_units, c->max_T, c->smem_optin, &B->refine_bytes,
+                                  &B->refine_warps);
     return BP_OK;
 }
 
@@ -530,25 +555,37 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     // fork: coarse DPs (side stream) || refine (main stream); both only read
     // the whole-layer DP results and write disjoint state
     if (!B->side) {
-        cudaStreamCreateWithFlags(&B->side, cudaStreamNonBlocking);
-        cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
+        int least = 0, greatest = 0;
+        cudaDeviceGetStreamPriorityRange(&least, &greatest);
+        cudaStreamCreateWithPriority(&B->side, cudaStreamNonBlocking, B->prio);
+        cudaStreamCreateWithPriority(&B->rstream, cudaStreamNonBlocking, greatest);
+        if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&B->join, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&B->rjoin, cudaEventDisableTiming);
     }
     launch_prune_reset(D, st);
     cudaEvent_t ph = phase_begin(c, st);
+    // fork: refine (its own stream at the greatest priority: the walks are
+    // the step's critical path, and their blocks must reach the SMs before
+    // the coarse DPs' or another part's fill them) || the coarse DPs (side
+    // stream); both only read the whole-layer DP results and write disjoint state
     cudaEventRecord(B->fork, st);
+    cudaStreamWaitEvent(B->rstream, B->fork, 0);
     cudaStreamWaitEvent(B->side, B->fork, 0);
+    const int refine_launches = (refine_region_bytes(maxN) > 200 * 1024 || !D.dedup) ? 1 : B->refine_grid ? 3 : 2;
+    timed(c, "refine", B->rstream, [&] {
+        launch_refine(D, c->sm_count, B->refine_grid, B->refine_warps, B->refine_bytes, B->dp_max_units, T,
+                      B->rstream);
+    }, refine_launches);
+    timed(c, "dedup_copy", B->rstream, [&] { launch_dedup_copy_refine(D, B->rstream); });
+    cudaEventRecord(B->rjoin, B->rstream);
     if (hb.nmslot > 0) {
         timed(c, "minmax_dp_coarse", B->side,
               [&] { launch_partition(D, 1, B->dp_grid, B->dp_max_units, maxN, T, B->side); });
         timed(c, "dedup_copy", B->side, [&] { launch_coarse_copy(D, B->side); });
     }
     cudaEventRecord(B->join, B->side);
-    const int refine_launches = (refine_region_bytes(maxN) > 200 * 1024 || !D.dedup) ? 1 : B->refine_grid ? 3 : 2;
-    timed(c, "refine", st, [&] {
-        launch_refine(D, c->sm_count, B->refine_grid, B->refine_bytes, B->dp_max_units, T, st);
-    }, refine_launches);
-    timed(c, "dedup_copy", st, [&] { launch_dedup_copy_refine(D, st); });
+    cudaStreamWaitEvent(st, B->rjoin, 0);
     cudaStreamWaitEvent(st, B->join, 0);
     // (pruning the coarse-path candidates on the side stream while refine runs,
     // launch_prune(D, 0, side), was measured no faster overall: refine's
@@ -675,6 +712,18 @@ bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<int32_
     return (int)a.size() >= SPLIT_MIN_PART && (int)b.size() >= SPLIT_MIN_PART;
 }
 
+// A part's streams: the first part (the largest stage count: the longest
+// refine walks and simulations, the step's critical chain) at the highest
+// priority, so that its kernels take the SMs first whenever they are ready and
+// the other part's fill the gaps (its refine phase, its prune tail).
+void make_part_lane(bp_batch* p, size_t k) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    p->prio = k == 0 ? hi : lo;
+    cudaStreamCreateWithPriority(&p->lane, cudaStreamNonBlocking, p->prio);
+    cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming);
+}
+
 // eager (bp_explore_batch): each part is uploaded and launched on its own
 // stream as soon as its host build is done, so the first part's kernels (the
 // long refine walks) run while the host builds the second.  *ran tells the
@@ -717,10 +766,7 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         if (timing) fprintf(stderr, "split part %d (%zu queries): built %.2f ms, prepared %.2f ms\n", k, idx.size(), tb, since());
         for (int32_t i : idx) B->part_ids_host.push_back(i);
         if (eager) {
-            if (!p->lane) {
-                cudaStreamCreateWithFlags(&p->lane, cudaStreamNonBlocking);
-                cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming);
-            }
+            if (!p->lane) make_part_lane(p, k);
             cudaStreamWaitEvent(p->lane, B->fork, 0);
             if ((rc = upload_inputs(c, p, p->lane)) != BP_OK || (rc = run(c, p, p->lane)) != BP_OK) return rc;
             cudaEventRecord(p->done, p->lane);
@@ -773,11 +819,9 @@ int run_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     if (B->parts.empty()) return run(c, B, st);
     if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
     cudaEventRecord(B->fork, st);
-    for (bp_batch* p : B->parts) {
-        if (!p->lane) {
-            cudaStreamCreateWithFlags(&p->lane, cudaStreamNonBlocking);
-            cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming);
-        }
+    for (size_t k = 0; k < B->parts.size(); ++k) {
+        bp_batch* p = B->parts[k];
+        if (!p->lane) make_part_lane(p, k);
         cudaStreamWaitEvent(p->lane, B->fork, 0);
         if (const int rc = run(c, p, p->lane); rc != BP_OK) return rc;
         cudaEventRecord(p->done, p->lane);
@@ -788,25 +832,44 @@ int run_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
 
 int fetch_any(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_stage* stages, cudaStream_t st) {
     if (B->parts.empty()) return fetch(c, B, res, cand, stages, st);
+    // query results: scattered into the caller's order on the device (part_ids),
+    // then one D2H straight into the caller's buffer
+    if (res) {
+        const size_t bytes = (size_t)B->nq * sizeof(bp_query_result);
+        if (!B->res_all.ensure(bytes)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(split results)");
+        const int64_t* ids = (const int64_t*)B->part_ids.p;
+        for (size_t k = 0; k < B->parts.size(); ++k) {
+            launch_scatter_results(B->parts[k]->dev.res, B->parts[k]->nq, ids, (bp_query_result*)B->res_all.p, st);
+            ids += B->part_q[k].size();
+        }
+        c->launches += (int64_t)B->parts.size();
+        const cudaError_t e = cudaMemcpyAsync(res, B->res_all.p, bytes, cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return cuda_fail(c, e, "fetch");
+        c->d2h += (int64_t)bytes;
+    }
+    // candidate / stage records (details): each part's through pinned staging,
+    // scattered to the caller's layout on the host; without them each part's
+    // fetch only waits and collects its profile
     c->stats_accumulate = false;
     for (size_t k = 0; k < B->parts.size(); ++k) {
         bp_batch* p = B->parts[k];
         const HostBatch& ph = p->hb;
-        std::vector<bp_query_result> r(res ? (size_t)p->nq : 0);
-        std::vector<bp_candidate> cd(cand ? (size_t)ph.ncand : 0);
-        std::vector<bp_stage> sg(stages && p->details ? (size_t)ph.nstage : 0);
-        const int rc = fetch(c, p, res ? r.data() : nullptr, cand ? cd.data() : nullptr,
-                             sg.empty() ? nullptr : sg.data(), st);
+        const size_t cbytes = cand ? (size_t)ph.ncand * sizeof(bp_candidate) : 0;
+        const size_t sbytes = stages && p->details ? (size_t)ph.nstage * sizeof(bp_stage) : 0;
+        if (!B->out_stage.ensure(std::max<size_t>(1, cbytes + sbytes)))
+            return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(split staging)");
+        bp_candidate* cd = cbytes ? (bp_candidate*)B->out_stage.p : nullptr;
+        bp_stage* sg = sbytes ? (bp_stage*)((char*)B->out_stage.p + cbytes) : nullptr;
+        const int rc = fetch(c, p, nullptr, cd, sg, st);
         c->stats_accumulate = true;
         if (rc != BP_OK) { c->stats_accumulate = false; return rc; }
+        if (!cd && !sg) continue;
         for (int j = 0; j < p->nq; ++j) {
             const QDesc& pd = ph.q[j];
             const QDesc& wd = B->hb.q[B->part_q[k][j]];
-            if (res) res[B->part_q[k][j]] = r[j];
             const int64_t nc = 2 * (int64_t)pd.nbase;
-            if (cand) std::memcpy(cand + wd.cand_off, cd.data() + pd.cand_off, (size_t)nc * sizeof(bp_candidate));
-            if (!sg.empty())
-                std::memcpy(stages + wd.stage_off, sg.data() + pd.stage_off, (size_t)(nc * pd.N) * sizeof(bp_stage));
+            if (cd) std::memcpy(cand + wd.cand_off, cd + pd.cand_off, (size_t)nc * sizeof(bp_candidate));
+            if (sg) std::memcpy(stages + wd.stage_off, sg + pd.stage_off, (size_t)(nc * pd.N) * sizeof(bp_stage));
         }
     }
     c->stats_accumulate = false;
@@ -867,6 +930,7 @@ bp_ctx* bp_create(int device) {
         g_err = std::string("cannot set kernel attributes: ") + cudaGetErrorString(ke);
         return nullptr;
     }
+    refine_trace_collect();   // diagnostics (BP_REFINE_TRACE): allocates the trace buffer
     bp_ctx* c = new (std::nothrow) bp_ctx();
     if (!c) return nullptr;
     c->device = device;
@@ -1006,9 +1070,12 @@ void bp_batch_free(bp_ctx* c, bp_batch* B) {
     B->stage_in.release();
     B->part_ids.release();
     B->part_best.release();
+    B->res_all.release();
+    B->out_stage.release();
     if (B->side) cudaStreamDestroy(B->side);
+    if (B->rstream) cudaStreamDestroy(B->rstream);
     if (B->lane) cudaStreamDestroy(B->lane);
-    for (cudaEvent_t ev : {B->fork, B->join, B->done})
+    for (cudaEvent_t ev : {B->fork, B->join, B->done, B->rjoin})
         if (ev) cudaEventDestroy(ev);
     delete B;
 }

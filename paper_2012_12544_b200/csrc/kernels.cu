@@ -22,6 +22,9 @@
 // The simulators (K4) are in sim.cu and xwave.cu, the DP (K2) in dp.cu, the
 // one-plan timeline / estimate (F3) in timeline.cu.
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include <cub/cub.cuh>
 
@@ -333,11 +336,39 @@ __global__ void k_refine(BatchDev B) {
 // packing them into lanes only serialises them) with its plan and stage-time
 // caches in shared memory; up to 32 such warps per SM hide each other's
 // latency.
+// The list the slim kernel hands out: the refining queries, stage count
+// descending (a walk's length grows with N: its longest walks start first and
+// do not queue behind short ones), then layers descending, then query index
+// (a stable radix sort of these keys; the others sort last).
+__global__ void k_refine_keys(BatchDev B) {
+    const int qi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (qi >= B.nq) return;
+    const bool w = refine_wanted(B, qi);
+    if (w) atomicAdd(B.rcount, 1);
+    const QDesc Q = B.q[qi];
+    const uint64_t N = Q.N < 65535 ? (uint64_t)Q.N : 65535;
+    const int64_t L = B.P.nets[Q.net].L;
+    const uint64_t Lk = L < 65535 ? (uint64_t)L : 65535;
+    B.okey[qi] = w ? (((65535 - N) << 32) | ((65535 - Lk) << 16)) : ~0ull;
+    B.oval[qi] = qi;
+}
+
 __global__ void k_refine_list(BatchDev B) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= B.nq) return;
     const int qi = B.qorder[i];
     if (refine_wanted(B, qi)) B.rlist[atomicAdd(B.rcount, 1)] = qi;
+}
+
+// Diagnostics only (BP_REFINE_TRACE, tests/refine_trace_probe.py): when the
+// host sets it, lane 0 of the slim kernel appends (query, steps, start, end,
+// SM) per walk, %globaltimer nanoseconds.
+__device__ unsigned long long* g_rtrace = nullptr;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
 // The general kernel over a query list (list[ctr[0]] entries, hand-out
@@ -360,7 +391,19 @@ __global__ void __launch_bounds__(32) k_refine_smem(BatchDev B, int nm, const in
     // finishes early takes the next query instead of a fixed stride's
     for (int i = atomicAdd(&ctr[1], 1); i < count; i = atomicAdd(&ctr[1], 1)) {
         const int qi = list[i];
+        const unsigned long long t_start = g_rtrace ? gtimer() : 0;
         refine_query_at(B, qi, &sc);
+        if (g_rtrace) {   // the general kernel's walks: SM id + 65536
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            const unsigned long long k = atomicAdd(g_rtrace, 1ull);
+            unsigned long long* r = g_rtrace + 1 + 5 * k;
+            r[0] = (unsigned long long)qi;
+            r[1] = (unsigned long long)B.qs[qi].refine_evals;
+            r[2] = t_start;
+            r[3] = gtimer();
+            r[4] = smid + 65536;
+        }
         atomicAdd(&B.work[WORK_REFINE], (unsigned long long)B.qs[qi].refine_evals);
         atomicMax(&B.work[WORK_REFINE_MAX], (unsigned long long)B.qs[qi].refine_evals);
         atomicAdd(&B.work[WORK_REFINE_MOVES], (unsigned long long)B.qs[qi].refine_moves);
@@ -468,8 +511,10 @@ __device__ void refine_tail_warp(const BatchDev& B, int qi, const int32_t* lo, c
     }
 }
 
-__global__ void __launch_bounds__(32) k_refine_fast(BatchDev B, int mN, int mL, int mT) {
-    extern __shared__ __align__(16) unsigned char fsm[];
+__global__ void __launch_bounds__(256) k_refine_fast(BatchDev B, int mN, int mL, int mT, int stride) {
+    extern __shared__ __align__(16) unsigned char fsm_all[];
+    // each warp walks its own queries in its own shared-memory region
+    unsigned char* fsm = fsm_all + (size_t)(threadIdx.x >> 5) * stride;
     const FastLayout f = fast_layout(mN, mL, mT);
     Rat* t = reinterpret_cast<Rat*>(fsm + f.t);
     Rat* lead = reinterpret_cast<Rat*>(fsm + f.lead);
@@ -480,7 +525,7 @@ __global__ void __launch_bounds__(32) k_refine_fast(BatchDev B, int mN, int mL, 
     uint8_t* memo = fsm + f.memo;
     int32_t* cost = reinterpret_cast<int32_t*>(fsm + f.cost);
     int32_t* act = reinterpret_cast<int32_t*>(fsm + f.act);
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     const int count = B.rcount[0];
     for (;;) {
         int i = 0;
@@ -488,6 +533,7 @@ __global__ void __launch_bounds__(32) k_refine_fast(BatchDev B, int mN, int mL, 
         i = __shfl_sync(0xffffffffu, i, 0);
         if (i >= count) break;
         const int qi = B.rlist[i];
+        const unsigned long long t_start = g_rtrace ? gtimer() : 0;
         const QDesc Q = B.q[qi];
         const NetView v = net_view(B.P, Q.net);
         const ChainView c = chain_view(B.P, Q.cl, Q.N);
@@ -539,9 +585,49 @@ __global__ void __launch_bounds__(32) k_refine_fast(BatchDev B, int mN, int mL, 
             atomicAdd(&B.work[WORK_REFINE], (unsigned long long)st[1]);
             atomicMax(&B.work[WORK_REFINE_MAX], (unsigned long long)st[1]);
             atomicAdd(&B.work[WORK_REFINE_MOVES], (unsigned long long)st[2]);
+            if (g_rtrace) {
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                const unsigned long long k = atomicAdd(g_rtrace, 1ull);
+                unsigned long long* r = g_rtrace + 1 + 5 * k;
+                r[0] = (unsigned long long)qi;
+                r[1] = (unsigned long long)st[1];
+                r[2] = t_start;
+                r[3] = gtimer();
+                r[4] = smid;
+            }
         }
         __syncwarp();
     }
+}
+
+// BP_REFINE_TRACE=<file>: the walk records of the runs since the last call,
+// appended to <file> (one "query steps start_ns end_ns sm" line each), then
+// the buffer is reset.  First call allocates (room for 2^20 walks).
+void refine_trace_collect() {
+    static const char* path = getenv("BP_REFINE_TRACE");
+    if (!path) return;
+    static unsigned long long* buf = nullptr;
+    const size_t cap = 1 << 20;
+    if (!buf) {
+        if (cudaMalloc(&buf, (1 + 5 * cap) * sizeof(unsigned long long)) != cudaSuccess) return;
+        cudaMemset(buf, 0, sizeof(unsigned long long));
+        cudaMemcpyToSymbol(g_rtrace, &buf, sizeof(buf));
+        return;
+    }
+    cudaDeviceSynchronize();
+    unsigned long long n = 0;
+    cudaMemcpy(&n, buf, sizeof(n), cudaMemcpyDeviceToHost);
+    if (n > cap) n = cap;
+    std::vector<unsigned long long> h(5 * n);
+    if (n) cudaMemcpy(h.data(), buf + 1, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+    if (FILE* f = fopen(path, "a")) {
+        for (size_t k = 0; k < n; ++k)
+            fprintf(f, "%llu %llu %llu %llu %llu\n", h[5 * k], h[5 * k + 1], h[5 * k + 2], h[5 * k + 3], h[5 * k + 4]);
+        fprintf(f, "--\n");
+        fclose(f);
+    }
+    cudaMemset(buf, 0, sizeof(unsigned long long));
 }
 
 // ---- batch-level sharing of the first estimate (cost_models.hpp:124-166).
@@ -918,8 +1004,8 @@ size_t refine_fast_bytes(int max_N, int max_L, int max_T) { return fast_layout(m
 // slim kernel first (refine_fast.cuh), the general one on the queries it
 // hands back (rlist[nq ...], rcount[2]); fast_grid / fast_bytes: 0 = no slim
 // kernel (tables too large for shared memory)
-void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes, int max_L, int max_T,
-                   cudaStream_t st) {
+void launch_refine(const BatchDev& B, int sms, int fast_grid, int fast_warps, size_t fast_bytes, int max_L,
+                   int max_T, cudaStream_t st) {
     if (!B.nq) return;
     const size_t bytes = refine_region_bytes(B.max_N);
     // very long chains, or no dedup (tens of thousands of queries to refine:
@@ -929,9 +1015,16 @@ void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes,
         return;
     }
     cudaMemsetAsync(B.rcount, 0, 4 * sizeof(int32_t), st);
-    k_refine_list<<<blocks(B.nq, 128), 128, 0, st>>>(B);
     if (fast_grid > 0) {
-        k_refine_fast<<<fast_grid, 32, fast_bytes, st>>>(B, B.max_N, max_L, max_T);
+        k_refine_keys<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+        size_t tb = B.otemp_bytes;
+        cub::DeviceRadixSort::SortPairs(B.otemp, tb, B.okey, B.okey2, B.oval, B.rlist, B.nq, 16, 48, st);
+    } else {
+        k_refine_list<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    }
+    if (fast_grid > 0) {
+        const int stride = (int)((refine_fast_bytes(B.max_N, max_L, max_T) + 127) & ~(size_t)127);
+        k_refine_fast<<<fast_grid, 32 * fast_warps, fast_bytes, st>>>(B, B.max_N, max_L, max_T, stride);
         k_refine_smem<<<sms * 8, 32, bytes, st>>>(B, B.max_N, B.rlist + B.nq, B.rcount + 2);
     } else {
         k_refine_smem<<<sms * 32, 32, bytes, st>>>(B, B.max_N, B.rlist, B.rcount);
@@ -941,15 +1034,33 @@ void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes,
 // launch geometry of the slim refine kernel for a batch (0: not used, its
 // tables do not fit in shared memory); the dynamic shared memory attribute is
 // set once per device (kernel_attributes_init)
-int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes) {
+int refine_setup(int max_N, int max_L, int max_T, size_t optin, size_t* fast_bytes, int* fast_warps) {
     const size_t fb = refine_fast_bytes(max_N, max_L, max_T);
     *fast_bytes = 0;
+    *fast_warps = 1;
     if (fb > 96 * 1024) return 0;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static const int excl = getenv("BP_REFINE_SMS") ? atoi(getenv("BP_REFINE_SMS")) : 0;
+    static const int ew = getenv("BP_REFINE_WARPS") ? atoi(getenv("BP_REFINE_WARPS")) : 8;
+    if (excl > 0) {
+        // exclusive SMs: blocks of several walking warps that take an SM's
+        // whole shared memory, so no other kernel's block shares their SMs
+        cudaFuncAttributes a;
+        cudaFuncGetAttributes(&a, k_refine_fast);
+        const size_t stride = (fb + 127) & ~(size_t)127;
+        const size_t dyn = optin - a.sharedSizeBytes;
+        int w = (int)std::min<size_t>((size_t)std::max(1, std::min(ew, 8)), dyn / stride);
+        if (w < 1) return 0;
+        *fast_warps = w;
+        *fast_bytes = dyn;
+        return std::min(excl, sms);
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_fast, 32, fb);
     if (per_sm <= 0) return 0;
+    static const int cap = getenv("BP_REFINE_PER_SM") ? atoi(getenv("BP_REFINE_PER_SM")) : 0;
+    if (cap > 0 && per_sm > cap) per_sm = cap;
     *fast_bytes = fb;
     return sms * per_sm;
 }
@@ -1012,6 +1123,17 @@ void launch_plan_finish(const BatchDev& B, cudaStream_t st) {
 void launch_rank(const BatchDev& B, cudaStream_t st) {
     if (B.nq) k_rank<<<blocks(B.nq, 128), 128, 0, st>>>(B);
 }
+// a split batch's part results into the caller's query order (ids: the
+// parent query index of each part query)
+__global__ void k_scatter_results(const bp_query_result* src, int n, const int64_t* ids, bp_query_result* dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) dst[ids[i]] = src[i];
+}
+void launch_scatter_results(const bp_query_result* src, int n, const int64_t* ids, bp_query_result* dst,
+                            cudaStream_t st) {
+    if (n > 0) k_scatter_results<<<blocks(n, 128), 128, 0, st>>>(src, n, ids, dst);
+}
+
 __global__ void k_best_merge(const bp_best_record* recs, int n, bp_best_record* out) {
     bp_best_record b = recs[0];
     for (int k = 1; k < n; ++k)

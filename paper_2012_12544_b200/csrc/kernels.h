@@ -20,9 +20,9 @@ void launch_dedup(const BatchDev& B, cudaStream_t st);
 void launch_coarse_copy(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_dp(const BatchDev& B, cudaStream_t st);
 void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
-void launch_refine(const BatchDev& B, int sms, int fast_grid, size_t fast_bytes, int max_L, int max_T,
+void launch_refine(const BatchDev& B, int sms, int fast_grid, int fast_warps, size_t fast_bytes, int max_L, int max_T,
                    cudaStream_t st);
-int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes);
+int refine_setup(int max_N, int max_L, int max_T, size_t optin, size_t* fast_bytes, int* fast_warps);
 cudaError_t kernel_attributes_init(int optin_bytes);
 cudaError_t partition_attributes_init(int optin_bytes);
 size_t refine_region_bytes(int max_N);
@@ -48,6 +48,9 @@ cudaError_t timeline_simulate(const Pools& P, int clusterN, const bp_plan_reques
                               int64_t* h2d, int64_t* d2h);
 cudaError_t timeline_estimate(const Pools& P, int clusterN, const bp_plan_request& q, bp_estimate_result* res,
                               bp_stage* stages, int32_t* infeasible, int64_t* h2d, int64_t* d2h);
+void refine_trace_collect();
+void launch_scatter_results(const bp_query_result* src, int n, const int64_t* ids, bp_query_result* dst,
+                            cudaStream_t st);   // diagnostics: BP_REFINE_TRACE (kernels.cu)
 void launch_best_merge(const bp_best_record* recs, int n, bp_best_record* out, cudaStream_t st);
 void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,
                  cudaStream_t st);

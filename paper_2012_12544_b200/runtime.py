@@ -48,10 +48,12 @@ class Explorer:
         self._keep = (nets, cls)
         self._loaded = p
 
-    def explore(self, p: Problem, details=True, stream=None):
-        """explore() for every query of p: host buffers in, host buffers out."""
+    def explore(self, p: Problem, details=True, stream=None, out=None):
+        """explore() for every query of p: host buffers in, host buffers out.
+        out: (res, cand, st) from p.alloc_outputs (e.g. pinned, reused across
+        calls) instead of fresh arrays."""
         self.load(p)
-        res, cand, st = p.alloc_outputs(details)
+        res, cand, st = out if out is not None else p.alloc_outputs(details)
         rc = self.lib.bp_explore_batch(self.ctx, p.c_queries(), p.queries.size,
                                        res.ctypes.data_as(C.POINTER(abi.bp_query_result)),
                                        None if cand is None else cand.ctypes.data_as(C.POINTER(abi.bp_candidate)),
