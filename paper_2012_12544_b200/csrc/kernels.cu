@@ -772,8 +772,20 @@ __global__ void k_prune(BatchDev B, int pass) {
         if (base >= count) break;
         if (base + lane < count) {
             const int64_t ci = B.plist[base + lane];
+            const unsigned long long t_start = g_rtrace ? gtimer() : 0;
             prune_candidate(B, ci, pass);
             count_prune(B, ci);
+            if (g_rtrace && B.cs[ci].ft_trials >= 4) {   // diagnostics: prune chains (SM id + 131072)
+                unsigned smid;
+                asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+                const unsigned long long k = atomicAdd(g_rtrace, 1ull);
+                unsigned long long* r = g_rtrace + 1 + 5 * k;
+                r[0] = (unsigned long long)ci;
+                r[1] = (unsigned long long)B.cs[ci].ft_trials * (unsigned long long)B.cand[ci].n_stages;
+                r[2] = t_start;
+                r[3] = gtimer();
+                r[4] = smid + 131072;
+            }
         }
     }
 }

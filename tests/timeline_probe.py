@@ -61,6 +61,14 @@ for line in open(trace):
     walks.append((t1 - t0, q, steps, t0, t1, sm))
 if walks:
     base = min(w[3] for w in walks)
+    prunes = [w for w in walks if w[5] >= 131072]
+    walks = [w for w in walks if w[5] < 131072]
+    if prunes:
+        pb = min(w[3] for w in prunes)
+        print(f"{len(prunes)} pruned candidates with >= 4 fine-tune trials; the longest (ms from the first one's start):")
+        for d, q, work, t0, t1, sm in sorted(prunes, reverse=True)[:8]:
+            print(f"  candidate {q:8d} trials x stages {work:6d} start {(t0 - pb) / 1e6:6.3f} end {(t1 - pb) / 1e6:6.3f} "
+                  f"dur {d / 1e6:6.3f} ms")
     gen = [w for w in walks if w[5] >= 65536]
     print(f"{len(walks) - len(gen)} slim refine walks, {len(gen)} in the general kernel "
           f"(its last ends at {max((w[4] for w in gen), default=base) / 1e6 - base / 1e6:.3f} ms, "
