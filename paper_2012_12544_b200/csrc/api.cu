@@ -99,6 +99,11 @@ struct bp_batch {
     // of one context must not share them)
     cudaStream_t side = nullptr, lane = nullptr;
     cudaStream_t rstream = nullptr;   // the refine walks, at the device's greatest priority
+    cudaGraphExec_t gexec = nullptr;  // run_graph: the captured kernel sequence
+    std::vector<char> gkey;           // ... and the launch inputs it was captured with
+    int64_t glaunches = 0;            // own kernels per replay
+    bool graph_failed = false;
+    cudaEvent_t gfork = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr, done = nullptr, rjoin = nullptr;
     int prio = 0;              // priority of this batch's own streams (split parts)
     // BP_OPT_SPLIT: the batch runs as two parts on two streams (see split_prepare)
@@ -526,12 +531,28 @@ int upload_inputs(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     return BP_OK;
 }
 
-int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
-    BatchDev& D = B->dev;
-    const HostBatch& hb = B->hb;
+// the batch's own side and refine streams and their fork / join events
+void ensure_streams(bp_batch* B) {
+    if (B->side) return;
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&B->side, cudaStreamNonBlocking, B->prio);
+    cudaStreamCreateWithPriority(&B->rstream, cudaStreamNonBlocking, greatest);
+    if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&B->join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&B->rjoin, cudaEventDisableTiming);
+}
+
+void set_run_flags(bp_ctx* c, BatchDev& D) {
     D.dedup = c->dedup ? 1 : 0;
     D.plan_only = c->plan_only ? 1 : 0;
     D.prune_lb = c->prune_lb && !c->plan_only ? 1 : 0;
+}
+
+int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
+    BatchDev& D = B->dev;
+    const HostBatch& hb = B->hb;
+    set_run_flags(c, D);
     cudaError_t e;
     e = cudaMemsetAsync(D.cand, 0, (size_t)hb.ncand * sizeof(bp_candidate), st);
     if (e == cudaSuccess && D.stages) e = cudaMemsetAsync(D.stages, 0, (size_t)hb.nstage * sizeof(bp_stage), st);
@@ -554,15 +575,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "bottleneck", st, [&] { launch_bottleneck(D, st); }, 2);
     // fork: coarse DPs (side stream) || refine (main stream); both only read
     // the whole-layer DP results and write disjoint state
-    if (!B->side) {
-        int least = 0, greatest = 0;
-        cudaDeviceGetStreamPriorityRange(&least, &greatest);
-        cudaStreamCreateWithPriority(&B->side, cudaStreamNonBlocking, B->prio);
-        cudaStreamCreateWithPriority(&B->rstream, cudaStreamNonBlocking, greatest);
-        if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&B->join, cudaEventDisableTiming);
-        cudaEventCreateWithFlags(&B->rjoin, cudaEventDisableTiming);
-    }
+    ensure_streams(B);
     launch_prune_reset(D, st);
     cudaEvent_t ph = phase_begin(c, st);
     // fork: refine (its own stream at the greatest priority: the walks are
@@ -634,6 +647,84 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "rank", st, [&] { launch_rank(D, st); });
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(c, e, "kernel launch");
+    return BP_OK;
+}
+
+// A batch's kernel sequence as a CUDA graph: captured on the first run (on
+// the batch's own lane stream, with its side and refine streams forked and
+// joined inside), replayed by every later run whose launch inputs are the
+// same -- the device tables and arena (BatchDev, by value in every kernel
+// node), and the host-side sizes run() decides launches on.  One graph launch
+// replaces ~45 kernel launches: the parts of a split batch start together,
+// and bp_explore_batch's second part is not held back by the first part's
+// launch calls.  Profiling runs launch kernel by kernel (events per launch).
+struct GraphKey {
+    BatchDev dev;
+    int64_t whole_items, nmslot;
+    int refine_grid, refine_warps, dp_grid, dp_max_units, max_T, sm_count;
+    size_t refine_bytes;
+};
+
+GraphKey graph_key(bp_ctx* c, bp_batch* B) {
+    GraphKey k;
+    std::memset(&k, 0, sizeof(k));
+    std::memcpy(&k.dev, &B->dev, sizeof(BatchDev));
+    k.whole_items = (int64_t)B->hb.whole_items.size();
+    k.nmslot = B->hb.nmslot;
+    k.refine_grid = B->refine_grid;
+    k.refine_warps = B->refine_warps;
+    k.refine_bytes = B->refine_bytes;
+    k.dp_grid = B->dp_grid;
+    k.dp_max_units = B->dp_max_units;
+    k.max_T = c->max_T;
+    k.sm_count = c->sm_count;
+    return k;
+}
+
+int run_graph(bp_ctx* c, bp_batch* B, cudaStream_t st) {
+    static const bool off = getenv("BP_NO_GRAPHS") != nullptr;
+    if (c->prof || off || B->graph_failed) return run(c, B, st);
+    set_run_flags(c, B->dev);
+    ensure_streams(B);
+    if (!B->lane) {
+        cudaStreamCreateWithPriority(&B->lane, cudaStreamNonBlocking, B->prio);
+        cudaEventCreateWithFlags(&B->done, cudaEventDisableTiming);
+    }
+    if (!B->gfork) cudaEventCreateWithFlags(&B->gfork, cudaEventDisableTiming);
+    cudaStream_t lane = B->lane;
+    const GraphKey key = graph_key(c, B);
+    if (!B->gexec || std::memcmp(&key, B->gkey.data(), sizeof(key)) != 0) {
+        if (B->gexec) cudaGraphExecDestroy(B->gexec);
+        B->gexec = nullptr;
+        const int64_t l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamBeginCapture(lane, cudaStreamCaptureModeThreadLocal);
+        int rc = e == cudaSuccess ? run(c, B, lane) : BP_CUDA_ERROR;
+        const cudaError_t e2 = e == cudaSuccess ? cudaStreamEndCapture(lane, &g) : e;
+        if (rc != BP_OK || e2 != cudaSuccess || cudaGraphInstantiate(&B->gexec, g, 0) != cudaSuccess) {
+            if (g) cudaGraphDestroy(g);
+            B->gexec = nullptr;
+            cudaGetLastError();
+            c->launches = l0;
+            B->graph_failed = true;   // launch this batch kernel by kernel from now on
+            return run(c, B, st);
+        }
+        cudaGraphDestroy(g);
+        B->glaunches = c->launches - l0;
+        c->launches = l0;
+        B->gkey.assign((const char*)&key, (const char*)&key + sizeof(key));
+    }
+    if (st != lane) {
+        cudaEventRecord(B->gfork, st);
+        cudaStreamWaitEvent(lane, B->gfork, 0);
+    }
+    cudaError_t e = cudaGraphLaunch(B->gexec, lane);
+    if (e != cudaSuccess) return cuda_fail(c, e, "graph launch");
+    c->launches += B->glaunches;
+    if (st != lane) {
+        cudaEventRecord(B->done, lane);
+        cudaStreamWaitEvent(st, B->done, 0);
+    }
     return BP_OK;
 }
 
@@ -768,7 +859,7 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         if (eager) {
             if (!p->lane) make_part_lane(p, k);
             cudaStreamWaitEvent(p->lane, B->fork, 0);
-            if ((rc = upload_inputs(c, p, p->lane)) != BP_OK || (rc = run(c, p, p->lane)) != BP_OK) return rc;
+            if ((rc = upload_inputs(c, p, p->lane)) != BP_OK || (rc = run_graph(c, p, p->lane)) != BP_OK) return rc;
             cudaEventRecord(p->done, p->lane);
             cudaStreamWaitEvent(st, p->done, 0);
             if (timing) fprintf(stderr, "split part %d launched %.2f ms\n", k, since());
@@ -816,14 +907,14 @@ int upload_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
 }
 
 int run_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
-    if (B->parts.empty()) return run(c, B, st);
+    if (B->parts.empty()) return run_graph(c, B, st);
     if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
     cudaEventRecord(B->fork, st);
     for (size_t k = 0; k < B->parts.size(); ++k) {
         bp_batch* p = B->parts[k];
         if (!p->lane) make_part_lane(p, k);
         cudaStreamWaitEvent(p->lane, B->fork, 0);
-        if (const int rc = run(c, p, p->lane); rc != BP_OK) return rc;
+        if (const int rc = run_graph(c, p, p->lane); rc != BP_OK) return rc;
         cudaEventRecord(p->done, p->lane);
         cudaStreamWaitEvent(st, p->done, 0);
     }
@@ -1075,7 +1166,8 @@ void bp_batch_free(bp_ctx* c, bp_batch* B) {
     if (B->side) cudaStreamDestroy(B->side);
     if (B->rstream) cudaStreamDestroy(B->rstream);
     if (B->lane) cudaStreamDestroy(B->lane);
-    for (cudaEvent_t ev : {B->fork, B->join, B->done, B->rjoin})
+    if (B->gexec) cudaGraphExecDestroy(B->gexec);
+    for (cudaEvent_t ev : {B->fork, B->join, B->done, B->rjoin, B->gfork})
         if (ev) cudaEventDestroy(ev);
     delete B;
 }
