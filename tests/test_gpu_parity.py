@@ -161,3 +161,34 @@ def test_plan_only_matches_explore(ex):
                     continue
                 assert f["status"] == g["status"] and f["detail"] == g["detail"], (qi, i, f, g)
         assert n_ok > 0
+
+
+def test_graph_replay_equals_launch_by_launch(ex):
+    """A prepared batch runs as a CUDA graph (captured on its first run,
+    replayed after); a profiled run launches kernel by kernel.  Same records,
+    same own-kernel count, on a split-size C5 sample (two parts) and on a
+    small batch; and a replay after the inputs changed (same sizes: the graph
+    is reused) gives the new inputs' results."""
+    for p in (W.subset(W.config_c5(models=8), np.arange(4096)), scenarios.c5_sample(257)):
+        b = ex.prepare(p, details=True)
+        outs, counts = [], []
+        for prof in (False, False, True):
+            ex.profiling(prof)
+            n0 = ex.launches()
+            ex.run(b)
+            counts.append(ex.launches() - n0)
+            outs.append(ex.fetch(b, p, details=True))
+        ex.profiling(False)
+        ex.free(b)
+        assert counts[0] == counts[1] == counts[2]
+        for o in outs[1:]:
+            for x, y, part in zip(outs[0], o, ("res", "cand", "stages")):
+                assert_same(x, y, "graph replay " + part)
+    # same sizes, other queries: 8 models' worth of the sweep, two different model ranges
+    a = W.config_c5(models=8)
+    z = W.config_c5(models=8, model_base=40)
+    want = ex.explore(z, details=False)[0]
+    got_a = ex.explore(a, details=False)[0]
+    got_z = ex.explore(z, details=False)[0]
+    assert got_z.tobytes() == want.tobytes()
+    assert got_a.tobytes() != got_z.tobytes()
