@@ -578,6 +578,8 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     ensure_streams(B);
     launch_prune_reset(D, st);
     cudaEvent_t ph = phase_begin(c, st);
+    const bool general_refine = refine_region_bytes(maxN) > 200 * 1024 || !D.dedup;
+    timed(c, "refine_list", st, [&] { launch_refine_list(D, B->refine_grid, st); }, general_refine ? 0 : 1);
     // fork: refine (its own stream at the greatest priority: the walks are
     // the step's critical path, and their blocks must reach the SMs before
     // the coarse DPs' or another part's fill them) || the coarse DPs (side
@@ -585,7 +587,7 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     cudaEventRecord(B->fork, st);
     cudaStreamWaitEvent(B->rstream, B->fork, 0);
     cudaStreamWaitEvent(B->side, B->fork, 0);
-    const int refine_launches = (refine_region_bytes(maxN) > 200 * 1024 || !D.dedup) ? 1 : B->refine_grid ? 3 : 2;
+    const int refine_launches = general_refine || !B->refine_grid ? 1 : 2;
     timed(c, "refine", B->rstream, [&] {
         launch_refine(D, c->sm_count, B->refine_grid, B->refine_warps, B->refine_bytes, B->dp_max_units, T,
                       B->rstream);
@@ -602,7 +604,8 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     cudaStreamWaitEvent(st, B->join, 0);
     // (pruning the coarse-path candidates on the side stream while refine runs,
     // launch_prune(D, 0, side), was measured no faster overall: refine's
-    // single-lane walks slow down by as much as the overlap saves)
+    // single-lane walks slow down by as much as the overlap saves; running
+    // the coarse DPs before refine instead of beside it was ~1 ms slower)
     phase_end(c, "phase_refine", st, ph);   // coarse DP beside refine, up to the join
     ph = phase_begin(c, st);
     timed(c, "prune_list", st, [&] { launch_prune(D, -1, st, 1); }, 2);

@@ -336,6 +336,17 @@ __global__ void k_refine(BatchDev B) {
 // packing them into lanes only serialises them) with its plan and stage-time
 // caches in shared memory; up to 32 such warps per SM hide each other's
 // latency.
+// Diagnostics only (BP_REFINE_TRACE, tests/refine_trace_probe.py): when the
+// host sets it, lane 0 of the slim kernel appends (query, steps, start, end,
+// SM) per walk, %globaltimer nanoseconds.
+__device__ unsigned long long* g_rtrace = nullptr;
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // The list the slim kernel hands out: the refining queries, stage count
 // descending (a walk's length grows with N: its longest walks start first and
 // do not queue behind short ones), then layers descending, then query index
@@ -343,6 +354,13 @@ __global__ void k_refine(BatchDev B) {
 __global__ void k_refine_keys(BatchDev B) {
     const int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi >= B.nq) return;
+    if (qi == 0 && g_rtrace) {   // diagnostics: the refine launch sequence starts (tag 262144)
+        const unsigned long long k = atomicAdd(g_rtrace, 1ull);
+        unsigned long long* r = g_rtrace + 1 + 5 * k;
+        r[0] = r[1] = 0;
+        r[2] = r[3] = gtimer();
+        r[4] = 262144;
+    }
     const bool w = refine_wanted(B, qi);
     if (w) atomicAdd(B.rcount, 1);
     const QDesc Q = B.q[qi];
@@ -358,17 +376,6 @@ __global__ void k_refine_list(BatchDev B) {
     if (i >= B.nq) return;
     const int qi = B.qorder[i];
     if (refine_wanted(B, qi)) B.rlist[atomicAdd(B.rcount, 1)] = qi;
-}
-
-// Diagnostics only (BP_REFINE_TRACE, tests/refine_trace_probe.py): when the
-// host sets it, lane 0 of the slim kernel appends (query, steps, start, end,
-// SM) per walk, %globaltimer nanoseconds.
-__device__ unsigned long long* g_rtrace = nullptr;
-
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
 }
 
 // The general kernel over a query list (list[ctr[0]] entries, hand-out
@@ -1016,16 +1023,12 @@ size_t refine_fast_bytes(int max_N, int max_L, int max_T) { return fast_layout(m
 // slim kernel first (refine_fast.cuh), the general one on the queries it
 // hands back (rlist[nq ...], rcount[2]); fast_grid / fast_bytes: 0 = no slim
 // kernel (tables too large for shared memory)
-void launch_refine(const BatchDev& B, int sms, int fast_grid, int fast_warps, size_t fast_bytes, int max_L,
-                   int max_T, cudaStream_t st) {
-    if (!B.nq) return;
-    const size_t bytes = refine_region_bytes(B.max_N);
-    // very long chains, or no dedup (tens of thousands of queries to refine:
-    // the packed global-memory version keeps more of them in flight)
-    if (bytes > 200 * 1024 || !B.dedup) {
-        k_refine<<<blocks(B.nq, 64), 64, 0, st>>>(B);
-        return;
-    }
+// the refine list (before the fork: the slim kernel is then the first work of
+// the refine stream, and its blocks are placed before the coarse DPs')
+bool refine_general_only(const BatchDev& B) { return refine_region_bytes(B.max_N) > 200 * 1024 || !B.dedup; }
+
+void launch_refine_list(const BatchDev& B, int fast_grid, cudaStream_t st) {
+    if (!B.nq || refine_general_only(B)) return;
     cudaMemsetAsync(B.rcount, 0, 4 * sizeof(int32_t), st);
     if (fast_grid > 0) {
         k_refine_keys<<<blocks(B.nq, 128), 128, 0, st>>>(B);
@@ -1033,6 +1036,18 @@ void launch_refine(const BatchDev& B, int sms, int fast_grid, int fast_warps, si
         cub::DeviceRadixSort::SortPairs(B.otemp, tb, B.okey, B.okey2, B.oval, B.rlist, B.nq, 16, 48, st);
     } else {
         k_refine_list<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+    }
+}
+
+void launch_refine(const BatchDev& B, int sms, int fast_grid, int fast_warps, size_t fast_bytes, int max_L,
+                   int max_T, cudaStream_t st) {
+    if (!B.nq) return;
+    const size_t bytes = refine_region_bytes(B.max_N);
+    // very long chains, or no dedup (tens of thousands of queries to refine:
+    // the packed global-memory version keeps more of them in flight)
+    if (refine_general_only(B)) {
+        k_refine<<<blocks(B.nq, 64), 64, 0, st>>>(B);
+        return;
     }
     if (fast_grid > 0) {
         const int stride = (int)((refine_fast_bytes(B.max_N, max_L, max_T) + 127) & ~(size_t)127);

@@ -61,8 +61,14 @@ for line in open(trace):
     walks.append((t1 - t0, q, steps, t0, t1, sm))
 if walks:
     base = min(w[3] for w in walks)
-    prunes = [w for w in walks if w[5] >= 131072]
+    starts = sorted(w[3] for w in walks if w[5] >= 262144)
+    prunes = [w for w in walks if 131072 <= w[5] < 262144]
     walks = [w for w in walks if w[5] < 131072]
+    for k, t in enumerate(starts):   # per refine launch sequence (one per part)
+        mine = [w for w in walks if w[3] >= t and (k + 1 == len(starts) or w[3] < starts[k + 1])]
+        if mine:
+            print(f"refine sequence {k}: first walk starts {(min(w[3] for w in mine) - t) / 1e6:.3f} ms after "
+                  f"k_refine_keys, last walk ends {(max(w[4] for w in mine) - t) / 1e6:.3f} ms after it")
     if prunes:
         pb = min(w[3] for w in prunes)
         print(f"{len(prunes)} pruned candidates with >= 4 fine-tune trials; the longest (ms from the first one's start):")
