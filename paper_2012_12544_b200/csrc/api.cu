@@ -6,6 +6,7 @@
 // There is no CPU fallback: without a usable device, bp_create returns NULL.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -786,10 +787,10 @@ int fetch(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, bp_s
 // layout at fetch.
 constexpr int SPLIT_MIN_QUERIES = 4096, SPLIT_MIN_PART = 512;
 
-bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<int32_t>& a, std::vector<int32_t>& b) {
+bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<std::vector<int32_t>>& groups) {
+    groups.clear();
     if (!c->split || c->plan_only || nq < SPLIT_MIN_QUERIES) return false;
-    std::vector<int32_t> n(nq);
-    int maxN = 0;
+    std::vector<int> n(nq);
     for (int i = 0; i < nq; ++i) {
         // a query the host build would reject: no split, so that the one-batch
         // path reports it with its own index
@@ -798,22 +799,49 @@ bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<int32_
             q[i].n_stages > c->hc.desc[q[i].cluster].N || (q[i].n_m > 0 && !q[i].m_list))
             return false;
         n[i] = q[i].n_stages > 0 ? q[i].n_stages : c->hc.desc[q[i].cluster].N;
-        maxN = std::max(maxN, n[i]);
     }
-    a.clear();
-    b.clear();
-    for (int i = 0; i < nq; ++i) (n[i] == maxN ? a : b).push_back(i);
-    return (int)a.size() >= SPLIT_MIN_PART && (int)b.size() >= SPLIT_MIN_PART;
+    // parts by stage count, largest first: the largest N, then (three parts)
+    // the next largest, then the rest; a part too small to pay is merged into
+    // the rest
+    static const int want = getenv("BP_SPLIT_PARTS") ? std::max(2, std::min(3, atoi(getenv("BP_SPLIT_PARTS")))) : 2;
+    std::vector<int> levels;   // the stage counts that get their own part
+    {
+        std::vector<int> sorted(n);
+        std::sort(sorted.begin(), sorted.end(), std::greater<int>());
+        sorted.erase(std::unique(sorted.begin(), sorted.end()), sorted.end());
+        for (int v : sorted) {
+            if ((int)levels.size() + 1 >= want) break;
+            const int cnt = (int)std::count(n.begin(), n.end(), v);
+            if (cnt < SPLIT_MIN_PART) break;
+            levels.push_back(v);
+        }
+    }
+    if (levels.empty()) return false;
+    groups.assign(levels.size() + 1, {});
+    for (int i = 0; i < nq; ++i) {
+        size_t k = 0;
+        while (k < levels.size() && n[i] != levels[k]) ++k;
+        groups[k].push_back(i);
+    }
+    while (groups.size() > 1 && (int)groups.back().size() < SPLIT_MIN_PART) {
+        // the rest is too small: fold it into the last level's part
+        std::vector<int32_t> r = std::move(groups.back());
+        groups.pop_back();
+        if (groups.size() == 1) return false;
+        groups.back().insert(groups.back().end(), r.begin(), r.end());
+        std::sort(groups.back().begin(), groups.back().end());
+    }
+    return groups.size() >= 2;
 }
 
 // A part's streams: the first part (the largest stage count: the longest
 // refine walks and simulations, the step's critical chain) at the highest
 // priority, so that its kernels take the SMs first whenever they are ready and
 // the other part's fill the gaps (its refine phase, its prune tail).
-void make_part_lane(bp_batch* p, size_t k) {
+void make_part_lane(bp_batch* p, size_t k, size_t nparts) {
     int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    p->prio = k == 0 ? hi : lo;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);   // lo = least (0), hi = greatest (negative)
+    p->prio = nparts <= 1 ? hi : hi + (int)((int64_t)(lo - hi) * (int64_t)k / (int64_t)(nparts - 1));
     cudaStreamCreateWithPriority(&p->lane, cudaStreamNonBlocking, p->prio);
     cudaEventCreateWithFlags(&p->done, cudaEventDisableTiming);
 }
@@ -825,8 +853,8 @@ void make_part_lane(bp_batch* p, size_t k) {
 int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, cudaStream_t st,
                 bool eager = false, bool* ran = nullptr) {
     if (ran) *ran = false;
-    std::vector<int32_t> ga, gb;
-    if (!split_groups(c, q, nq, ga, gb)) {
+    std::vector<std::vector<int32_t>> groups;
+    if (!split_groups(c, q, nq, groups)) {
         for (bp_batch* p : B->parts) bp_batch_free(c, p);
         B->parts.clear();
         return prepare(c, B, q, nq, details, st);
@@ -835,8 +863,12 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
     B->nq = nq;
     B->gen = c->gen;
     B->details = details != 0;
-    while (B->parts.size() < 2) B->parts.push_back(new bp_batch());
-    B->part_q = {std::move(ga), std::move(gb)};
+    while (B->parts.size() > groups.size()) {
+        bp_batch_free(c, B->parts.back());
+        B->parts.pop_back();
+    }
+    while (B->parts.size() < groups.size()) B->parts.push_back(new bp_batch());
+    B->part_q = std::move(groups);
     B->part_ids_host.clear();
     if (eager) {
         if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
@@ -847,7 +879,7 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
     static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
     const auto t0 = std::chrono::steady_clock::now();
     auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
-    for (int k = 0; k < 2; ++k) {
+    for (size_t k = 0; k < B->parts.size(); ++k) {
         // the part's host build, on its own queries (its own dense layout)
         const std::vector<int32_t>& idx = B->part_q[k];
         in.resize(idx.size());
@@ -857,15 +889,15 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         const double tb = since();
         int rc = prepare_built(c, p, (int)idx.size(), details, st);
         if (rc != BP_OK) return rc;
-        if (timing) fprintf(stderr, "split part %d (%zu queries): built %.2f ms, prepared %.2f ms\n", k, idx.size(), tb, since());
+        if (timing) fprintf(stderr, "split part %zu (%zu queries): built %.2f ms, prepared %.2f ms\n", k, idx.size(), tb, since());
         for (int32_t i : idx) B->part_ids_host.push_back(i);
         if (eager) {
-            if (!p->lane) make_part_lane(p, k);
+            if (!p->lane) make_part_lane(p, k, B->parts.size());
             cudaStreamWaitEvent(p->lane, B->fork, 0);
             if ((rc = upload_inputs(c, p, p->lane)) != BP_OK || (rc = run_graph(c, p, p->lane)) != BP_OK) return rc;
             cudaEventRecord(p->done, p->lane);
             cudaStreamWaitEvent(st, p->done, 0);
-            if (timing) fprintf(stderr, "split part %d launched %.2f ms\n", k, since());
+            if (timing) fprintf(stderr, "split part %zu launched %.2f ms\n", k, since());
         }
     }
     // the whole batch's layout, in the caller's query order, from the parts'
@@ -873,7 +905,7 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
     // the parts' records to them
     HostBatch& hb = B->hb;
     hb.q.resize(nq);
-    for (int k = 0; k < 2; ++k)
+    for (size_t k = 0; k < B->parts.size(); ++k)
         for (size_t j = 0; j < B->part_q[k].size(); ++j) hb.q[B->part_q[k][j]] = B->parts[k]->hb.q[j];
     hb.ncand = hb.nstage = 0;
     for (int i = 0; i < nq; ++i) {
@@ -886,7 +918,7 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
             return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
     }
     const size_t idb = B->part_ids_host.size() * sizeof(int64_t);
-    if (!B->part_ids.ensure(idb) || !B->part_best.ensure(2 * sizeof(bp_best_record)) || !B->stage_in.ensure(idb))
+    if (!B->part_ids.ensure(idb) || !B->part_best.ensure(B->parts.size() * sizeof(bp_best_record)) || !B->stage_in.ensure(idb))
         return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(split)");
     std::memcpy(B->stage_in.p, B->part_ids_host.data(), idb);
     B->in_bytes = idb;   // upload_any copies them with the parts' inputs
@@ -915,7 +947,7 @@ int run_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     cudaEventRecord(B->fork, st);
     for (size_t k = 0; k < B->parts.size(); ++k) {
         bp_batch* p = B->parts[k];
-        if (!p->lane) make_part_lane(p, k);
+        if (!p->lane) make_part_lane(p, k, B->parts.size());
         cudaStreamWaitEvent(p->lane, B->fork, 0);
         if (const int rc = run_graph(c, p, p->lane); rc != BP_OK) return rc;
         cudaEventRecord(p->done, p->lane);

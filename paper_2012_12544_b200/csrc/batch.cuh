@@ -88,7 +88,12 @@ struct CState {
     int32_t mem0_buf;      // 0: that memory is in sMem (estimate was feasible), 1: in sMem0
     int64_t lb;            // BP_OPT_PRUNE_LB: makespan lower bound * D (scaled-integer class), -1 = none
     int32_t lbstate;       // LB_* below
-    int32_t pad;
+    // a simulated candidate's outcome before its link busy fractions (the
+    // only part of an asynchronous simulation that depends on the links):
+    // 1 = the events and feature high-water fit (sim_mk is the makespan),
+    // 2 = one of them overflowed; 0 = not simulated
+    int32_t sim_core;
+    Rat sim_mk;
 };
 
 // BP_OPT_PRUNE_LB states of a simulation representative: simulated normally,

@@ -490,7 +490,7 @@ BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S_in) {
     // a register copy: through the reference every access reloaded the
     // seven base pointers from local memory (the Rat calls may alias them)
     const SimState S = S_in;
-    const CState& cs = B.cs[ci];
+    CState& cs = B.cs[ci];
     bp_candidate& cd = B.cand[ci];
     const int qi = B.cq[ci];
     const QDesc Q = B.q[qi];
@@ -578,7 +578,7 @@ BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S_in) {
             cv = ov;
         }
     }
-    if (e.bad()) { fail(cd, e); return; }
+    if (e.bad()) { cs.sim_core = 2; fail(cd, e); return; }
     Rat mk{0, 1};
     for (int s = 0; s < N; ++s)
         if (rat_gt(S.f(s), mk)) mk = S.f(s);
@@ -589,6 +589,8 @@ BPK_HDNI void sim_exact(const BatchDev& B, int64_t ci, const SimState& S_in) {
         if (w > M) w = M;
         if ((i128)w * S.act(s) > (i128)INT64_MAX) { e.set(ERR_OVERFLOW); break; }
     }
+    cs.sim_core = e.bad() ? 2 : 1;   // shared with asynchronous members (sim_copy)
+    cs.sim_mk = mk;
     // link busy fraction Rat(M * SR) / makespan (239-244)
     for (int k = 0; k + 1 < N && !e.bad(); ++k)
         if (!rat_eq(mk, Rat{0, 1})) (void)rat_div(R(M * S.sr(k)), mk, e);

@@ -53,7 +53,11 @@ __device__ uint64_t sim_hash(const BatchDev& B, int64_t ci) {
     mix((uint64_t)cs.plan_kind * 8 + (uint64_t)cd.kind);
     mix((uint64_t)cd.M);
     mix((uint64_t)cd.micro);
-    for (int k = 0; k + 1 < Q.N; ++k) mix((uint64_t)c.bw[k]);
+    // an asynchronous schedule has no transfer ops (simulator.hpp:111-117):
+    // its events do not depend on the links, only its busy fractions do
+    // (recomputed per candidate when the outcome is shared, sim_copy)
+    if (!kind_async(cd.kind))
+        for (int k = 0; k + 1 < Q.N; ++k) mix((uint64_t)c.bw[k]);
     if (cs.plan_kind != PLAN_REFINED) {
         const int64_t slot = Q.stage_off + (ci - Q.cand_off) * Q.N;
         for (int s = 0; s < Q.N; ++s) mix(((uint64_t)(uint32_t)B.clo[slot + s] << 32) | (uint32_t)B.chi[slot + s]);
@@ -70,8 +74,9 @@ __device__ bool same_sim(const BatchDev& B, int64_t a, int64_t b) {
         return false;
     const QDesc A = B.q[qa], Q = B.q[qb];   // same class: same network, N and stage types
     const ChainView ca = chain_view(B.P, A.cl, A.N), cb = chain_view(B.P, Q.cl, Q.N);
-    for (int k = 0; k + 1 < A.N; ++k)
-        if (ca.bw[k] != cb.bw[k]) return false;
+    if (!kind_async(x.kind))
+        for (int k = 0; k + 1 < A.N; ++k)
+            if (ca.bw[k] != cb.bw[k]) return false;
     if (cx.plan_kind != PLAN_REFINED) {
         const int64_t sa = A.stage_off + (a - A.cand_off) * A.N, sb = Q.stage_off + (b - Q.cand_off) * Q.N;
         for (int s = 0; s < A.N; ++s)
@@ -109,15 +114,53 @@ __global__ void k_sim_classify(BatchDev B) {
 
 // simulated candidates whose inputs equal an earlier candidate's copy its
 // outcome after the simulators ran
+// A member's outcome from its representative's simulation.  Synchronous
+// kinds share only with identical links: the record is copied.  An
+// asynchronous member may differ from its representative in the links: it
+// takes the representative's events outcome (sim_core, sim_mk) and forms its
+// own link busy fractions Rat(M * SR) / makespan (simulator.hpp:239-244).
+__device__ void sim_copy(const BatchDev& B, int64_t ci, int64_t r) {
+    bp_candidate& cd = B.cand[ci];
+    if (!kind_async(cd.kind)) {
+        cd.status = B.cand[r].status;
+        cd.makespan = B.cand[r].makespan;
+        return;
+    }
+    const CState& rs = B.cs[r];
+    if (rs.sim_core != 1) {   // the shared events (or high-water) overflowed
+        cd.status = BP_C_ERR_OVERFLOW;
+        return;
+    }
+    const Rat mk = rs.sim_mk;
+    const CState& cs = B.cs[ci];
+    const QDesc Q = B.q[B.cq[ci]];
+    const int N = Q.N;
+    const NetView v = net_view(B.P, Q.net);
+    const ChainView c = chain_view(B.P, Q.cl, N);
+    const int32_t* hi = cs.plan_kind == PLAN_REFINED ? B.qhi + Q.qstage_off
+                                                     : B.chi + Q.stage_off + (ci - Q.cand_off) * N;
+    Err e{ERR_NONE};
+    for (int k = 0; k + 1 < N && !e.bad(); ++k) {
+        if (mk.n == 0) break;
+        const int64_t a = v.a[hi[k] - 1] * cd.micro;
+        const int64_t sr = a == 0 ? 0 : ceil_div64(a, c.bw[k]);
+        (void)rat_div(R(cd.M * sr), mk, e);
+    }
+    if (e.bad()) {
+        cd.status = BP_C_ERR_OVERFLOW;
+    } else {
+        cd.makespan = bp_rat{mk.n, mk.d};
+        cd.status = BP_C_OK;
+    }
+}
+
 __global__ void k_sim_share(BatchDev B) {
     int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (ci >= B.ncand) return;
     const int32_t r = B.cs[ci].sim_rep;
     if (r < 0) return;
     if (B.prune_lb && B.cs[r].lbstate == LB_DEFERRED) return;   // not simulated (yet)
-    bp_candidate& cd = B.cand[ci];
-    cd.status = B.cand[r].status;
-    cd.makespan = B.cand[r].makespan;
+    sim_copy(B, ci, r);
 }
 
 __global__ void k_sim_prep(BatchDev B) {
@@ -134,6 +177,10 @@ __global__ void k_sim_prep(BatchDev B) {
             const int32_t r = B.srep[slot];
             if (B.dedup && r != ci && same_sim(B, ci, r)) {
                 B.cs[ci].sim_rep = r;
+                // an asynchronous member may classify apart from its
+                // representative (its link term in the bound differs): it
+                // follows the representative's class (BP_OPT_PRUNE_LB rounds)
+                B.cs[ci].sim_cls = B.cs[r].sim_cls;
                 cls = -1;
             }
         }
@@ -453,6 +500,16 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
             if (!has[i]) continue;
             // feature high-water: min(M, depth) * a (219-238)
             if ((i128)wv[i] * A[i] > (i128)INT64_MAX) e.set(ERR_OVERFLOW);
+        }
+    }
+    // the events and high-water (shared with asynchronous members), then this
+    // candidate's own link busy fractions
+    const unsigned core_bad = __ballot_sync(FULL, e.bad());
+    if (active) {
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            const int s = r * S + i;
+            if (!has[i]) continue;
             // busy fraction Rat(M * SR) / makespan (239-244)
             if (s + 1 < N && mk.n != 0) (void)rat_div(R(M * (SRout[i] / D)), mk, e);
         }
@@ -461,6 +518,8 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
     if (active && r == 0) {
         bp_candidate& cd = B.cand[ci];
         const unsigned gm = G == 32 ? FULL : ((1u << (G & 31)) - 1u) << (lane - r);
+        B.cs[ci].sim_core = (core_bad & gm) ? 2 : 1;
+        B.cs[ci].sim_mk = mk;
         if (bad & gm) {
             cd.status = BP_C_ERR_OVERFLOW;
         } else {
@@ -607,8 +666,7 @@ __global__ void k_lb_finish(BatchDev B) {
         cd.status = BP_C_PRUNED_LB;
         cd.makespan = bp_rat{0, 0};
     } else if (cs.sim_rep >= 0 && cd.status == C_PENDING) {
-        cd.status = B.cand[r].status;
-        cd.makespan = B.cand[r].makespan;
+        sim_copy(B, ci, r);
     }
 }
 

@@ -174,15 +174,17 @@ __global__ void __launch_bounds__(NT) k_sim_flow(BatchDev B, int cls) {
         Rat mk{0, 1};
         for (int t = 0; t < N; ++t)
             if (rat_gt(sm.fr[t], mk)) mk = sm.fr[t];
-        if (!aborted && s < N) {
-            // feature high-water: min(M, depth) * a (219-238)
-            if ((i128)w * act > (i128)INT64_MAX) e.set(ERR_OVERFLOW);
-            // link busy fraction Rat(M * SR) / makespan (239-244)
-            if (s + 1 < N && mk.n != 0) (void)rat_div(R(M * srlink), mk, e);
-        }
-        // every thread left the loop in the same round: the next word is clean
-        const bool bad = flow_or<NT>((aborted || e.bad()) ? 1u : 0u, sm.red, round + 1) != 0;
+        // feature high-water: min(M, depth) * a (219-238)
+        if (!aborted && s < N && (i128)w * act > (i128)INT64_MAX) e.set(ERR_OVERFLOW);
+        // (every thread left the loop in the same round: the next words are clean)
+        const bool core_bad = flow_or<NT>((aborted || e.bad()) ? 1u : 0u, sm.red, round + 1) != 0;
+        // link busy fraction Rat(M * SR) / makespan (239-244): this
+        // candidate's own (asynchronous members sharing the events form theirs)
+        if (!core_bad && s + 1 < N && mk.n != 0) (void)rat_div(R(M * srlink), mk, e);
+        const bool bad = core_bad || flow_or<NT>(e.bad() ? 1u : 0u, sm.red, round + 2) != 0;
         if (s == 0) {
+            B.cs[ci].sim_core = core_bad ? 2 : 1;
+            B.cs[ci].sim_mk = mk;
             bp_candidate& out = B.cand[ci];
             if (bad) {
                 out.status = BP_C_ERR_OVERFLOW;
