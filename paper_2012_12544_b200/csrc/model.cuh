@@ -495,6 +495,11 @@ BPK_HD int fine_tune_int(const NetView& v, const ChainView& c, int kind, int64_t
     const int64_t fmul = (kind == KIND_FBP || kind == KIND_SO) ? 2 : 1;
     WholePlan wp{&v, &c, lo, hi};
     int guard = 0, trials = 0;
+    // a trial changes stages i0, i1 only: its total overload is the current
+    // one with their two terms replaced (exact: every value is an integer
+    // below 2^61, ft_int_ok); the worst stage and the bottleneck test are
+    // formed over all stages only for a trial whose total improves
+    auto over = [&](int i, int64_t mem) { return mem > c.cap[i] ? mem - c.cap[i] : (int64_t)0; };
     while (total > 0) {
         if (++guard > limit) { o.trials = trials; return FT_NOCONV; }
         int cn[2], cd[2], nc = 0;
@@ -527,14 +532,18 @@ BPK_HD int fine_tune_int(const NetView& v, const ChainView& c, int kind, int64_t
                     s.Mem[i] = R((int64_t)(N - i) * s.A[i] * fmul + 2 * s.W[i].n);
                 }
                 ++trials;
-                int64_t tot = 0, wo = 0;
-                int wi = 0;
-                for (int i = 0; i < N; ++i) {                  // overloads (partition.hpp:344-356, 381-383)
-                    const int64_t ov = s.Mem[i].n > c.cap[i] ? s.Mem[i].n - c.cap[i] : 0;
-                    tot += ov;
-                    if (i == 0 || ov > wo) { wo = ov; wi = i; }
-                }
+                // overloads (partition.hpp:344-356, 381-383)
+                const int64_t tot = total - over(i0, kM[0].n) - over(i1, kM[1].n) + over(i0, s.Mem[i0].n) +
+                                    over(i1, s.Mem[i1].n);
                 bool ok = tot < total;
+                int wi = 0;
+                if (ok) {
+                    int64_t wo = 0;
+                    for (int i = 0; i < N; ++i) {
+                        const int64_t ov = over(i, s.Mem[i].n);
+                        if (i == 0 || ov > wo) { wo = ov; wi = i; }
+                    }
+                }
                 if (ok && !relax) {
                     int64_t target = 0;                         // max_stage_compute_time
                     for (int n = 0; n < N; ++n) {
