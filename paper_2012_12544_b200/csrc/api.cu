@@ -427,7 +427,14 @@ int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
     // stage the inputs in pinned memory and copy once
     if (!B->stage_in.ensure(in_end)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc");
     char* h = (char*)B->stage_in.p;
-    std::memcpy(h + o_q, hb.q.data(), nqs * sizeof(QDesc));
+    {   // in chunks on the host pool (the records were just written by its workers)
+        const size_t CH = 8192;
+        const QDesc* src = hb.q.data();
+        host_parallel_for((int)((nqs + CH - 1) / CH), [&](int k) {
+            const size_t a = (size_t)k * CH, n = std::min(CH, nqs - a);
+            std::memcpy(h + o_q + a * sizeof(QDesc), src + a, n * sizeof(QDesc));
+        });
+    }
     if (!hb.Mpool.empty()) std::memcpy(h + o_M, hb.Mpool.data(), hb.Mpool.size() * 8);
     int32_t cnt[4] = {0, 0, 0, 0};   // [0] is set by k_sched_scatter, [1] by k_coarse_queue
     std::memcpy(h + o_cnt, cnt, sizeof(cnt));
@@ -875,17 +882,17 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         cudaEventRecord(B->fork, st);
     }
     std::string err;
-    std::vector<bp_query> in;
     static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
     const auto t0 = std::chrono::steady_clock::now();
     auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
     for (size_t k = 0; k < B->parts.size(); ++k) {
         // the part's host build, on its own queries (its own dense layout)
         const std::vector<int32_t>& idx = B->part_q[k];
-        in.resize(idx.size());
-        for (size_t j = 0; j < idx.size(); ++j) in[j] = q[idx[j]];
+        const int32_t* ix = idx.data();
         bp_batch* p = B->parts[k];
-        if (!build_batch(in.data(), (int)in.size(), c->hn, c->hc, p->hb, err)) return fail(c, BP_BAD_INPUT, err);
+        if (!build_batch_at([q, ix](int j) -> const bp_query& { return q[ix[j]]; }, (int)idx.size(), c->hn, c->hc,
+                            p->hb, err))
+            return fail(c, BP_BAD_INPUT, err);
         const double tb = since();
         int rc = prepare_built(c, p, (int)idx.size(), details, st);
         if (rc != BP_OK) return rc;

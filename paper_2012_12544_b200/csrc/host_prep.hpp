@@ -12,7 +12,10 @@
 #pragma once
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -41,21 +44,74 @@ struct HostCls {
 };
 
 // Run f(i) for i in [0, n) on up to 8 host threads (serially when n is small).
+// A persistent pool of host worker threads (created on first use, never
+// destroyed): host_parallel_for hands out the indices [0, n) to the workers
+// and the calling thread.  Dispatch is a condition-variable wake-up (tens of
+// microseconds), not a thread creation per call.
+class HostPool {
+  public:
+    static HostPool& get() {
+        static HostPool* p = new HostPool();   // leaked on purpose: no teardown order at exit
+        return *p;
+    }
+    int workers() const { return (int)th_.size(); }
+    template <class F>
+    void run(int n, F& f) {
+        std::lock_guard<std::mutex> call(call_);   // one parallel region at a time
+        std::atomic<int> next{0};
+        auto body = [&] {
+            for (int i; (i = next.fetch_add(1)) < n;) f(i);
+        };
+        {
+            std::lock_guard<std::mutex> l(m_);
+            job_ = body;
+            busy_ = (int)th_.size();
+            ++gen_;
+        }
+        cv_.notify_all();
+        body();
+        std::unique_lock<std::mutex> l(m_);
+        done_.wait(l, [&] { return busy_ == 0; });
+        job_ = nullptr;
+    }
+
+  private:
+    HostPool() {
+        const int hw = (int)std::thread::hardware_concurrency();
+        const int n = std::max(0, std::min(7, hw - 1));
+        for (int t = 0; t < n; ++t)
+            th_.emplace_back([this] {
+                uint64_t seen = 0;
+                for (;;) {
+                    std::function<void()> job;
+                    {
+                        std::unique_lock<std::mutex> l(m_);
+                        cv_.wait(l, [&] { return gen_ != seen; });
+                        seen = gen_;
+                        job = job_;
+                    }
+                    if (job) job();
+                    std::lock_guard<std::mutex> l(m_);
+                    if (--busy_ == 0) done_.notify_one();
+                }
+            });
+        for (auto& t : th_) t.detach();
+    }
+    std::vector<std::thread> th_;
+    std::mutex m_, call_;
+    std::condition_variable cv_, done_;
+    std::function<void()> job_;
+    uint64_t gen_ = 0;
+    int busy_ = 0;
+};
+
 template <class F>
 inline void host_parallel_for(int n, F&& f) {
-    const int hw = (int)std::thread::hardware_concurrency();
-    const int nt = std::min(std::min(8, hw > 0 ? hw : 1), n / 8);
-    if (nt <= 1) {
+    if (n <= 1 || HostPool::get().workers() == 0) {
         for (int i = 0; i < n; ++i) f(i);
         return;
     }
-    std::atomic<int> next{0};
-    std::vector<std::thread> pool;
-    for (int t = 0; t < nt; ++t)
-        pool.emplace_back([&] {
-            for (int i; (i = next.fetch_add(1)) < n;) f(i);
-        });
-    for (auto& th : pool) th.join();
+    HostPool::get().run(n, f);
 }
 
 // One network's tables into its slices of H (layout already in H.desc[i]):
@@ -241,42 +297,47 @@ struct HostBatch {
     int max_units = 0, max_N = 0, max_nbase = 0;
 };
 
-inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const HostCls& HC, HostBatch& HB,
-                        std::string& err) {
-    // reuse the vectors' capacity across calls (a sweep is re-prepared per step)
-    HB.q.resize(nq);
-    HB.Mpool.clear();
-    HB.whole_items.clear();
-    HB.whole_items.reserve(nq);
-    HB.ncand = HB.nstage = HB.nqstage = HB.nmslot = 0;
-    HB.max_units = HB.max_N = HB.max_nbase = 0;
+// One chunk of the batch build: queries [i0, i1) into HB.q with offsets
+// relative to the chunk and M lists in the chunk's own pool (the chunks are
+// joined by build_batch_at).
+struct BuildChunk {
+    std::vector<int64_t> mpool;
+    std::vector<DPItem> items;
+    int64_t ncand = 0, nstage = 0, nqstage = 0, nmslot = 0;
+    int max_units = 0, max_N = 0, max_nbase = 0;
+    int err_i = -1;
+    std::string err;
+};
+
+template <class QAt>
+inline void build_chunk(QAt& qat, int i0, int i1, const HostNets& HN, const HostCls& HC,
+                        const std::vector<int32_t>& first_bad_type, QDesc* qd, BuildChunk& ch) {
+    ch.mpool.clear();
+    ch.items.clear();
+    ch.ncand = ch.nstage = ch.nqstage = ch.nmslot = 0;
+    ch.max_units = ch.max_N = ch.max_nbase = 0;
+    ch.err_i = -1;
     std::unordered_map<int64_t, std::pair<int64_t, int>> divisors;   // mini -> (offset, count)
     int64_t last_mini = -1;
     std::pair<int64_t, int> last_div{0, 0};
-    // per network, the smallest type id without a profile: a chain prefix
-    // whose largest type id is below it passes validate_pair's type check
-    // at once (otherwise the per-accelerator loop decides)
-    std::vector<int32_t> first_bad_type(HN.desc.size());
-    for (size_t n = 0; n < HN.desc.size(); ++n) {
-        int32_t t = 0;
-        while (t < HN.desc[n].T && HN.type_ok[HN.desc[n].off_tflag + t]) ++t;
-        first_bad_type[n] = t;
-    }
-    for (int i = 0; i < nq; ++i) {
-        const bp_query& b = qs[i];
+    auto fail_at = [&](int i, const char* what) {
+        ch.err_i = i;
+        ch.err = "query " + std::to_string(i) + what;
+    };
+    for (int i = i0; i < i1; ++i) {
+        const bp_query& b = qat(i);
         if (b.network < 0 || b.network >= (int)HN.desc.size() || b.cluster < 0 || b.cluster >= (int)HC.desc.size()) {
-            err = "query " + std::to_string(i) + ": network/cluster index out of range";
-            return false;
+            fail_at(i, ": network/cluster index out of range");
+            return;
         }
         const NetDesc& nd = HN.desc[b.network];
         const ClDesc& cd = HC.desc[b.cluster];
         int N = b.n_stages > 0 ? b.n_stages : cd.N;
         if (N > cd.N || b.n_stages < 0) {
-            err = "query " + std::to_string(i) + ": n_stages exceeds the cluster";
-            return false;
+            fail_at(i, ": n_stages exceeds the cluster");
+            return;
         }
-        QDesc& Q = HB.q[i];
-        Q = QDesc{};
+        QDesc Q{};
         Q.net = b.network;
         Q.cl = b.cluster;
         Q.N = N;
@@ -288,13 +349,16 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
             if (t >= nd.T || !HN.type_ok[nd.off_tflag + t]) ok = false;
         }
         if (b.n_m > 0) {
-            if (!b.m_list) { err = "query " + std::to_string(i) + ": m_list is NULL"; return false; }
-            Q.m_off = (int64_t)HB.Mpool.size();
+            if (!b.m_list) {
+                fail_at(i, ": m_list is NULL");
+                return;
+            }
+            Q.m_off = (int64_t)ch.mpool.size();
             Q.nbase = b.n_m;
             for (int k = 0; k < b.n_m; ++k) {
                 int64_t m = b.m_list[k];
                 if (m < 1 || (b.mini_batch >= 1 && b.mini_batch % m != 0)) ok = false;
-                HB.Mpool.push_back(m < 1 ? 1 : m);
+                ch.mpool.push_back(m < 1 ? 1 : m);
             }
         } else if (b.mini_batch >= 1 && b.mini_batch == last_mini) {   // sweeps repeat one mini-batch size
             Q.m_off = last_div.first;
@@ -302,15 +366,15 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
         } else if (b.mini_batch >= 1) {
             auto it = divisors.find(b.mini_batch);
             if (it == divisors.end()) {
-                int64_t off = (int64_t)HB.Mpool.size();
+                int64_t off = (int64_t)ch.mpool.size();
                 std::vector<int64_t> small, large;
                 for (int64_t d = 1; d * d <= b.mini_batch; ++d)
                     if (b.mini_batch % d == 0) {
                         small.push_back(d);
                         if (d != b.mini_batch / d) large.push_back(b.mini_batch / d);
                     }
-                for (auto x : small) HB.Mpool.push_back(x);
-                for (auto r = large.rbegin(); r != large.rend(); ++r) HB.Mpool.push_back(*r);
+                for (auto x : small) ch.mpool.push_back(x);
+                for (auto r = large.rbegin(); r != large.rend(); ++r) ch.mpool.push_back(*r);
                 it = divisors.emplace(b.mini_batch, std::make_pair(off, (int)(small.size() + large.size()))).first;
             }
             Q.m_off = it->second.first;
@@ -319,26 +383,105 @@ inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const Ho
             last_div = it->second;
         }
         Q.schema_ok = ok ? 1 : 0;   // nbase kept: the output layout counts the slots
-        Q.cand_off = HB.ncand;
-        Q.stage_off = HB.nstage;
-        Q.qstage_off = HB.nqstage;
-        Q.mslot_off = HB.nmslot;
-        HB.ncand += 2 * (int64_t)Q.nbase;
-        HB.nstage += 2 * (int64_t)Q.nbase * N;
-        HB.nqstage += N;
-        HB.nmslot += Q.nbase;
-        HB.max_N = std::max(HB.max_N, N);
-        HB.max_nbase = std::max(HB.max_nbase, Q.nbase);
+        Q.cand_off = ch.ncand;
+        Q.stage_off = ch.nstage;
+        Q.qstage_off = ch.nqstage;
+        Q.mslot_off = ch.nmslot;
+        ch.ncand += 2 * (int64_t)Q.nbase;
+        ch.nstage += 2 * (int64_t)Q.nbase * N;
+        ch.nqstage += N;
+        ch.nmslot += Q.nbase;
+        ch.max_N = std::max(ch.max_N, N);
+        ch.max_nbase = std::max(ch.max_nbase, Q.nbase);
         if (ok && N >= 2) {
-            HB.whole_items.push_back(DPItem{i, -1, -1});
-            HB.max_units = std::max(HB.max_units, nd.L);
+            ch.items.push_back(DPItem{i, -1, -1});
+            ch.max_units = std::max(ch.max_units, nd.L);
         }
+        qd[i] = Q;
     }
+}
+
+// qat(i): the batch's i-th query (a split part reads the caller's array
+// through its index list, without a gathered copy).  Large batches are built
+// in chunks on the host pool (their QDesc writes are the cost), then joined:
+// the same records as one serial pass (offsets are prefix sums in query
+// order; the M lists live in per-chunk runs of Mpool), and the first failing
+// query's error.
+template <class QAt>
+inline bool build_batch_at(QAt&& qat, int nq, const HostNets& HN, const HostCls& HC, HostBatch& HB,
+                           std::string& err) {
+    // reuse the vectors' capacity across calls (a sweep is re-prepared per step)
+    HB.q.resize(nq);
+    // per network, the smallest type id without a profile: a chain prefix
+    // whose largest type id is below it passes validate_pair's type check
+    // at once (otherwise the per-accelerator loop decides)
+    std::vector<int32_t> first_bad_type(HN.desc.size());
+    for (size_t n = 0; n < HN.desc.size(); ++n) {
+        int32_t t = 0;
+        while (t < HN.desc[n].T && HN.type_ok[HN.desc[n].off_tflag + t]) ++t;
+        first_bad_type[n] = t;
+    }
+    constexpr int CHUNK = 8192;
+    const int nch = std::max(1, (nq + CHUNK - 1) / CHUNK);
+    // (the calling thread's chunk records, reached through a plain pointer:
+    // a thread_local named inside the lambda would be each worker's own)
+    static thread_local std::vector<BuildChunk> chunk_store;
+    if ((int)chunk_store.size() < nch) chunk_store.resize(nch);
+    BuildChunk* const chunks = chunk_store.data();
+    QDesc* qd = HB.q.data();
+    host_parallel_for(nch, [&](int k) {
+        build_chunk(qat, k * CHUNK, std::min(nq, (k + 1) * CHUNK), HN, HC, first_bad_type, qd, chunks[k]);
+    });
+    for (int k = 0; k < nch; ++k)
+        if (chunks[k].err_i >= 0) {
+            err = chunks[k].err;
+            return false;
+        }
+    // join: chunk bases, then every query's offsets
+    std::vector<int64_t> bc(nch), bs(nch), bq(nch), bm(nch), bp(nch);
+    HB.Mpool.clear();
+    HB.whole_items.clear();
+    HB.ncand = HB.nstage = HB.nqstage = HB.nmslot = 0;
+    HB.max_units = HB.max_N = HB.max_nbase = 0;
+    for (int k = 0; k < nch; ++k) {
+        const BuildChunk& ch = chunks[k];
+        bc[k] = HB.ncand;
+        bs[k] = HB.nstage;
+        bq[k] = HB.nqstage;
+        bm[k] = HB.nmslot;
+        bp[k] = (int64_t)HB.Mpool.size();
+        HB.ncand += ch.ncand;
+        HB.nstage += ch.nstage;
+        HB.nqstage += ch.nqstage;
+        HB.nmslot += ch.nmslot;
+        HB.max_units = std::max(HB.max_units, ch.max_units);
+        HB.max_N = std::max(HB.max_N, ch.max_N);
+        HB.max_nbase = std::max(HB.max_nbase, ch.max_nbase);
+        HB.Mpool.insert(HB.Mpool.end(), ch.mpool.begin(), ch.mpool.end());
+        HB.whole_items.insert(HB.whole_items.end(), ch.items.begin(), ch.items.end());
+    }
+    if (nch > 1)
+        host_parallel_for(nch - 1, [&](int k1) {
+            const int k = k1 + 1;
+            for (int i = k * CHUNK, e = std::min(nq, (k + 1) * CHUNK); i < e; ++i) {
+                QDesc& Q = qd[i];
+                Q.cand_off += bc[k];
+                Q.stage_off += bs[k];
+                Q.qstage_off += bq[k];
+                Q.mslot_off += bm[k];
+                if (Q.nbase > 0) Q.m_off += bp[k];
+            }
+        });
     // The scheduling orders (queries by stage count, layers, network and
     // chain type signature; candidates following their query; whole-layer DP
     // items heaviest first) are built on the device (kernels.cu, k_sched_*):
     // results do not depend on them.
     return true;
+}
+
+inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const HostCls& HC, HostBatch& HB,
+                        std::string& err) {
+    return build_batch_at([qs](int i) -> const bp_query& { return qs[i]; }, nq, HN, HC, HB, err);
 }
 
 }  // namespace bpk

@@ -21,20 +21,31 @@ from paper_2012_12544_b200 import workloads as W  # noqa: E402
 from paper_2012_12544_b200.runtime import Explorer  # noqa: E402
 
 split = "--no-split" not in sys.argv
+e2e = "--e2e" in sys.argv     # through explore(): tables and queries uploaded, results copied back
 p = W.config_c5()
 ex = Explorer(0)
 ex.split(split)
-b = ex.prepare(p)
 ex.profiling(True)
-for _ in range(2):
+if e2e:
+    out = p.alloc_outputs(False, pinned=True)
+    for _ in range(2):
+        ex.load(p, force=True)
+        ex.explore(p, details=False, out=out)
+    open(path, "w").close()
+    open(trace, "w").close()
+    ex.load(p, force=True)
+    ex.explore(p, details=False, out=out)
+else:
+    b = ex.prepare(p)
+    for _ in range(2):
+        ex.run(b)
+    torch.cuda.synchronize()
+    ex.fetch(b, p)              # the warm-up runs' spans and walks: discarded
+    open(path, "w").close()
+    open(trace, "w").close()
     ex.run(b)
-torch.cuda.synchronize()
-ex.fetch(b, p)              # the warm-up runs' spans and walks: discarded
-open(path, "w").close()
-open(trace, "w").close()
-ex.run(b)
-torch.cuda.synchronize()
-ex.fetch(b, p)
+    torch.cuda.synchronize()
+    ex.fetch(b, p)
 ex.profiling(False)
 rows = []
 for line in open(path):
