@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <functional>
 #include <mutex>
+#include <pthread.h>
 #include <string>
 #include <thread>
 #include <unordered_map>
@@ -51,7 +52,12 @@ struct HostCls {
 class HostPool {
   public:
     static HostPool& get() {
-        static HostPool* p = new HostPool();   // leaked on purpose: no teardown order at exit
+        // leaked on purpose (no teardown order at exit); a forked child has
+        // none of the parent's workers, so it starts a pool of its own
+        static std::once_flag once;
+        std::call_once(once, [] { pthread_atfork(nullptr, nullptr, [] { slot() = nullptr; }); });
+        HostPool*& p = slot();
+        if (!p) p = new HostPool();
         return *p;
     }
     int workers() const { return (int)th_.size(); }
@@ -76,6 +82,10 @@ class HostPool {
     }
 
   private:
+    static HostPool*& slot() {
+        static HostPool* p = nullptr;
+        return p;
+    }
     HostPool() {
         const int hw = (int)std::thread::hardware_concurrency();
         const int n = std::max(0, std::min(7, hw - 1));
