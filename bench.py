@@ -575,6 +575,27 @@ def run_b200(args):
     e2e_value = cands_per_step * args.steps / (e2e_total / 1e3)
     assert r2.tobytes() == res.tobytes(), "e2e results differ from the device-resident run"
 
+    # ---- the same, returning every candidate record too (the drop-in's whole
+    # ExplorationResult: ranked lists need them), into pinned buffers
+    outc = p.alloc_outputs("candidates", pinned=True)
+    ex.load(p, force=True)
+    ex.explore(p, details="candidates", stream=sp, out=outc)
+    torch.cuda.synchronize()
+    hc0, dc0 = ex.transfers()
+    cand_ms = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        ex.load(p, force=True)
+        r3, _, _ = ex.explore(p, details="candidates", stream=sp, out=outc)
+        cand_ms.append(1e3 * (time.perf_counter() - t))
+    hc1, dc1 = ex.transfers()
+    assert r3.tobytes() == res.tobytes(), "e2e (candidate records) results differ"
+    cand_total, _ = max_over_ranks(sum(cand_ms))
+    e2e_cand = {"value": cands_per_step * 3 / (cand_total / 1e3), "unit": UNIT, "ms_per_step": cand_total / 3,
+                "h2d_bytes_per_step": (hc1 - hc0) // 3, "d2h_bytes_per_step": (dc1 - dc0) // 3,
+                "note": "e2e with every bp_candidate record returned as well (details=candidates), 3 steps"}
+
     alone = walk_alone(ex, full, sp) if (rank == 0 and args.models == 128 and args.scaling == "strong") else None
     if rank != 0:
         if world > 1:
@@ -604,6 +625,7 @@ def run_b200(args):
                        "l2": "256 MiB buffer written between timed steps (L2 flush)"},
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_total / args.steps,
                     "h2d_bytes_per_step": (h2 - h1) // args.steps, "d2h_bytes_per_step": (d2 - d1) // args.steps},
+            "e2e_candidates": e2e_cand,
             "no_dedup": {"value": value_nodedup, "unit": UNIT, "ms_per_step": nd_ms / args.steps,
                          "note": "same steps with BP_OPT_DEDUP=0: identical subproblems of the batch not shared"},
             "lb_pruned": {"value": value_lb, "unit": UNIT, "ms_per_step": lb_ms / args.steps,

@@ -113,7 +113,8 @@ struct bp_batch {
     DevBuf part_ids;                               // device: parent query index per part query (parts concatenated)
     DevBuf part_best;                              // device: one bp_best_record per part
     DevBuf res_all;                                // device: the parts' query results in the caller's order
-    HostPinned out_stage;                          // pinned staging of a part's candidate / stage records
+    DevBuf part_woff;                              // device: (candidate, stage) offset in the caller's layout per part query
+    DevBuf cand_all, stage_all;                    // device: the parts' candidate / stage records in the caller's layout
     std::vector<int64_t> part_ids_host;
 };
 
@@ -924,14 +925,24 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         if (q[i].cand_offset != d.cand_off || q[i].stage_offset != d.stage_off)
             return fail(c, BP_BAD_INPUT, "query offsets differ from bp_layout(); call bp_layout first");
     }
-    const size_t idb = B->part_ids_host.size() * sizeof(int64_t);
-    if (!B->part_ids.ensure(idb) || !B->part_best.ensure(B->parts.size() * sizeof(bp_best_record)) || !B->stage_in.ensure(idb))
+    // per part query (parts concatenated): its parent index, then the offsets
+    // of its candidate and stage records in the caller's layout
+    const size_t npq = B->part_ids_host.size(), idb = npq * sizeof(int64_t);
+    if (!B->part_ids.ensure(idb) || !B->part_woff.ensure(2 * idb) ||
+        !B->part_best.ensure(B->parts.size() * sizeof(bp_best_record)) || !B->stage_in.ensure(3 * idb))
         return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(split)");
     std::memcpy(B->stage_in.p, B->part_ids_host.data(), idb);
-    B->in_bytes = idb;   // upload_any copies them with the parts' inputs
+    int64_t* wo = reinterpret_cast<int64_t*>(static_cast<char*>(B->stage_in.p) + idb);
+    for (size_t j = 0; j < npq; ++j) {
+        const QDesc& d = hb.q[B->part_ids_host[j]];
+        wo[2 * j] = d.cand_off;
+        wo[2 * j + 1] = d.stage_off;
+    }
+    B->in_bytes = 3 * idb;   // upload_any copies them with the parts' inputs
     if (eager) {
-        const cudaError_t e = cudaMemcpyAsync(B->part_ids.p, B->stage_in.p, idb, cudaMemcpyHostToDevice, st);
-        c->h2d += (int64_t)idb;
+        cudaError_t e = cudaMemcpyAsync(B->part_ids.p, B->stage_in.p, idb, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(B->part_woff.p, wo, 2 * idb, cudaMemcpyHostToDevice, st);
+        c->h2d += (int64_t)(3 * idb);
         if (e != cudaSuccess) return cuda_fail(c, e, "H2D split ids");
         if (ran) *ran = true;
     }
@@ -940,7 +951,10 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
 
 int upload_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     if (B->parts.empty()) return upload_inputs(c, B, st);
-    const cudaError_t e = cudaMemcpyAsync(B->part_ids.p, B->stage_in.p, B->in_bytes, cudaMemcpyHostToDevice, st);
+    const size_t idb = B->in_bytes / 3;
+    cudaError_t e = cudaMemcpyAsync(B->part_ids.p, B->stage_in.p, idb, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(B->part_woff.p, static_cast<char*>(B->stage_in.p) + idb, 2 * idb, cudaMemcpyHostToDevice, st);
     c->h2d += (int64_t)B->in_bytes;
     if (e != cudaSuccess) return cuda_fail(c, e, "H2D split ids");
     for (bp_batch* p : B->parts)
@@ -980,30 +994,36 @@ int fetch_any(bp_ctx* c, bp_batch* B, bp_query_result* res, bp_candidate* cand, 
         if (e != cudaSuccess) return cuda_fail(c, e, "fetch");
         c->d2h += (int64_t)bytes;
     }
-    // candidate / stage records (details): each part's through pinned staging,
-    // scattered to the caller's layout on the host; without them each part's
-    // fetch only waits and collects its profile
+    // candidate / stage records (details): scattered on the device into the
+    // caller's layout (part_woff), then one D2H each
+    const HostBatch& wh = B->hb;
+    const bool want_st = stages && B->details;
+    if (cand || want_st) {
+        if ((cand && !B->cand_all.ensure((size_t)wh.ncand * sizeof(bp_candidate))) ||
+            (want_st && !B->stage_all.ensure((size_t)wh.nstage * sizeof(bp_stage))))
+            return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(split records)");
+        const int64_t* wo = (const int64_t*)B->part_woff.p;
+        for (size_t k = 0; k < B->parts.size(); ++k) {
+            launch_scatter_records(B->parts[k]->dev, wo, cand ? (bp_candidate*)B->cand_all.p : nullptr,
+                                   want_st ? (bp_stage*)B->stage_all.p : nullptr, st);
+            wo += 2 * B->part_q[k].size();
+        }
+        c->launches += (int64_t)B->parts.size();
+        cudaError_t e = cudaSuccess;
+        if (cand && wh.ncand)
+            e = cudaMemcpyAsync(cand, B->cand_all.p, (size_t)wh.ncand * sizeof(bp_candidate), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && want_st && wh.nstage)
+            e = cudaMemcpyAsync(stages, B->stage_all.p, (size_t)wh.nstage * sizeof(bp_stage), cudaMemcpyDeviceToHost, st);
+        if (e != cudaSuccess) return cuda_fail(c, e, "fetch");
+        if (cand) c->d2h += wh.ncand * (int64_t)sizeof(bp_candidate);
+        if (want_st) c->d2h += wh.nstage * (int64_t)sizeof(bp_stage);
+    }
+    // each part's fetch: waits, and collects its profile
     c->stats_accumulate = false;
     for (size_t k = 0; k < B->parts.size(); ++k) {
-        bp_batch* p = B->parts[k];
-        const HostBatch& ph = p->hb;
-        const size_t cbytes = cand ? (size_t)ph.ncand * sizeof(bp_candidate) : 0;
-        const size_t sbytes = stages && p->details ? (size_t)ph.nstage * sizeof(bp_stage) : 0;
-        if (!B->out_stage.ensure(std::max<size_t>(1, cbytes + sbytes)))
-            return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(split staging)");
-        bp_candidate* cd = cbytes ? (bp_candidate*)B->out_stage.p : nullptr;
-        bp_stage* sg = sbytes ? (bp_stage*)((char*)B->out_stage.p + cbytes) : nullptr;
-        const int rc = fetch(c, p, nullptr, cd, sg, st);
+        const int rc = fetch(c, B->parts[k], nullptr, nullptr, nullptr, st);
         c->stats_accumulate = true;
         if (rc != BP_OK) { c->stats_accumulate = false; return rc; }
-        if (!cd && !sg) continue;
-        for (int j = 0; j < p->nq; ++j) {
-            const QDesc& pd = ph.q[j];
-            const QDesc& wd = B->hb.q[B->part_q[k][j]];
-            const int64_t nc = 2 * (int64_t)pd.nbase;
-            if (cd) std::memcpy(cand + wd.cand_off, cd + pd.cand_off, (size_t)nc * sizeof(bp_candidate));
-            if (sg) std::memcpy(stages + wd.stage_off, sg + pd.stage_off, (size_t)(nc * pd.N) * sizeof(bp_stage));
-        }
     }
     c->stats_accumulate = false;
     return BP_OK;
@@ -1204,7 +1224,9 @@ void bp_batch_free(bp_ctx* c, bp_batch* B) {
     B->part_ids.release();
     B->part_best.release();
     B->res_all.release();
-    B->out_stage.release();
+    B->part_woff.release();
+    B->cand_all.release();
+    B->stage_all.release();
     if (B->side) cudaStreamDestroy(B->side);
     if (B->rstream) cudaStreamDestroy(B->rstream);
     if (B->lane) cudaStreamDestroy(B->lane);

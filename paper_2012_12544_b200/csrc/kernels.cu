@@ -1161,6 +1161,24 @@ void launch_scatter_results(const bp_query_result* src, int n, const int64_t* id
     if (n > 0) k_scatter_results<<<blocks(n, 128), 128, 0, st>>>(src, n, ids, dst);
 }
 
+// a split batch's part candidate (and stage) records into the caller's
+// layout: woff[2 j], woff[2 j + 1] = the caller's candidate / stage offset of
+// part query j
+__global__ void k_scatter_records(BatchDev P, const int64_t* woff, bp_candidate* cand, bp_stage* st) {
+    const int64_t ci = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ci >= P.ncand) return;
+    const int j = P.cq[ci];
+    const QDesc Q = P.q[j];
+    const int64_t local = ci - Q.cand_off;
+    if (cand) cand[woff[2 * j] + local] = P.cand[ci];
+    if (st && P.stages)
+        for (int s = 0; s < Q.N; ++s) st[woff[2 * j + 1] + local * Q.N + s] = P.stages[Q.stage_off + local * Q.N + s];
+}
+void launch_scatter_records(const BatchDev& P, const int64_t* woff, bp_candidate* cand, bp_stage* st,
+                            cudaStream_t s) {
+    if (P.ncand > 0) k_scatter_records<<<blocks(P.ncand, 128), 128, 0, s>>>(P, woff, cand, st);
+}
+
 __global__ void k_best_merge(const bp_best_record* recs, int n, bp_best_record* out) {
     bp_best_record b = recs[0];
     for (int k = 1; k < n; ++k)

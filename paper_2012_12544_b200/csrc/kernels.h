@@ -51,7 +51,9 @@ cudaError_t timeline_estimate(const Pools& P, int clusterN, const bp_plan_reques
                               bp_stage* stages, int32_t* infeasible, int64_t* h2d, int64_t* d2h);
 void refine_trace_collect();
 void launch_scatter_results(const bp_query_result* src, int n, const int64_t* ids, bp_query_result* dst,
-                            cudaStream_t st);   // diagnostics: BP_REFINE_TRACE (kernels.cu)
+                            cudaStream_t st);
+void launch_scatter_records(const BatchDev& P, const int64_t* woff, bp_candidate* cand, bp_stage* st,
+                            cudaStream_t s);   // diagnostics: BP_REFINE_TRACE (kernels.cu)
 void launch_best_merge(const bp_best_record* recs, int n, bp_best_record* out, cudaStream_t st);
 void launch_best(const BatchDev& B, bp_best_record* out, int64_t query_base, const int64_t* query_ids,
                  cudaStream_t st);

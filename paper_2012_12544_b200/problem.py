@@ -237,12 +237,18 @@ class Problem:
         """details: True = query, candidate and stage records; "candidates" =
         query and candidate records (no per-stage plans); False = query
         records only."""
-        if pinned:
+        if pinned:   # page-locked host buffers (kept alive on the problem), for reuse across calls
             import torch
-            r = torch.empty(self.queries.size * RESULT_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
-            self._pinned_res = r
-            res = r.numpy().view(RESULT_DTYPE)
-            return res, None, None
+
+            def buf(n, dt, name):
+                t = torch.empty(max(1, n) * dt.itemsize, dtype=torch.uint8, pin_memory=True)
+                setattr(self, name, t)
+                return t.numpy().view(dt)[:n]
+            res = buf(self.queries.size, RESULT_DTYPE, "_pinned_res")
+            cand = buf(self.total_candidates, CAND_DTYPE, "_pinned_cand") if details else None
+            st = (buf(self.total_stages, STAGE_DTYPE, "_pinned_st")
+                  if details and details != "candidates" else None)
+            return res, cand, st
         res = np.zeros(self.queries.size, dtype=RESULT_DTYPE)
         cand = np.zeros(self.total_candidates, dtype=CAND_DTYPE) if details else None
         st = np.zeros(self.total_stages, dtype=STAGE_DTYPE) if details and details != "candidates" else None

@@ -44,7 +44,7 @@ def bench_name(kernel, seen):
     if k.startswith("k_sim_flow"):
         return "sim_flow" + k.split("<")[1].rstrip(">").strip()
     return {"k_refine": "refine", "k_refine_smem": "refine", "k_refine_list": "refine", "k_refine_keys": "refine", "k_refine_fast": "refine",
-            "k_scatter_results": "fetch",
+            "k_scatter_results": "fetch", "k_scatter_records": "fetch",
             "k_lb_bound": "lb_prune", "k_lb_round1": "lb_prune", "k_lb_incumbent": "lb_prune",
             "k_lb_decide": "lb_prune", "k_lb_finish": "lb_prune", "k_best_merge": "best", "k_prune": "prune",
             "k_prune_key": "prune", "k_prune_members": "prune", "k_sim_exact": "sim_exact",
