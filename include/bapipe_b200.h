@@ -272,8 +272,9 @@ enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2, BP_OPT_PRUNE_LB = 3, BP_OPT_SPLIT
  *   values); only per-candidate records of pruned candidates differ. */
 /*   BP_OPT_SPLIT (default 1): a batch of at least 4096 queries runs as two
  *   concurrent parts -- the queries with the batch's largest stage count
- *   (the longest refine walks) and the rest -- on two streams.  Results are
- *   identical either way. */
+ *   (the longest refine walks) and the rest -- on two streams.  A value
+ *   k >= 2 asks for up to k parts (the k-1 largest stage counts, then the
+ *   rest); 0 turns it off.  Results are identical either way. */
 int bp_set_option(bp_ctx* ctx, int option, int64_t value);
 
 /* ---- one plan: full-timeline simulate and estimate ----------------------

@@ -137,7 +137,7 @@ struct bp_ctx {
     bool dedup = true;       // BP_OPT_DEDUP
     bool plan_only = false;  // BP_OPT_PLAN_ONLY
     bool prune_lb = false;   // BP_OPT_PRUNE_LB
-    bool split = true;       // BP_OPT_SPLIT
+    int split = 2;           // BP_OPT_SPLIT: parts per large batch (0 = off)
     std::map<std::string, KStat> stats;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -811,7 +811,7 @@ bool split_groups(const bp_ctx* c, const bp_query* q, int nq, std::vector<std::v
     // parts by stage count, largest first: the largest N, then (three parts)
     // the next largest, then the rest; a part too small to pay is merged into
     // the rest
-    static const int want = getenv("BP_SPLIT_PARTS") ? std::max(2, std::min(3, atoi(getenv("BP_SPLIT_PARTS")))) : 2;
+    const int want = c->split;
     std::vector<int> levels;   // the stage counts that get their own part
     {
         std::vector<int> sorted(n);
@@ -1280,7 +1280,7 @@ int bp_set_option(bp_ctx* c, int option, int64_t value) {
         case BP_OPT_DEDUP: c->dedup = value != 0; return BP_OK;
         case BP_OPT_PLAN_ONLY: c->plan_only = value != 0; return BP_OK;
         case BP_OPT_PRUNE_LB: c->prune_lb = value != 0; return BP_OK;
-        case BP_OPT_SPLIT: c->split = value != 0; return BP_OK;
+        case BP_OPT_SPLIT: c->split = value <= 0 ? 0 : value == 1 ? 2 : (int)std::min<int64_t>(value, 8); return BP_OK;
         default: return fail(c, BP_BAD_INPUT, "unknown option " + std::to_string(option));
     }
 }

@@ -116,8 +116,10 @@ class Explorer:
 
     def split(self, on=True):
         """BP_OPT_SPLIT: run large batches as two concurrent parts (default
-        on; results are identical either way)."""
-        rc = self.lib.bp_set_option(self.ctx, abi.BP_OPT_SPLIT, 1 if on else 0)
+        on; an int k >= 2 asks for up to k parts; results are identical
+        either way)."""
+        value = (1 if on else 0) if isinstance(on, bool) else int(on)
+        rc = self.lib.bp_set_option(self.ctx, abi.BP_OPT_SPLIT, value)
         if rc != 0:
             raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
 
