@@ -94,6 +94,8 @@ struct CState {
     // 2 = one of them overflowed; 0 = not simulated
     int32_t sim_core;
     Rat sim_mk;
+    int32_t est_fbbal;     // prune: the first estimate's fb_balanced (asynchronous members form their heuristic)
+    int32_t pad2;
 };
 
 // BP_OPT_PRUNE_LB states of a simulation representative: simulated normally,

@@ -669,9 +669,37 @@ __device__ bool est_key_of(const BatchDev& B, int64_t ci, uint64_t& h, int32_t& 
     mix((uint64_t)cd.kind);
     mix((uint64_t)cd.M);
     mix((uint64_t)cd.micro);
-    for (int k = 0; k + 1 < Q.N; ++k) mix((uint64_t)c.bw[k]);
+    // an asynchronous kind's estimate does not read the links except for the
+    // SR part of `balanced` (cost_models.hpp:138-150): members form their
+    // own heuristic (est_heuristic)
+    if (!kind_async(cd.kind))
+        for (int k = 0; k + 1 < Q.N; ++k) mix((uint64_t)c.bw[k]);
     if (!h) h = 1;
     return true;
+}
+
+// estimate()'s heuristic flag for candidate ci on its links, given whether its
+// plan's stage F and B are all equal (cost_models.hpp:138-150): balanced also
+// needs every link's SR equal to the first link's
+// (refined: the first estimate's plan is the query's refined plan, else the
+// candidate's coarse plan in its own slot)
+__device__ int est_heuristic(const BatchDev& B, int64_t ci, int fb_balanced, bool refined) {
+    const bp_candidate& cd = B.cand[ci];
+    const QDesc Q = B.q[B.cq[ci]];
+    const int N = Q.N;
+    if (cd.M < N || !fb_balanced) return 1;
+    const NetView v = net_view(B.P, Q.net);
+    const ChainView c = chain_view(B.P, Q.cl, N);
+    const int32_t* hi = refined ? B.qhi + Q.qstage_off : B.chi + Q.stage_off + (ci - Q.cand_off) * N;
+    auto sr = [&](int k) {
+        const int64_t a = v.a[hi[k] - 1] * cd.micro;
+        return a == 0 ? (int64_t)0 : ceil_div64(a, c.bw[k]);
+    };
+    if (N < 3) return 0;
+    const int64_t s0 = sr(0);
+    for (int k = 1; k + 1 < N; ++k)
+        if (sr(k) != s0) return 1;
+    return 0;
 }
 
 __device__ bool same_est(const BatchDev& B, int64_t a, int64_t b, int32_t ca, int32_t cb) {
@@ -680,8 +708,9 @@ __device__ bool same_est(const BatchDev& B, int64_t a, int64_t b, int32_t ca, in
     if (B.qrep[qa] != B.qrep[qb] || ca != cb || x.kind != y.kind || x.M != y.M || x.micro != y.micro) return false;
     const QDesc A = B.q[qa], Q = B.q[qb];
     const ChainView xa = chain_view(B.P, A.cl, A.N), xb = chain_view(B.P, Q.cl, Q.N);
-    for (int k = 0; k + 1 < A.N; ++k)
-        if (xa.bw[k] != xb.bw[k]) return false;
+    if (!kind_async(x.kind))
+        for (int k = 0; k + 1 < A.N; ++k)
+            if (xa.bw[k] != xb.bw[k]) return false;
     return true;
 }
 
@@ -842,7 +871,7 @@ __global__ void k_prune_members(BatchDev B, int pass) {
                 for (int s = 0; s < N; ++s) B.stages[so + s] = B.stages[sr + s];
             cd.est_minibatch = rd.est_minibatch;
             cd.bubble = rd.bubble;
-            cd.heuristic = rd.heuristic;
+            cd.heuristic = kind_async(cd.kind) ? est_heuristic(B, ci, B.cs[r].est_fbbal, coarse < 0) : rd.heuristic;
             cd.peak_memory = rd.peak_memory;
             cd.max_bw_demand = rd.max_bw_demand;
             cd.plan_fractional = rd.plan_fractional;

@@ -60,6 +60,7 @@ struct EstOut {
     Rat peak_mem;       // max_i(features_i + weights_i) (explorer.hpp:405-408)
     Rat max_bw;         // max bandwidth demand (explorer.hpp:409-410)
     int trials = 0;     // memory_fine_tune trial moves (instrumentation)
+    int fb_balanced = 1;   // all stages' F equal and all B equal (heuristic's link-independent part)
 };
 
 // Optional per-stage outputs (features, weights, bw demand), may be null.
@@ -142,6 +143,7 @@ BPK_HD void estimate_body(const PS& p, const NetView& v, const ChainView& c, int
         if (rat_gt(s.B[i], Bm)) Bm = s.B[i];
         if (s.SR[i] > SRm) SRm = s.SR[i];
     }
+    const bool fb_bal = balanced;   // F and B (the SR part depends on the links)
     for (int i = 1; i < N; ++i)
         if (s.SR[i] != s.SR[N > 1 ? 1 : 0]) balanced = false;
     o.Fm = Fm;
@@ -149,6 +151,7 @@ BPK_HD void estimate_body(const PS& p, const NetView& v, const ChainView& c, int
     o.minibatch = minibatch_time(kind, M, N, Fm, Bm, R(SRm), e);
     o.bubble = bubble_fraction(kind, M, N, Fm, Bm, R(SRm), e);
     o.heuristic = (!balanced || M < N) ? 1 : 0;
+    o.fb_balanced = fb_bal ? 1 : 0;
     if (e.bad()) return;
     o.feasible = 1;
     o.peak_mem = Rat{0, 1};
@@ -250,6 +253,7 @@ BPK_HD void estimate_move_body(const WholePlan& p, const NetView& v, const Chain
         if (rat_gt(s.B[i], Bm)) Bm = s.B[i];
         if (s.SR[i] > SRm) SRm = s.SR[i];
     }
+    const bool fb_bal = balanced;   // F and B (the SR part depends on the links)
     for (int i = 1; i < N; ++i)
         if (s.SR[i] != s.SR[N > 1 ? 1 : 0]) balanced = false;
     o.Fm = Fm;
@@ -257,6 +261,7 @@ BPK_HD void estimate_move_body(const WholePlan& p, const NetView& v, const Chain
     o.minibatch = minibatch_time(kind, M, N, Fm, Bm, R(SRm), e);
     o.bubble = bubble_fraction(kind, M, N, Fm, Bm, R(SRm), e);
     o.heuristic = (!balanced || M < N) ? 1 : 0;
+    o.fb_balanced = fb_bal ? 1 : 0;
     if (e.bad()) return;
     for (int i = i0; i <= i1; ++i) {
         Rat fm = rat_mul(R(N - i), R(s.A[i]), e);
@@ -446,6 +451,7 @@ BPK_HD void estimate_whole_int(const WholePlan& p, const NetView& v, const Chain
         if (s.B[i].n > Bm) Bm = s.B[i].n;
         if (s.SR[i] > SRm) SRm = s.SR[i];
     }
+    const bool fb_bal = balanced;   // F and B (the SR part depends on the links)
     for (int i = 1; i < N; ++i)
         if (s.SR[i] != s.SR[N > 1 ? 1 : 0]) balanced = false;
     o.Fm = R(Fm);
@@ -461,6 +467,7 @@ BPK_HD void estimate_whole_int(const WholePlan& p, const NetView& v, const Chain
     else if (kind == KIND_SO) o.bubble = rat_div(R((int64_t)(N - 1) * (Fm + Bm + 2 * SRm)), R(mb), e);
     else o.bubble = rat_nd(N - 1, M + N - 1, e);
     o.heuristic = (!balanced || M < N) ? 1 : 0;
+    o.fb_balanced = fb_bal ? 1 : 0;
     if (e.bad()) return;
     o.feasible = 1;
     const int64_t fmul = (kind == KIND_FBP || kind == KIND_SO) ? 2 : 1;

@@ -282,6 +282,7 @@ BPK_HDNI void prune_candidate(const BatchDev& B, int64_t ci, int pass = -1) {
             o.feasible = 0;
         } else {
             estimate(plan, v, c, kind, M, micro, S, o, nullptr, e);
+            cs.est_fbbal = o.fb_balanced;
             if (cs.pshare && B.sMem0 && !e.bad() && !o.feasible)
                 for (int s = 0; s < N; ++s) B.sMem0[slot + s] = S.Mem[s];
         }
