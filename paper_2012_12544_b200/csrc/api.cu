@@ -898,7 +898,6 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
         int rc = prepare_built(c, p, (int)idx.size(), details, st);
         if (rc != BP_OK) return rc;
         if (timing) fprintf(stderr, "split part %zu (%zu queries): built %.2f ms, prepared %.2f ms\n", k, idx.size(), tb, since());
-        for (int32_t i : idx) B->part_ids_host.push_back(i);
         if (eager) {
             if (!p->lane) make_part_lane(p, k, B->parts.size());
             cudaStreamWaitEvent(p->lane, B->fork, 0);
@@ -908,6 +907,8 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
             if (timing) fprintf(stderr, "split part %zu launched %.2f ms\n", k, since());
         }
     }
+    for (size_t k = 0; k < B->parts.size(); ++k)
+        for (int32_t i : B->part_q[k]) B->part_ids_host.push_back(i);
     // the whole batch's layout, in the caller's query order, from the parts'
     // builds: the caller's offsets must be bp_layout's, and fetch scatters
     // the parts' records to them
