@@ -646,8 +646,10 @@ int run(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     timed(c, "sim_flow64", B->side, [&] { launch_sim_flow(D, 1, c->sm_count, B->side); });
     timed(c, "sim_exact", B->side, [&] { launch_sim_exact(D, c->sm_count, B->side); }, 4);
     cudaEventRecord(B->join, B->side);
-    for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
+    // the long dataflow kernel first, the short scaled-integer classes after
+    // it: the phase ends on short kernels (LPT over the launches)
     timed(c, "sim_flow32", st, [&] { launch_sim_flow(D, 0, c->sm_count, st); });
+    for (int k = 0; k < 8; ++k) timed(c, fast_names[k], st, [&] { launch_sim_fast(D, k, c->sm_count, st); });
     cudaStreamWaitEvent(st, B->join, 0);
     timed(c, "sim_share", st, [&] { launch_sim_share(D, st); });
     if (D.prune_lb) {   // round 2: the candidates whose bound does not exceed their query's best
