@@ -409,7 +409,7 @@ int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
     while (stab < 2 * std::max<int64_t>(1, hb.ncand)) stab <<= 1;
     size_t o_skey = L.take<unsigned long long>((size_t)stab), o_srep = L.take<int32_t>((size_t)stab);
     size_t o_rlist = L.take<int32_t>(2 * nqs), o_rcount = L.take<int32_t>(4);
-    size_t o_plist = L.take<int32_t>(nc), o_pctr = L.take<int32_t>(2);
+    size_t o_plist = L.take<int32_t>(nc), o_pctr = L.take<int32_t>(3);
     size_t o_qseed = L.take<unsigned long long>(nqs), o_qinc = L.take<bp_rat>(nqs);
     size_t o_pkey = L.take<unsigned long long>((size_t)stab), o_pbest = L.take<unsigned long long>((size_t)stab);
     int32_t ctab = 1;

@@ -174,7 +174,7 @@ struct BatchDev {
     int32_t* rlist;           // [nq] queries to refine this run (compacted)
     int32_t* rcount;          // [2] list length, next entry
     int32_t* plist;           // [ncand] candidates to prune this run (compacted)
-    int32_t* pctr;            // [2] list length, next chunk
+    int32_t* pctr;            // [3] list length, next chunk, (members' list) light entries at the back
     unsigned long long* pkey; // [pmask+1] estimate-input hashes (prune dedup)
     unsigned long long* pbest;// [pmask+1] max (capacity score, -index) per hash
     int32_t pmask;

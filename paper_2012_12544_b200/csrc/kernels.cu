@@ -798,16 +798,20 @@ __global__ void k_prune_list(BatchDev B, int pass) {
     B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;
 }
 
-__global__ void k_prune(BatchDev B, int pass) {
+// two_ended: the members' list -- pctr[0] heavy entries from the front, then
+// pctr[2] light ones from the back (k_prune_members), heavy first (LPT)
+__global__ void k_prune(BatchDev B, int pass, int two_ended) {
     const int lane = threadIdx.x & 31;
-    const int count = B.pctr[0];
+    const int heavy = B.pctr[0], light = two_ended ? B.pctr[2] : 0;
+    const int count = heavy + light;
     for (;;) {
         int base = 0;
         if (lane == 0) base = atomicAdd(&B.pctr[1], 32);
         base = __shfl_sync(0xffffffffu, base, 0);
         if (base >= count) break;
         if (base + lane < count) {
-            const int64_t ci = B.plist[base + lane];
+            const int at = base + lane;
+            const int64_t ci = at < heavy ? B.plist[at] : B.plist[B.ncand - 1 - (at - heavy)];
             const unsigned long long t_start = g_rtrace ? gtimer() : 0;
             prune_candidate(B, ci, pass);
             count_prune(B, ci);
@@ -881,7 +885,9 @@ __global__ void k_prune_members(BatchDev B, int pass) {
             return;
         }
     }
-    B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;   // pruned by the second k_prune
+    // pruned by the second k_prune: the long fine-tunes (many stages) first
+    if (B.cand[ci].n_stages >= 32) B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;
+    else B.plist[B.ncand - 1 - atomicAdd(&B.pctr[2], 1)] = (int32_t)ci;
 }
 
 // BP_OPT_PLAN_ONLY: a candidate that passed the estimate and memory check is
@@ -1166,12 +1172,12 @@ void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part) {
         cudaMemsetAsync(B.pctr, 0, 2 * sizeof(int32_t), st);
         k_prune_list<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
     }
-    if (part & 2) k_prune<<<grid, 32, 0, st>>>(B, pass);
+    if (part & 2) k_prune<<<grid, 32, 0, st>>>(B, pass, 0);
     if (part & 4) {
-        cudaMemsetAsync(B.pctr, 0, 2 * sizeof(int32_t), st);
+        cudaMemsetAsync(B.pctr, 0, 3 * sizeof(int32_t), st);
         k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
     }
-    if (part & 8) k_prune<<<grid, 32, 0, st>>>(B, -1);
+    if (part & 8) k_prune<<<grid, 32, 0, st>>>(B, -1, 1);
 }
 void launch_plan_finish(const BatchDev& B, cudaStream_t st) {
     if (B.ncand) k_plan_finish<<<blocks(B.ncand, 128), 128, 0, st>>>(B);
