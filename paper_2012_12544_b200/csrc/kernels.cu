@@ -795,11 +795,14 @@ __global__ void k_prune_list(BatchDev B, int pass) {
         int32_t coarse;
         if (est_key_of(B, ci, h, coarse) && est_rep(B, h) != ci) return;   // deferred to k_prune_members
     }
-    B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;
+    // two-ended: the candidates with 32+ stages (the long fine-tunes) first
+    if (B.cand[ci].n_stages >= 32) B.plist[atomicAdd(&B.pctr[0], 1)] = (int32_t)ci;
+    else B.plist[B.ncand - 1 - atomicAdd(&B.pctr[2], 1)] = (int32_t)ci;
 }
 
-// two_ended: the members' list -- pctr[0] heavy entries from the front, then
-// pctr[2] light ones from the back (k_prune_members), heavy first (LPT)
+// The work lists are two-ended: pctr[0] heavy entries from the front, pctr[2]
+// light ones from the back (k_prune_list, k_prune_members), handed out heavy
+// first (LPT); two_ended = 0 reads the front only
 __global__ void k_prune(BatchDev B, int pass, int two_ended) {
     const int lane = threadIdx.x & 31;
     const int heavy = B.pctr[0], light = two_ended ? B.pctr[2] : 0;
@@ -1169,10 +1172,10 @@ void launch_prune(const BatchDev& B, int pass, cudaStream_t st, int part) {
     }
     if (part & 1) {
         k_prune_key<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
-        cudaMemsetAsync(B.pctr, 0, 2 * sizeof(int32_t), st);
+        cudaMemsetAsync(B.pctr, 0, 3 * sizeof(int32_t), st);
         k_prune_list<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
     }
-    if (part & 2) k_prune<<<grid, 32, 0, st>>>(B, pass, 0);
+    if (part & 2) k_prune<<<grid, 32, 0, st>>>(B, pass, 1);
     if (part & 4) {
         cudaMemsetAsync(B.pctr, 0, 3 * sizeof(int32_t), st);
         k_prune_members<<<blocks(B.ncand, 128), 128, 0, st>>>(B, pass);
