@@ -480,6 +480,7 @@ int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
     D.xsorted = dptr<int32_t>(b, o_xsorted);
     D.xhist = dptr<int32_t>(b, o_xhist);
     D.max_N = std::max(1, hb.max_N);
+    D.max_nbase = std::max(1, hb.max_nbase);
     D.cq = dptr<int32_t>(b, o_cq);
     D.corder = dptr<int32_t>(b, o_co);
     D.dp_items = dptr<DPItem>(b, o_items);

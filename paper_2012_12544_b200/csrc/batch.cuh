@@ -153,6 +153,7 @@ struct BatchDev {
     int32_t* xsorted;         // [ncand]
     int32_t* xhist;           // [XBUCKETS] counts, then running offsets; [XBUCKETS] = chunk counter
     int max_N;                // largest stage count in the batch (exact-sim state sizing)
+    int max_nbase;            // largest M-slot count of a query (k_bottleneck's grid)
     // batch-level deduplication of the whole-layer DP + refine (kernels.cu):
     // qrep[q] = the query whose results q shares (q itself if none); NULL in
     // the host emulation (no sharing)

@@ -126,11 +126,13 @@ __device__ __forceinline__ uint64_t coarse_hash(int32_t cls, int64_t a_th) {
     return h ? h : 1;
 }
 
+// a thread per (query, M slot): blockIdx.y is the M slot (a query's link
+// loop per slot was a serial chain of 64-bit divisions before refine)
 __global__ void k_bottleneck(BatchDev B) {
     int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi >= B.nq) return;
     const QDesc Q = B.q[qi];
-    for (int m = 0; m < Q.nbase; ++m) {
+    for (int m = blockIdx.y; m < Q.nbase; m += gridDim.y) {
         MState& ms = B.ms[Q.mslot_off + m];
         ms.q = qi;
         ms.crep = -1;
@@ -148,7 +150,6 @@ __global__ void k_bottleneck(BatchDev B) {
             }
         }
     }
-    if (B.qs[qi].need_refine) atomicOr(&B.qs[B.qrep[qi]].grp_refine, 1);
 }
 
 // queue one coarse DP per distinct (class, a_th); the others share its plan
@@ -156,6 +157,7 @@ __global__ void k_coarse_queue(BatchDev B) {
     int qi = blockIdx.x * blockDim.x + threadIdx.x;
     if (qi >= B.nq) return;
     const QDesc Q = B.q[qi];
+    if (B.qs[qi].need_refine) atomicOr(&B.qs[B.qrep[qi]].grp_refine, 1);
     for (int m = 0; m < Q.nbase; ++m) {
         MState& ms = B.ms[Q.mslot_off + m];
         if (!ms.want) continue;
@@ -1042,7 +1044,7 @@ void launch_bottleneck(const BatchDev& B, cudaStream_t st) {
     cudaMemsetAsync(B.ckey, 0, ((size_t)B.cmask + 1) * sizeof(unsigned long long), st);
     cudaMemsetAsync(B.crep, 0x7f, ((size_t)B.cmask + 1) * sizeof(int32_t), st);
     if (B.nq) {
-        k_bottleneck<<<blocks(B.nq, 128), 128, 0, st>>>(B);
+        k_bottleneck<<<dim3((unsigned)blocks(B.nq, 128), (unsigned)std::min(B.max_nbase, 65535)), 128, 0, st>>>(B);
         k_coarse_queue<<<blocks(B.nq, 128), 128, 0, st>>>(B);
     }
 }
