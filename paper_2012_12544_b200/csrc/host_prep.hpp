@@ -419,7 +419,7 @@ inline void build_chunk(QAt& qat, int i0, int i1, const HostNets& HN, const Host
 // query's error.
 template <class QAt>
 inline bool build_batch_at(QAt&& qat, int nq, const HostNets& HN, const HostCls& HC, HostBatch& HB,
-                           std::string& err) {
+                           std::string& err, int chunk = 8192) {
     // reuse the vectors' capacity across calls (a sweep is re-prepared per step)
     HB.q.resize(nq);
     // per network, the smallest type id without a profile: a chain prefix
@@ -431,8 +431,8 @@ inline bool build_batch_at(QAt&& qat, int nq, const HostNets& HN, const HostCls&
         while (t < HN.desc[n].T && HN.type_ok[HN.desc[n].off_tflag + t]) ++t;
         first_bad_type[n] = t;
     }
-    constexpr int CHUNK = 8192;
-    const int nch = std::max(1, (nq + CHUNK - 1) / CHUNK);
+    const int CHUNK = std::max(1, chunk);
+    const int nch = std::max(1, (int)(((int64_t)nq + CHUNK - 1) / CHUNK));
     // (the calling thread's chunk records, reached through a plain pointer:
     // a thread_local named inside the lambda would be each worker's own)
     static thread_local std::vector<BuildChunk> chunk_store;
@@ -440,7 +440,8 @@ inline bool build_batch_at(QAt&& qat, int nq, const HostNets& HN, const HostCls&
     BuildChunk* const chunks = chunk_store.data();
     QDesc* qd = HB.q.data();
     host_parallel_for(nch, [&](int k) {
-        build_chunk(qat, k * CHUNK, std::min(nq, (k + 1) * CHUNK), HN, HC, first_bad_type, qd, chunks[k]);
+        build_chunk(qat, k * CHUNK, (int)std::min<int64_t>(nq, (int64_t)(k + 1) * CHUNK), HN, HC, first_bad_type, qd,
+                    chunks[k]);
     });
     for (int k = 0; k < nch; ++k)
         if (chunks[k].err_i >= 0) {
@@ -473,7 +474,7 @@ inline bool build_batch_at(QAt&& qat, int nq, const HostNets& HN, const HostCls&
     if (nch > 1)
         host_parallel_for(nch - 1, [&](int k1) {
             const int k = k1 + 1;
-            for (int i = k * CHUNK, e = std::min(nq, (k + 1) * CHUNK); i < e; ++i) {
+            for (int i = k * CHUNK, e = (int)std::min<int64_t>(nq, (int64_t)(k + 1) * CHUNK); i < e; ++i) {
                 QDesc& Q = qd[i];
                 Q.cand_off += bc[k];
                 Q.stage_off += bs[k];
@@ -490,8 +491,8 @@ inline bool build_batch_at(QAt&& qat, int nq, const HostNets& HN, const HostCls&
 }
 
 inline bool build_batch(const bp_query* qs, int nq, const HostNets& HN, const HostCls& HC, HostBatch& HB,
-                        std::string& err) {
-    return build_batch_at([qs](int i) -> const bp_query& { return qs[i]; }, nq, HN, HC, HB, err);
+                        std::string& err, int chunk = 8192) {
+    return build_batch_at([qs](int i) -> const bp_query& { return qs[i]; }, nq, HN, HC, HB, err, chunk);
 }
 
 }  // namespace bpk
