@@ -129,7 +129,13 @@ struct bp_ctx {
     bool have_nets = false, have_cls = false;
     uint64_t gen = 0;        // bumped by every bp_set_networks / bp_set_clusters
     DevBuf nets_mem, cls_mem;
-    HostPinned stage_tables;   // pinned staging of the network / cluster tables
+    HostPinned stage_tables;   // pinned staging of the network tables
+    HostPinned stage_cls;      // ... and of the cluster tables
+    // table uploads run on their own stream and end with tables_ev: the set_*
+    // calls return without waiting, and every consumer of the device tables
+    // (a batch run, a timeline call) orders itself after the event
+    cudaStream_t tstream = nullptr;
+    cudaEvent_t tables_ev = nullptr;
     Pools P{};
     int max_T = 1;
     size_t smem_optin = 227 * 1024;   // cudaDeviceProp::sharedMemPerBlockOptin
@@ -253,6 +259,8 @@ int upload_networks(bp_ctx* c) {
     size_t o_Pw = L.take<int64_t>(H.n_pref);
     size_t o_tok = L.take<uint8_t>(H.type_ok.size());
     if (!c->nets_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(networks)");
+    // the previous upload's copies have read the staging buffers
+    cudaEventSynchronize(c->tables_ev);
     if (!c->stage_tables.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(tables)");
     void* b = c->nets_mem.p;
     // through pinned staging (one DMA per table, no pageable bounce)
@@ -261,7 +269,7 @@ int upload_networks(bp_ctx* c) {
         if (!bytes) return cudaSuccess;
         std::memcpy(static_cast<char*>(c->stage_tables.p) + off, src, bytes);
         return cudaMemcpyAsync(dptr<char>(b, off), static_cast<char*>(c->stage_tables.p) + off, bytes,
-                               cudaMemcpyHostToDevice, 0);
+                               cudaMemcpyHostToDevice, c->tstream);
     };
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(NetDesc));
@@ -287,13 +295,17 @@ int upload_networks(bp_ctx* c) {
     c->max_T = std::max(1, H.max_T);
     // K1 cost_prefix on the device
     if (!H.desc.empty()) {
-        timed(c, "cost_prefix", 0, [&] {
+        timed(c, "cost_prefix", c->tstream, [&] {
             launch_cost_prefix(P.nets, (int)H.desc.size(), P.fp, P.bp, P.w, const_cast<int64_t*>(P.Pfp),
                                const_cast<int64_t*>(P.Pbp), const_cast<int64_t*>(P.Pc), const_cast<int64_t*>(P.Pw),
-                               0, c->max_T);
+                               c->tstream, c->max_T);
         });
-        e = cudaDeviceSynchronize();
-        if (e != cudaSuccess) return cuda_fail(c, e, "cost_prefix");
+    }
+    e = cudaEventRecord(c->tables_ev, c->tstream);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(c, e, "cost_prefix");
+    if (c->prof) {
+        cudaStreamSynchronize(c->tstream);
         collect(c);
     }
     return BP_OK;
@@ -308,21 +320,22 @@ int upload_clusters(bp_ctx* c) {
     size_t o_mm = L.take<int64_t>(H.minm.size());
     size_t o_bw = L.take<int64_t>(H.bw.size());
     if (!c->cls_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(clusters)");
-    if (!c->stage_tables.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(tables)");
+    cudaEventSynchronize(c->tables_ev);   // the previous upload has read the staging buffers
+    if (!c->stage_cls.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(tables)");
     void* b = c->cls_mem.p;
     auto up = [&](size_t off, const void* src, size_t bytes) {
         c->h2d += (int64_t)bytes;
         if (!bytes) return cudaSuccess;
-        std::memcpy(static_cast<char*>(c->stage_tables.p) + off, src, bytes);
-        return cudaMemcpyAsync(dptr<char>(b, off), static_cast<char*>(c->stage_tables.p) + off, bytes,
-                               cudaMemcpyHostToDevice, 0);
+        std::memcpy(static_cast<char*>(c->stage_cls.p) + off, src, bytes);
+        return cudaMemcpyAsync(dptr<char>(b, off), static_cast<char*>(c->stage_cls.p) + off, bytes,
+                               cudaMemcpyHostToDevice, c->tstream);
     };
     cudaError_t e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(ClDesc));
     if (e == cudaSuccess) e = up(o_t, H.ctype.data(), H.ctype.size() * 4);
     if (e == cudaSuccess) e = up(o_cap, H.cap.data(), H.cap.size() * 8);
     if (e == cudaSuccess) e = up(o_mm, H.minm.data(), H.minm.size() * 8);
     if (e == cudaSuccess) e = up(o_bw, H.bw.data(), H.bw.size() * 8);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(0);   // the staging buffer is reused
+    if (e == cudaSuccess) e = cudaEventRecord(c->tables_ev, c->tstream);
     if (e != cudaSuccess) return cuda_fail(c, e, "upload clusters");
     c->P.cls = dptr<ClDesc>(b, o_desc);
     c->P.ctype = dptr<int32_t>(b, o_t);
@@ -698,6 +711,7 @@ GraphKey graph_key(bp_ctx* c, bp_batch* B) {
 
 int run_graph(bp_ctx* c, bp_batch* B, cudaStream_t st) {
     static const bool off = getenv("BP_NO_GRAPHS") != nullptr;
+    cudaStreamWaitEvent(st, c->tables_ev, 0);   // the device tables are uploaded
     if (c->prof || off || B->graph_failed) return run(c, B, st);
     set_run_flags(c, B->dev);
     ensure_streams(B);
@@ -1092,6 +1106,12 @@ bp_ctx* bp_create(int device) {
     if (!c) return nullptr;
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
+    if (cudaStreamCreateWithFlags(&c->tstream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->tables_ev, cudaEventDisableTiming) != cudaSuccess) {
+        g_err = "cannot create the table upload stream";
+        delete c;
+        return nullptr;
+    }
     c->smem_optin = (size_t)prop.sharedMemPerBlockOptin;
     return c;
 }
@@ -1104,6 +1124,9 @@ void bp_destroy(bp_ctx* c) {
     c->nets_mem.release();
     c->cls_mem.release();
     c->stage_tables.release();
+    c->stage_cls.release();
+    if (c->tstream) cudaStreamDestroy(c->tstream);
+    if (c->tables_ev) cudaEventDestroy(c->tables_ev);
     for (auto e : c->event_pool) cudaEventDestroy(e);
     delete c;
 }
@@ -1309,6 +1332,7 @@ int bp_simulate_plan(bp_ctx* c, const bp_plan_request* q, bp_timeline_result* re
     if (rc != BP_OK) return rc;
     if (!res) return fail(c, BP_BAD_INPUT, "null result");
     if (q->mini_batches < 1) return fail(c, BP_BAD_INPUT, "mini_batches >= 1 required");
+    cudaEventSynchronize(c->tables_ev);
     const cudaError_t e = timeline_simulate(c->P, c->hc.desc[(size_t)q->cluster].N, *q, res, events, cap, highwater,
                                             weight_static, busy, &c->h2d, &c->d2h);
     c->launches += 2;
@@ -1324,6 +1348,7 @@ int bp_estimate_plan(bp_ctx* c, const bp_plan_request* q, bp_estimate_result* re
     if (!res) return fail(c, BP_BAD_INPUT, "null result");
     if (q->n_stages > c->hc.desc[(size_t)q->cluster].N)
         return fail(c, BP_BAD_INPUT, "plan longer than the cluster");
+    cudaEventSynchronize(c->tables_ev);
     const cudaError_t e = timeline_estimate(c->P, c->hc.desc[(size_t)q->cluster].N, *q, res, stages, mem_infeasible,
                                             &c->h2d, &c->d2h);
     c->launches += 1;
