@@ -213,7 +213,10 @@ void bp_destroy(bp_ctx* ctx);
 const char* bp_last_error(const bp_ctx* ctx);   /* ctx may be NULL */
 int bp_abi_version(void);
 
-/* Upload (replace) the network / cluster tables.  Arrays are copied. */
+/* Upload (replace) the network / cluster tables.  Arrays are copied before
+ * the call returns; the device copy completes asynchronously, after every run
+ * this context enqueued before the call and before any run enqueued after it
+ * (and before a bp_simulate_plan / bp_estimate_plan reads the tables). */
 int bp_set_networks(bp_ctx* ctx, const bp_network* nets, int n);
 int bp_set_clusters(bp_ctx* ctx, const bp_cluster* cls, int n);
 

@@ -136,6 +136,11 @@ struct bp_ctx {
     // (a batch run, a timeline call) orders itself after the event
     cudaStream_t tstream = nullptr;
     cudaEvent_t tables_ev = nullptr;
+    cudaEvent_t nets_ev = nullptr, cls_ev = nullptr;   // each staging buffer's last copy
+    // batch runs enqueued since the last table upload (an event on each
+    // caller stream): an upload's copies wait for them on the device, so
+    // that no run in flight reads a table while it is overwritten
+    std::vector<cudaEvent_t> runs;
     Pools P{};
     int max_T = 1;
     size_t smem_optin = 227 * 1024;   // cudaDeviceProp::sharedMemPerBlockOptin
@@ -173,6 +178,9 @@ cudaEvent_t get_event(bp_ctx* c) {
     cudaEventCreate(&e);
     return e;
 }
+
+void note_run(bp_ctx* c, cudaStream_t st);
+void tables_wait_runs(bp_ctx* c);
 
 // Launch wrapper: counts launches, brackets them with events when profiling.
 template <class F>
@@ -239,6 +247,28 @@ void collect(bp_ctx* c) {
     c->pending.clear();
 }
 
+void note_run(bp_ctx* c, cudaStream_t st) {
+    cudaEvent_t ev = get_event(c);
+    cudaEventRecord(ev, st);
+    c->runs.push_back(ev);
+    if (c->runs.size() > 64) {   // drop the finished ones
+        std::vector<cudaEvent_t> keep;
+        for (cudaEvent_t e : c->runs) {
+            if (cudaEventQuery(e) == cudaSuccess) c->event_pool.push_back(e);
+            else keep.push_back(e);
+        }
+        c->runs.swap(keep);
+    }
+}
+
+void tables_wait_runs(bp_ctx* c) {
+    for (cudaEvent_t e : c->runs) {
+        cudaStreamWaitEvent(c->tstream, e, 0);
+        c->event_pool.push_back(e);   // the wait is bound at this call: the event may be reused
+    }
+    c->runs.clear();
+}
+
 template <class T>
 T* dptr(void* base, size_t off) {
     return reinterpret_cast<T*>(reinterpret_cast<char*>(base) + off);
@@ -259,26 +289,31 @@ int upload_networks(bp_ctx* c) {
     size_t o_Pw = L.take<int64_t>(H.n_pref);
     size_t o_tok = L.take<uint8_t>(H.type_ok.size());
     if (!c->nets_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(networks)");
-    // the previous upload's copies have read the staging buffers
-    cudaEventSynchronize(c->tables_ev);
+    // the previous network upload's copies have read the staging buffer
+    cudaEventSynchronize(c->nets_ev);
     if (!c->stage_tables.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(tables)");
     void* b = c->nets_mem.p;
-    // through pinned staging (one DMA per table, no pageable bounce)
-    auto up = [&](size_t off, const void* src, size_t bytes) {
-        c->h2d += (int64_t)bytes;
-        if (!bytes) return cudaSuccess;
-        std::memcpy(static_cast<char*>(c->stage_tables.p) + off, src, bytes);
-        return cudaMemcpyAsync(dptr<char>(b, off), static_cast<char*>(c->stage_tables.p) + off, bytes,
-                               cudaMemcpyHostToDevice, c->tstream);
-    };
-    cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = up(o_desc, H.desc.data(), H.desc.size() * sizeof(NetDesc));
-    if (e == cudaSuccess) e = up(o_fp, H.fp.data(), H.fp.size() * 8);
-    if (e == cudaSuccess) e = up(o_bp, H.bp.data(), H.bp.size() * 8);
-    if (e == cudaSuccess) e = up(o_w, H.w.data(), H.w.size() * 8);
-    if (e == cudaSuccess) e = up(o_a, H.a.data(), H.a.size() * 8);
-    if (e == cudaSuccess) e = up(o_as, H.asort.data(), H.asort.size() * 8);
-    if (e == cudaSuccess) e = up(o_tok, H.type_ok.data(), H.type_ok.size());
+    // through pinned staging, laid out as on the device: the tables are
+    // staged in 256 KB pieces on the host pool, then copied in two DMAs (the
+    // prefix tables between them are the device's own, k_cost_prefix)
+    char* stg = static_cast<char*>(c->stage_tables.p);
+    struct Piece { size_t off; const void* src; size_t bytes; };
+    const Piece tabs[] = {{o_desc, H.desc.data(), H.desc.size() * sizeof(NetDesc)}, {o_fp, H.fp.data(), H.fp.size() * 8},
+                          {o_bp, H.bp.data(), H.bp.size() * 8},   {o_w, H.w.data(), H.w.size() * 8},
+                          {o_a, H.a.data(), H.a.size() * 8},      {o_as, H.asort.data(), H.asort.size() * 8},
+                          {o_tok, H.type_ok.data(), H.type_ok.size()}};
+    std::vector<Piece> pieces;
+    const size_t PIECE = 256 * 1024;
+    for (const Piece& t : tabs) {
+        c->h2d += (int64_t)t.bytes;
+        for (size_t a = 0; a < t.bytes; a += PIECE)
+            pieces.push_back({t.off + a, static_cast<const char*>(t.src) + a, std::min(PIECE, t.bytes - a)});
+    }
+    host_parallel_for((int)pieces.size(), [&](int k) { std::memcpy(stg + pieces[k].off, pieces[k].src, pieces[k].bytes); });
+    cudaError_t e = cudaMemcpyAsync(b, stg, o_Pfp, cudaMemcpyHostToDevice, c->tstream);
+    if (e == cudaSuccess && H.type_ok.size())
+        e = cudaMemcpyAsync(dptr<char>(b, o_tok), stg + o_tok, H.type_ok.size(), cudaMemcpyHostToDevice, c->tstream);
+    if (e == cudaSuccess) e = cudaEventRecord(c->nets_ev, c->tstream);
     if (e != cudaSuccess) return cuda_fail(c, e, "upload networks");
     Pools& P = c->P;
     P.nets = dptr<NetDesc>(b, o_desc);
@@ -320,7 +355,7 @@ int upload_clusters(bp_ctx* c) {
     size_t o_mm = L.take<int64_t>(H.minm.size());
     size_t o_bw = L.take<int64_t>(H.bw.size());
     if (!c->cls_mem.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaMalloc(clusters)");
-    cudaEventSynchronize(c->tables_ev);   // the previous upload has read the staging buffers
+    cudaEventSynchronize(c->cls_ev);   // the previous cluster upload has read the staging buffer
     if (!c->stage_cls.ensure(L.off)) return fail(c, BP_OUT_OF_MEMORY, "cudaHostAlloc(tables)");
     void* b = c->cls_mem.p;
     auto up = [&](size_t off, const void* src, size_t bytes) {
@@ -335,6 +370,7 @@ int upload_clusters(bp_ctx* c) {
     if (e == cudaSuccess) e = up(o_cap, H.cap.data(), H.cap.size() * 8);
     if (e == cudaSuccess) e = up(o_mm, H.minm.data(), H.minm.size() * 8);
     if (e == cudaSuccess) e = up(o_bw, H.bw.data(), H.bw.size() * 8);
+    if (e == cudaSuccess) e = cudaEventRecord(c->cls_ev, c->tstream);
     if (e == cudaSuccess) e = cudaEventRecord(c->tables_ev, c->tstream);
     if (e != cudaSuccess) return cuda_fail(c, e, "upload clusters");
     c->P.cls = dptr<ClDesc>(b, o_desc);
@@ -924,6 +960,7 @@ int prepare_any(bp_ctx* c, bp_batch* B, const bp_query* q, int nq, int details, 
             if (timing) fprintf(stderr, "split part %zu launched %.2f ms\n", k, since());
         }
     }
+    if (eager) note_run(c, st);
     for (size_t k = 0; k < B->parts.size(); ++k)
         for (int32_t i : B->part_q[k]) B->part_ids_host.push_back(i);
     // the whole batch's layout, in the caller's query order, from the parts'
@@ -981,7 +1018,11 @@ int upload_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
 }
 
 int run_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
-    if (B->parts.empty()) return run_graph(c, B, st);
+    if (B->parts.empty()) {
+        const int rc = run_graph(c, B, st);
+        if (rc == BP_OK) note_run(c, st);
+        return rc;
+    }
     if (!B->fork) cudaEventCreateWithFlags(&B->fork, cudaEventDisableTiming);
     cudaEventRecord(B->fork, st);
     for (size_t k = 0; k < B->parts.size(); ++k) {
@@ -992,6 +1033,7 @@ int run_any(bp_ctx* c, bp_batch* B, cudaStream_t st) {
         cudaEventRecord(p->done, p->lane);
         cudaStreamWaitEvent(st, p->done, 0);
     }
+    note_run(c, st);
     return BP_OK;
 }
 
@@ -1107,7 +1149,9 @@ bp_ctx* bp_create(int device) {
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
     if (cudaStreamCreateWithFlags(&c->tstream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&c->tables_ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&c->tables_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->nets_ev, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->cls_ev, cudaEventDisableTiming) != cudaSuccess) {
         g_err = "cannot create the table upload stream";
         delete c;
         return nullptr;
@@ -1126,7 +1170,8 @@ void bp_destroy(bp_ctx* c) {
     c->stage_tables.release();
     c->stage_cls.release();
     if (c->tstream) cudaStreamDestroy(c->tstream);
-    if (c->tables_ev) cudaEventDestroy(c->tables_ev);
+    for (cudaEvent_t ev : {c->tables_ev, c->nets_ev, c->cls_ev})
+        if (ev) cudaEventDestroy(ev);
     for (auto e : c->event_pool) cudaEventDestroy(e);
     delete c;
 }
@@ -1140,10 +1185,11 @@ int bp_set_networks(bp_ctx* c, const bp_network* nets, int n) {
         const auto t0 = std::chrono::steady_clock::now();
         // batches prepared before this call point at the old tables: they are
         // refused from now on (bp_batch_*: generation check), and whatever
-        // is still in flight on any stream finishes before the tables change
+        // run is still in flight finishes before the upload overwrites a table
+        // (the upload waits for the runs on the device, tables_wait_runs)
         ++c->gen;
         c->have_nets = false;
-        cudaDeviceSynchronize();
+        tables_wait_runs(c);
         if (!build_nets(nets, n, c->hn, err, false)) return fail(c, BP_BAD_INPUT, err);
         const auto t1 = std::chrono::steady_clock::now();
         int rc = upload_networks(c);
@@ -1167,7 +1213,7 @@ int bp_set_clusters(bp_ctx* c, const bp_cluster* cls, int n) {
         std::string err;
         ++c->gen;
         c->have_cls = false;
-        cudaDeviceSynchronize();
+        tables_wait_runs(c);
         if (!build_clusters(cls, n, c->hc, err)) return fail(c, BP_BAD_INPUT, err);
         int rc = upload_clusters(c);
         c->have_cls = rc == BP_OK;
