@@ -466,7 +466,7 @@ def run_b200(args):
     step_ms = [a.elapsed_time(b) for a, b in evs]
 
     # ---- per-kernel breakdown (CUDA events around every launch), on the same
-    # steps run as ONE batch (BP_OPT_SPLIT off): with the split, two parts run
+    # steps run as ONE batch (BP_OPT_SPLIT off): with the split, the parts run
     # concurrently and their kernel spans would overlap
     ex.split(False)
     kb = ex.prepare(p, details=False, stream=sp)
@@ -643,7 +643,7 @@ def run_b200(args):
             "refine_latency": refine_lat,
             "kernels": kern,
             "kernels_note": (f"per-kernel CUDA-event spans of the same steps run as one batch (BP_OPT_SPLIT off: "
-                             f"{kb_ms:.2f} ms per step); the headline runs the batch as two concurrent parts"),
+                             f"{kb_ms:.2f} ms per step); the headline runs the batch as concurrent parts by stage count"),
             "best": {"makespan": f"{int(best['makespan']['num'])}/{int(best['makespan']['den'])}",
                      "M": int(best["M"]), "kind": int(best["kind"]), "query_id": int(best["query_id"])},
             "query_status_hist": np.bincount(res["status"], minlength=7).tolist()}

@@ -273,11 +273,11 @@ enum { BP_OPT_DEDUP = 1, BP_OPT_PLAN_ONLY = 2, BP_OPT_PRUNE_LB = 3, BP_OPT_SPLIT
  *   BP_C_PRUNED_LB.  Every bp_query_result is byte-identical to the
  *   unpruned run (status, n_ranked, best, first_error and the best's
  *   values); only per-candidate records of pruned candidates differ. */
-/*   BP_OPT_SPLIT (default 1): a batch of at least 4096 queries runs as two
- *   concurrent parts -- the queries with the batch's largest stage count
- *   (the longest refine walks) and the rest -- on two streams.  A value
- *   k >= 2 asks for up to k parts (the k-1 largest stage counts, then the
- *   rest); 0 turns it off.  Results are identical either way. */
+/*   BP_OPT_SPLIT (default 1 = up to four parts): a batch of at least 4096
+ *   queries runs as concurrent parts on their own streams -- the queries of
+ *   each of the batch's largest stage counts (the longest refine walks), then
+ *   the rest; a part needs 512 queries.  A value k >= 2 asks for up to k
+ *   parts; 0 turns it off.  Results are identical either way. */
 int bp_set_option(bp_ctx* ctx, int option, int64_t value);
 
 /* ---- one plan: full-timeline simulate and estimate ----------------------

@@ -148,7 +148,7 @@ struct bp_ctx {
     bool dedup = true;       // BP_OPT_DEDUP
     bool plan_only = false;  // BP_OPT_PLAN_ONLY
     bool prune_lb = false;   // BP_OPT_PRUNE_LB
-    int split = 2;           // BP_OPT_SPLIT: parts per large batch (0 = off)
+    int split = 4;           // BP_OPT_SPLIT: parts per large batch (0 = off)
     std::map<std::string, KStat> stats;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
@@ -1320,6 +1320,12 @@ int bp_explore_batch(bp_ctx* c, const bp_query* q, int nq, bp_query_result* res,
         static const bool timing = getenv("BP_HOST_TIMING") != nullptr;   // diagnostics (stderr)
         auto now = [] { return std::chrono::steady_clock::now(); };
         const auto t0 = now();
+        cudaEvent_t te0 = nullptr, te1 = nullptr;   // diagnostics: the call's span on the caller's stream
+        if (timing) {
+            cudaEventCreate(&te0);
+            cudaEventCreate(&te1);
+            cudaEventRecord(te0, st);
+        }
         bool ran = false;
         int rc = prepare_any(c, B, q, nq, stages != nullptr, st, true, &ran);
         const auto t1 = now();
@@ -1329,8 +1335,14 @@ int bp_explore_batch(bp_ctx* c, const bp_query* q, int nq, bp_query_result* res,
         if (rc == BP_OK) rc = fetch_any(c, B, res, cand, stages, st);
         if (timing) {
             auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-            fprintf(stderr, "bp_explore_batch: prepare %.2f ms, launch %.2f ms, wait+fetch %.2f ms\n", ms(t0, t1),
-                    ms(t1, t2), ms(t2, now()));
+            cudaEventRecord(te1, st);
+            cudaEventSynchronize(te1);
+            float dev = 0;
+            cudaEventElapsedTime(&dev, te0, te1);
+            fprintf(stderr, "bp_explore_batch: prepare %.2f ms, launch %.2f ms, wait+fetch %.2f ms; caller-stream span %.2f ms\n",
+                    ms(t0, t1), ms(t1, t2), ms(t2, now()), dev);
+            cudaEventDestroy(te0);
+            cudaEventDestroy(te1);
         }
         return rc;
     } catch (const std::bad_alloc&) {
@@ -1353,7 +1365,7 @@ int bp_set_option(bp_ctx* c, int option, int64_t value) {
         case BP_OPT_DEDUP: c->dedup = value != 0; return BP_OK;
         case BP_OPT_PLAN_ONLY: c->plan_only = value != 0; return BP_OK;
         case BP_OPT_PRUNE_LB: c->prune_lb = value != 0; return BP_OK;
-        case BP_OPT_SPLIT: c->split = value <= 0 ? 0 : value == 1 ? 2 : (int)std::min<int64_t>(value, 8); return BP_OK;
+        case BP_OPT_SPLIT: c->split = value <= 0 ? 0 : value == 1 ? 4 : (int)std::min<int64_t>(value, 8); return BP_OK;
         default: return fail(c, BP_BAD_INPUT, "unknown option " + std::to_string(option));
     }
 }

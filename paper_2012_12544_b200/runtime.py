@@ -115,9 +115,9 @@ class Explorer:
             raise RuntimeError(self.lib.bp_last_error(self.ctx).decode())
 
     def split(self, on=True):
-        """BP_OPT_SPLIT: run large batches as two concurrent parts (default
-        on; an int k >= 2 asks for up to k parts; results are identical
-        either way)."""
+        """BP_OPT_SPLIT: run large batches as concurrent parts by stage count
+        (default on: up to four parts; an int k >= 2 asks for up to k;
+        results are identical either way)."""
         value = (1 if on else 0) if isinstance(on, bool) else int(on)
         rc = self.lib.bp_set_option(self.ctx, abi.BP_OPT_SPLIT, value)
         if rc != 0:

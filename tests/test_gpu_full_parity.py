@@ -67,12 +67,12 @@ def global_candidates(p, idx):
     return np.concatenate([np.arange(q["cand_offset"][i], q["cand_offset"][i] + p.n_candidates[i]) for i in idx])
 
 
-@pytest.mark.parametrize("dedup,split", [(True, True), (False, True), (True, False), (True, 4)],
-                         ids=["dedup_split", "no_dedup", "one_batch", "four_parts"])
+@pytest.mark.parametrize("dedup,split", [(True, True), (False, True), (True, False), (True, 2)],
+                         ids=["dedup_split", "no_dedup", "one_batch", "two_parts"])
 def test_c5_every_candidate_matches_reference(ex, c5, gold, dedup, split):
-    """BP_OPT_SPLIT on (the default: the N = 64 queries and the rest run as two
-    concurrent parts), off, and four parts (N = 64, 32, 24, the rest); batch
-    dedup on and off."""
+    """BP_OPT_SPLIT on (the default: the N = 64, 32 and 24 queries and the rest
+    run as four concurrent parts), off, and two parts (N = 64 and the rest);
+    batch dedup on and off."""
     ex.dedup(dedup)
     ex.split(split)
     try:

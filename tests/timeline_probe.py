@@ -1,5 +1,5 @@
 """Tool (not collected by pytest): the launch timeline of one C5 sweep as the
-headline runs it (BP_OPT_SPLIT on: two parts on their own streams).  Every
+headline runs it (BP_OPT_SPLIT on: the parts on their own streams).  Every
 launch is bracketed by CUDA events (profiling on) and BP_TIMELINE makes the
 library write each span's start / end relative to the first.  Prints the spans
 in start order and, per part stream, the busy intervals -- which phases of
