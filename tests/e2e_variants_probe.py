@@ -18,7 +18,7 @@ def v2():
     ex.explore(p, details=False, stream=sp.cuda_stream, out=out)
 r1, r2 = med(v1), med(v2)
 parts = {}
-for k in (3, 4):
+for k in (2, 6, 8):
     ex.split(k)
     parts[k] = (med(v1), med(v3b) if False else None)
     ex.split(True)
@@ -28,4 +28,4 @@ def v3():
 def v4():
     bb = ex.prepare(p, stream=sp.cuda_stream); ex.run(bb, stream=sp.cuda_stream); ex.fetch(bb, p, stream=sp.cuda_stream); ex.free(bb)
 print("load+explore %.2f  explore only %.2f  run only (resident) %.2f  prepare+run+fetch %.2f" % (r1, r2, med(v3), med(v4)))
-print("load+explore with 3 parts %.2f, 4 parts %.2f" % (parts[3][0], parts[4][0]))
+print("load+explore with 2 parts %.2f, 6 parts %.2f, 8 parts %.2f" % (parts[2][0], parts[6][0], parts[8][0]))

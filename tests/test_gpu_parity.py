@@ -192,3 +192,21 @@ def test_graph_replay_equals_launch_by_launch(ex):
     got_z = ex.explore(z, details=False)[0]
     assert got_z.tobytes() == want.tobytes()
     assert got_a.tobytes() != got_z.tobytes()
+
+
+def test_pinned_outputs_equal_pageable(ex):
+    """bp_explore_batch into page-locked caller buffers (bench.py's e2e legs):
+    the records equal those of pageable buffers, on a split-size C5 sample,
+    twice in a row (buffers reused).  (Writing each part's records straight
+    into the page-locked buffers from the scatter kernels, zero-copy, was
+    measured: no gain for the query records, 2x slower for the candidate
+    records -- fine-grained PCIe writes.)"""
+    p = W.subset(W.config_c5(models=8), np.arange(4096))
+    want = ex.explore(p, details="candidates")
+    out = p.alloc_outputs("candidates", pinned=True)
+    for _ in range(2):
+        out[0][:] = np.zeros(1, dtype=out[0].dtype)
+        out[1][:] = np.zeros(1, dtype=out[1].dtype)
+        got = ex.explore(p, details="candidates", out=out)
+        assert got[0].tobytes() == want[0].tobytes()
+        assert got[1].tobytes() == want[1].tobytes()
