@@ -578,8 +578,7 @@ int prepare_built(bp_ctx* c, bp_batch* B, int nq, int details, cudaStream_t) {
     if (per_sm > 8) per_sm = 8;
     B->dp_grid = c->sm_count * per_sm;
     B->dp_max_units = max_units;
-    B->refine_grid = refine_setup(std::max(1, hb.max_N), max_units, c->max_T, c->smem_optin, &B->refine_bytes,
-                                  &B->refine_warps);
+    B->refine_grid = refine_setup(std::max(1, hb.max_N), max_units, c->max_T, &B->refine_bytes, &B->refine_warps);
     return BP_OK;
 }
 

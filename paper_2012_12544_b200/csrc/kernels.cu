@@ -1101,33 +1101,16 @@ void launch_refine(const BatchDev& B, int sms, int fast_grid, int fast_warps, si
 // launch geometry of the slim refine kernel for a batch (0: not used, its
 // tables do not fit in shared memory); the dynamic shared memory attribute is
 // set once per device (kernel_attributes_init)
-int refine_setup(int max_N, int max_L, int max_T, size_t optin, size_t* fast_bytes, int* fast_warps) {
+int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes, int* fast_warps) {
     const size_t fb = refine_fast_bytes(max_N, max_L, max_T);
     *fast_bytes = 0;
-    *fast_warps = 1;
+    *fast_warps = 1;   // (the kernel takes several walking warps per block; one measured best)
     if (fb > 96 * 1024) return 0;
     int dev = 0, sms = 0, per_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    static const int excl = getenv("BP_REFINE_SMS") ? atoi(getenv("BP_REFINE_SMS")) : 0;
-    static const int ew = getenv("BP_REFINE_WARPS") ? atoi(getenv("BP_REFINE_WARPS")) : 8;
-    if (excl > 0) {
-        // exclusive SMs: blocks of several walking warps that take an SM's
-        // whole shared memory, so no other kernel's block shares their SMs
-        cudaFuncAttributes a;
-        cudaFuncGetAttributes(&a, k_refine_fast);
-        const size_t stride = (fb + 127) & ~(size_t)127;
-        const size_t dyn = optin - a.sharedSizeBytes;
-        int w = (int)std::min<size_t>((size_t)std::max(1, std::min(ew, 8)), dyn / stride);
-        if (w < 1) return 0;
-        *fast_warps = w;
-        *fast_bytes = dyn;
-        return std::min(excl, sms);
-    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_refine_fast, 32, fb);
     if (per_sm <= 0) return 0;
-    static const int cap = getenv("BP_REFINE_PER_SM") ? atoi(getenv("BP_REFINE_PER_SM")) : 0;
-    if (cap > 0 && per_sm > cap) per_sm = cap;
     *fast_bytes = fb;
     return sms * per_sm;
 }

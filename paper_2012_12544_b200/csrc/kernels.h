@@ -23,7 +23,7 @@ void launch_dedup_copy_refine(const BatchDev& B, cudaStream_t st);
 void launch_refine_list(const BatchDev& B, int fast_grid, cudaStream_t st);
 void launch_refine(const BatchDev& B, int sms, int fast_grid, int fast_warps, size_t fast_bytes, int max_L, int max_T,
                    cudaStream_t st);
-int refine_setup(int max_N, int max_L, int max_T, size_t optin, size_t* fast_bytes, int* fast_warps);
+int refine_setup(int max_N, int max_L, int max_T, size_t* fast_bytes, int* fast_warps);
 cudaError_t kernel_attributes_init(int optin_bytes);
 cudaError_t partition_attributes_init(int optin_bytes);
 size_t refine_region_bytes(int max_N);
