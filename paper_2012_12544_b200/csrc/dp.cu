@@ -103,7 +103,7 @@ __device__ void dp_bands(const DPSmem& S, const ChainView& c, int N, int U, int6
 __global__ void __launch_bounds__(DP_THREADS) k_partition(BatchDev B, int which, int max_units, int max_N, int T_slots) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int64_t s_red[DP_THREADS / 32];
-    __shared__ int32_t s_U, s_slot_of_type_n;
+    __shared__ int32_t s_U;
     __shared__ int64_t s_T, s_F;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n_items = B.dp_count[which];

@@ -56,7 +56,7 @@ BPK_HDNI void setup_query(const BatchDev& B, int qi, int lane = 0, int nlanes = 
         cd.rank = -1;
         cd.n_stages = Q.N;
         // (`bapipe plan` calls balance_partition with no min-micro filter)
-        cd.status = (B.plan_only || Q.mini / cd.M >= min_micro) ? C_PENDING : BP_C_REJ_MIN_MICRO;
+        cd.status = (B.plan_only || Q.mini / cd.M >= min_micro) ? (int32_t)C_PENDING : (int32_t)BP_C_REJ_MIN_MICRO;
         B.cand[ci] = cd;
         B.cs[ci] = CState{};
         B.cq[ci] = qi;
@@ -146,7 +146,6 @@ BPK_HD void refine_commit(const BatchDev& B, int qi, const NetView& v, const Cha
 // (shared memory in k_refine_smem)
 BPK_HDNI void refine_query_at(const BatchDev& B, int qi, const RefineScratch* sc, const NetView* vo = nullptr) {
     const QDesc Q = B.q[qi];
-    QState& qs = B.qs[qi];
     if (!refine_wanted(B, qi)) return;
     NetView v = vo ? *vo : net_view(B.P, Q.net);
     ChainView c = chain_view(B.P, Q.cl, Q.N);

@@ -496,7 +496,6 @@ __global__ void __launch_bounds__(SIM_THREADS) k_sim_fast(BatchDev B, int cls) {
         mk = Rat{X / (int64_t)g, D / (int64_t)g};
 #pragma unroll
         for (int i = 0; i < S; ++i) {
-            const int s = r * S + i;
             if (!has[i]) continue;
             // feature high-water: min(M, depth) * a (219-238)
             if ((i128)wv[i] * A[i] > (i128)INT64_MAX) e.set(ERR_OVERFLOW);
