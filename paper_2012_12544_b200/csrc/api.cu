@@ -141,6 +141,7 @@ struct bp_ctx {
     // caller stream): an upload's copies wait for them on the device, so
     // that no run in flight reads a table while it is overwritten
     std::vector<cudaEvent_t> runs;
+    cudaEvent_t tl_base = nullptr;   // diagnostics (BP_TIMELINE): recorded at each profiled run's start
     Pools P{};
     int max_T = 1;
     size_t smem_optin = 227 * 1024;   // cudaDeviceProp::sharedMemPerBlockOptin
@@ -221,7 +222,7 @@ void collect(bp_ctx* c) {
     static const char* tl = getenv("BP_TIMELINE");
     if (tl && !c->pending.empty()) {
         if (FILE* f = fopen(tl, "a")) {
-            cudaEvent_t base = c->pending.front().second.first;
+            cudaEvent_t base = c->tl_base ? c->tl_base : c->pending.front().second.first;
             cudaEventSynchronize(c->pending.back().second.second);
             for (auto& p : c->pending) {
                 float a = 0, b = 0;
@@ -1169,7 +1170,7 @@ void bp_destroy(bp_ctx* c) {
     c->stage_tables.release();
     c->stage_cls.release();
     if (c->tstream) cudaStreamDestroy(c->tstream);
-    for (cudaEvent_t ev : {c->tables_ev, c->nets_ev, c->cls_ev})
+    for (cudaEvent_t ev : {c->tables_ev, c->nets_ev, c->cls_ev, c->tl_base})
         if (ev) cudaEventDestroy(ev);
     for (auto e : c->event_pool) cudaEventDestroy(e);
     delete c;
@@ -1265,10 +1266,17 @@ bp_batch* bp_batch_prepare(bp_ctx* c, const bp_query* q, int nq, int want_detail
 static bool stale(const bp_ctx* c, const bp_batch* B) { return B->gen != c->gen; }
 static const char* STALE = "batch prepared before the last bp_set_networks / bp_set_clusters: prepare it again";
 
+static void mark_run_start(bp_ctx* c, cudaStream_t st) {
+    if (!c->prof) return;
+    if (!c->tl_base) cudaEventCreate(&c->tl_base);
+    cudaEventRecord(c->tl_base, st);
+}
+
 int bp_batch_run(bp_ctx* c, bp_batch* B, void* stream) {
     if (!c || !B) return fail(c, BP_BAD_INPUT, "bad arguments");
     if (stale(c, B)) return fail(c, BP_BAD_INPUT, STALE);
     cudaSetDevice(c->device);
+    mark_run_start(c, (cudaStream_t)stream);
     return run_any(c, B, (cudaStream_t)stream);
 }
 
@@ -1326,6 +1334,7 @@ int bp_explore_batch(bp_ctx* c, const bp_query* q, int nq, bp_query_result* res,
             cudaEventRecord(te0, st);
         }
         bool ran = false;
+        mark_run_start(c, st);
         int rc = prepare_any(c, B, q, nq, stages != nullptr, st, true, &ran);
         const auto t1 = now();
         if (rc == BP_OK && !ran) rc = upload_any(c, B, st);
